@@ -1,0 +1,185 @@
+/*
+ * gs_sched.h — C ABI of the B200 candidate-scoring path.
+ *
+ * The reference (`gpusched`, pure Python + NumPy) has no FFI; its drop-in
+ * boundary is the Python seam around `CostEvaluator` and `_cut`
+ * (reference pkg/src/gpusched/search.py:90-124, 168-201).  Each entry point
+ * below replaces one reference interface on that seam; the Python mirror in
+ * paper_2012_07145_b200/ binds them with ctypes.
+ *
+ * Conventions: all array arguments are DEVICE pointers owned by the caller
+ * unless named `host_*`; every call is stream-ordered on `stream`
+ * (cudaStream_t passed as void*) and never synchronizes unless stated; the
+ * return value is 0 on success or a negative GS_ERR_* code with a message
+ * retrievable by gs_last_error().  Handles are immutable after creation
+ * except gs_set_weights, and distinct handles are thread-safe.
+ */
+#ifndef GS_SCHED_H
+#define GS_SCHED_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_MAX_NDIM 4
+#define GS_NUM_FEATURES 56
+#define GS_ALGO_DIM 10
+#define GS_NUM_COEFFS 30
+
+enum {
+  GS_OK = 0,
+  GS_ERR_ARG = -1,        /* bad argument / unsupported configuration     */
+  GS_ERR_CUDA = -2,       /* CUDA runtime error                            */
+  GS_ERR_CAPACITY = -3,   /* a candidate exceeded a workspace capacity     */
+  GS_ERR_SCHEDULE = -4    /* a decision log is structurally illegal        */
+};
+
+/* Placement kinds (reference loopnest.py:23, PLACEMENT_KINDS order). */
+enum { GS_ROOT = 0, GS_FUSE_BLOCK = 1, GS_FUSE_THREAD = 2, GS_INLINE = 3 };
+
+/* Prune verdicts (reference options.py:48-50 PruneReport.REASONS order + 1). */
+enum {
+  GS_VALID = 0, GS_PRUNE_RECOMPUTE = 1, GS_PRUNE_IDLE_SMS = 2, GS_PRUNE_WARP_UTIL = 3,
+  GS_PRUNE_SERIAL = 4, GS_PRUNE_THREAD_ALLOC = 5, GS_PRUNE_HW_LIMIT = 6
+};
+
+/* ---- candidate-independent pipeline descriptor (reference pipeline.py:25-173) */
+typedef struct {
+  int32_t ndim;
+  int32_t extent[GS_MAX_NDIM];
+  int32_t elem_bytes;
+  int32_t is_external;
+  int32_t is_output;
+  int32_t n_stages;
+  int32_t stage_begin;   /* first global stage index */
+  int32_t name_rank;     /* rank in Python str order (hash canonical order) */
+  int32_t pad;
+} GsFunc;                /* 48 bytes */
+
+typedef struct {
+  int32_t func;
+  int32_t n_access;
+  int32_t access_begin;
+  int32_t branching;     /* Strahler number (featurize.py:306-309) */
+} GsStage;               /* 16 bytes */
+
+typedef struct {
+  int32_t producer;
+  int32_t consumer;
+  int32_t stage;         /* global stage index of the reading stage */
+  int32_t window;        /* window volume (product of hi-lo+1) */
+  int32_t s[GS_MAX_NDIM], lo[GS_MAX_NDIM], hi[GS_MAX_NDIM];
+} GsAccess;              /* 64 bytes */
+
+typedef struct {         /* reference machine.py:14-33 */
+  int32_t warp_size, num_sms, max_threads_per_block, max_active_warps_per_sm,
+          max_active_blocks_per_sm, shared_mem_per_block_limit, shared_mem_per_sm,
+          global_transaction_bytes, shared_banks, bank_width_bytes;
+} GsMachine;
+
+typedef struct {         /* reference options.py:60-68 */
+  double recompute_factor, min_blocks_per_sm_factor, warp_utilization_floor;
+  int64_t unroll_budget, thread_alloc_bytes;
+} GsThresholds;
+
+typedef struct {
+  int32_t n_funcs, n_stages, n_access;
+  const GsFunc* funcs;           /* host pointers; copied at creation */
+  const GsStage* stages;
+  const GsAccess* access;
+  const double* algo;            /* [n_stages][10] algorithm features */
+  const uint8_t* name_repr;      /* concatenated Python repr() bytes of names */
+  const int32_t* name_off;       /* [n_funcs + 1] offsets into name_repr */
+  GsMachine machine;
+  GsThresholds thresholds;
+} GsPipelineDesc;
+
+/* ---- one decision record, 16 bytes (reference loopnest.py:34-48) ------- */
+typedef struct {
+  uint16_t func;                 /* 0xFFFF = padding (end of log) */
+  uint16_t consumer;             /* 0xFFFF = None */
+  uint8_t kind;                  /* GS_ROOT .. GS_INLINE */
+  uint8_t flags;                 /* bit0: serial present, bit1: thread present */
+  uint8_t serial[GS_MAX_NDIM];
+  uint8_t thread[GS_MAX_NDIM];
+  uint16_t pad;
+} GsDecision;
+
+typedef struct GsPipeline* gs_pipeline_t;
+
+const char* gs_last_error(void);
+int gs_version(void);
+
+/* Pack + upload a pipeline; replaces the per-call `PipelineGraph` walk of
+ * featurize.py:275-303 / resolve.py:207-226. */
+int gs_pipeline_create(const GsPipelineDesc* desc, gs_pipeline_t* out);
+int gs_pipeline_destroy(gs_pipeline_t p);
+int gs_pipeline_max_rows(gs_pipeline_t p);
+
+/* Upload coefficient-network weights (fp64 host arrays, reference tensor
+ * names/shapes costmodel.py:183-220); call again whenever the Python-side
+ * `evaluator.weights` object changes (driver.py:110, 219). Synchronous. */
+int gs_set_weights(gs_pipeline_t p, int embed_dim, int hidden_dim,
+                   const double* algo_w, const double* algo_b,
+                   const double* sched_w, const double* sched_b,
+                   const double* head_w, const double* head_b,
+                   const double* out_w, const double* out_b);
+
+/* K1: resolve + featurize + prune for N candidates (decision logs of
+ * stride S).  Replaces featurize() (featurize.py:275-303) and prune()
+ * (options.py:200-255).  Outputs, per candidate c and row r < n_rows[c]:
+ * feats[(c*R + r)*56 + k] (fp64, FEATURE_ORDER), row_key[c*R + r] =
+ * func << 8 | stage, verdict[c].  R = gs_pipeline_max_rows(). */
+int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
+                 double* feats, int32_t* row_key, int32_t* n_rows,
+                 uint8_t* verdict, void* stream);
+
+/* K2: basis + two-tower network + g.c + h + in-order stage sum.  Replaces
+ * CostEvaluator.cost (search.py:115-124).  row_cost/basis_gh optional
+ * (NULL = not written; basis_gh is [c*R + r][31] = g[30], h). */
+int gs_cost(gs_pipeline_t p, const double* feats, const int32_t* row_key,
+            const int32_t* n_rows, int64_t n, double* total, double* row_cost,
+            double* basis_gh, void* stream);
+
+/* K3: blake2b-64 structural hash at `depth` (loopnest.py:131-165). */
+int gs_struct_hash(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
+                   int depth, uint64_t* out, void* stream);
+
+/* K4: bucket by hash + hierarchical-sampling representatives
+ * (sampling.py:45-59, search.py:127-165).  `valid[i]` = verdict==0.
+ * Writes rep candidate indices in (hash asc, permutation position) order to
+ * rep_idx and their count to *n_reps (device int64), and the drawn
+ * rejects (in draw order, for PruneReports) to rej_idx (nullable) and
+ * their count to *n_rejects (device int64).  Needs a workspace of
+ * gs_select_workspace_bytes(n) bytes. */
+int64_t gs_select_workspace_bytes(int64_t n);
+int gs_select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n,
+                   uint64_t phase_seed, void* workspace, int64_t ws_bytes,
+                   int64_t* rep_idx, int64_t* n_reps, int64_t* rej_idx,
+                   int64_t* n_rejects, void* stream);
+
+/* K5: beam cut (search.py:76-87, 168-201): penalty for flagged hashes,
+ * optional Gumbel(T) on log-cost, stable radix top-k.  keys: unpenalized
+ * totals of the reps (rep order); pass_hash: hash at pass depth per rep;
+ * flagged: sorted array of flagged hashes at that depth.  Writes the first
+ * k rep positions (ascending key, ties by rep order) to out_pos and the
+ * count to *n_out (k <= 2048).  bottom (nullable) gets 1 for reps in the
+ * bottom half by unpenalized cost (stable), the memo-flag set of
+ * search.py:196-200.  Workspace: gs_topk_workspace_bytes(n). */
+int64_t gs_topk_workspace_bytes(int64_t n);
+int gs_beam_topk(const double* costs, const uint64_t* pass_hash, int64_t n,
+                 const uint64_t* flagged, int64_t n_flagged, double penalty,
+                 double temperature, uint64_t phase_seed, int64_t k,
+                 void* workspace, int64_t ws_bytes, int64_t* out_pos,
+                 int64_t* n_out, uint8_t* bottom, void* stream);
+
+/* Device-side error word of the last K1 launch (capacity overflow etc.);
+ * synchronizes `stream`. */
+int gs_check(gs_pipeline_t p, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GS_SCHED_H */

@@ -1,0 +1,249 @@
+// extern "C" entry points of libgs_sched.so (declared in include/gs_sched.h).
+#include "gs_internal.cuh"
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <algorithm>
+
+namespace gs {
+Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rcap, int pcap, int nwarps);
+int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
+                     double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, const Layout& L,
+                     int nwarps, int grid, int* gerr, cudaStream_t st);
+int featurize_occupancy(int nd, int nwarps, int smem);
+int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st);
+int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
+                const int32_t* n_rows, int64_t n, int R, double* total, double* row_cost, double* basis_gh,
+                int num_sms, cudaStream_t st);
+int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, const int32_t* sorted_funcs,
+                const uint8_t* names, const int32_t* name_off, uint64_t* out, cudaStream_t st);
+int64_t select_workspace_bytes(int64_t n);
+int select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, uint64_t phase_seed, void* ws,
+                int64_t ws_bytes, int64_t* rep_idx, int64_t* n_reps, int64_t* n_rejects, int64_t* rej_idx,
+                cudaStream_t st);
+int64_t topk_workspace_bytes(int64_t n);
+int beam_topk(const double* costs, const uint64_t* ph, int64_t n, const uint64_t* flagged, int64_t nflag,
+              double penalty, double temperature, uint64_t phase_seed, int64_t k, void* ws, int64_t ws_bytes,
+              int64_t* out_pos, int64_t* n_out, uint8_t* bottom, cudaStream_t st);
+}  // namespace gs
+
+using namespace gs;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess) return fail(GS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct GsPipeline {
+  PipeDev host{};
+  PipeDev* dev = nullptr;
+  uint8_t* blob = nullptr;
+  int32_t* stage_of_func = nullptr;
+  double* algo = nullptr;
+  int32_t* sorted = nullptr;
+  uint8_t* names = nullptr;
+  int32_t* name_off = nullptr;
+  int* err = nullptr;
+  NetDev net{};
+  std::vector<double*> wbufs;
+  int num_sms = 0;
+  int max_smem = 0;
+  int rcap = 0, pcap = 0;
+};
+
+extern "C" {
+
+const char* gs_last_error(void) { return g_err.c_str(); }
+int gs_version(void) { return 1; }
+
+int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
+  if (!d || !out || d->n_funcs <= 0 || d->n_funcs > 0x7FFF || d->n_stages < 0 || d->n_access < 0)
+    return fail(GS_ERR_ARG, "bad pipeline descriptor");
+  if (d->machine.warp_size != 32) return fail(GS_ERR_ARG, "only warp_size == 32 is supported");
+  const int Mg = d->machine.global_transaction_bytes, Ms = d->machine.shared_banks * d->machine.bank_width_bytes;
+  if (Mg < 1 || Mg > kMaxM || Ms < 1 || Ms > kMaxM)
+    return fail(GS_ERR_ARG, "transaction / bank period must be in [1, 128] bytes");
+  for (int s = 0; s < d->n_stages; ++s)
+    if (d->stages[s].n_access > 0 && d->stages[s].access_begin + d->stages[s].n_access > d->n_access)
+      return fail(GS_ERR_ARG, "stage access range out of bounds");
+  auto* p = new GsPipeline();
+  PipeDev& h = p->host;
+  h.nf = d->n_funcs; h.ns = d->n_stages; h.na = d->n_access;
+  int nd = 1, R = 0;
+  for (int f = 0; f < h.nf; ++f) {
+    nd = std::max(nd, d->funcs[f].ndim);
+    if (!d->funcs[f].is_external) R += d->funcs[f].n_stages;
+    if (d->funcs[f].n_stages > 255) { delete p; return fail(GS_ERR_ARG, "more than 255 stages in a func"); }
+  }
+  if (nd > GS_MAX_NDIM) { delete p; return fail(GS_ERR_ARG, "ndim > 4"); }
+  h.nd = nd; h.max_rows = R; h.m = d->machine; h.th = d->thresholds;
+  auto al = [](int x) { return (x + 15) & ~15; };
+  h.off_stages = al(h.nf * (int)sizeof(GsFunc));
+  h.off_access = h.off_stages + al(std::max(1, h.ns) * (int)sizeof(GsStage));
+  h.blob_bytes = h.off_access + al(std::max(1, h.na) * (int)sizeof(GsAccess));
+  std::vector<uint8_t> blob(h.blob_bytes, 0);
+  memcpy(blob.data(), d->funcs, h.nf * sizeof(GsFunc));
+  if (h.ns) memcpy(blob.data() + h.off_stages, d->stages, h.ns * sizeof(GsStage));
+  if (h.na) memcpy(blob.data() + h.off_access, d->access, h.na * sizeof(GsAccess));
+  // capacities for expanded reads / chain paths (per candidate, in shared memory)
+  p->rcap = std::min(4096, 4 * h.na + 64);
+  p->pcap = std::min(65535, 6 * p->rcap);
+  cudaDeviceProp prop;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaGetDeviceProperties(&prop, dev));
+  p->num_sms = prop.multiProcessorCount;
+  p->max_smem = (int)prop.sharedMemPerBlockOptin;
+  CK(cudaMalloc(&p->dev, sizeof(PipeDev)));
+  CK(cudaMemcpy(p->dev, &h, sizeof(PipeDev), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&p->blob, h.blob_bytes));
+  CK(cudaMemcpy(p->blob, blob.data(), h.blob_bytes, cudaMemcpyHostToDevice));
+  std::vector<int32_t> sof(h.nf);
+  for (int f = 0; f < h.nf; ++f) sof[f] = d->funcs[f].stage_begin;
+  CK(cudaMalloc(&p->stage_of_func, 4 * h.nf));
+  CK(cudaMemcpy(p->stage_of_func, sof.data(), 4 * h.nf, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&p->algo, 8 * GS_ALGO_DIM * std::max(1, h.ns)));
+  if (h.ns) CK(cudaMemcpy(p->algo, d->algo, 8 * GS_ALGO_DIM * h.ns, cudaMemcpyHostToDevice));
+  std::vector<int32_t> sorted(h.nf);
+  for (int f = 0; f < h.nf; ++f) {
+    int r = d->funcs[f].name_rank;
+    if (r < 0 || r >= h.nf) { delete p; return fail(GS_ERR_ARG, "bad name_rank"); }
+    sorted[r] = f;
+  }
+  CK(cudaMalloc(&p->sorted, 4 * h.nf));
+  CK(cudaMemcpy(p->sorted, sorted.data(), 4 * h.nf, cudaMemcpyHostToDevice));
+  const int nb = d->name_off[h.nf];
+  CK(cudaMalloc(&p->names, std::max(1, nb)));
+  CK(cudaMemcpy(p->names, d->name_repr, nb, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&p->name_off, 4 * (h.nf + 1)));
+  CK(cudaMemcpy(p->name_off, d->name_off, 4 * (h.nf + 1), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&p->err, sizeof(int)));
+  CK(cudaMemset(p->err, 0, sizeof(int)));
+  *out = p;
+  return GS_OK;
+}
+
+int gs_pipeline_destroy(gs_pipeline_t p) {
+  if (!p) return GS_OK;
+  cudaFree(p->dev); cudaFree(p->blob); cudaFree(p->stage_of_func); cudaFree(p->algo); cudaFree(p->sorted);
+  cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err);
+  for (double* b : p->wbufs) cudaFree(b);
+  delete p;
+  return GS_OK;
+}
+
+int gs_pipeline_max_rows(gs_pipeline_t p) { return p ? p->host.max_rows : 0; }
+
+int gs_set_weights(gs_pipeline_t p, int E, int H, const double* aw, const double* ab, const double* sw,
+                   const double* sb, const double* hw, const double* hb, const double* ow, const double* ob) {
+  if (!p || E < 1 || E > 64 || H < 1 || H > 512) return fail(GS_ERR_ARG, "embed_dim must be in [1,64], hidden in [1,512]");
+  for (double* b : p->wbufs) cudaFree(b);
+  p->wbufs.clear();
+  const double* src[8] = {aw, ab, sw, sb, hw, hb, ow, ob};
+  const size_t cnt[8] = {(size_t)GS_ALGO_DIM * E, (size_t)E, (size_t)GS_NUM_FEATURES * E, (size_t)E,
+                         (size_t)2 * E * H, (size_t)H, (size_t)H * GS_NUM_COEFFS, (size_t)GS_NUM_COEFFS};
+  double* dst[8];
+  for (int i = 0; i < 8; ++i) {
+    CK(cudaMalloc(&dst[i], 8 * cnt[i]));
+    CK(cudaMemcpy(dst[i], src[i], 8 * cnt[i], cudaMemcpyHostToDevice));
+    p->wbufs.push_back(dst[i]);
+  }
+  double* hoisted;
+  CK(cudaMalloc(&hoisted, 8 * (size_t)H * std::max(1, p->host.ns)));
+  p->wbufs.push_back(hoisted);
+  p->net = NetDev{E, H, dst[0], dst[1], dst[2], dst[3], dst[4], dst[5], dst[6], dst[7], hoisted};
+  launch_hoist(p->net, p->algo, p->host.ns, 0);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return GS_OK;
+}
+
+static Layout layout_for(gs_pipeline_t p, int S, int nwarps) {
+  return make_layout(p->host.nd, p->host.nf, p->host.ns, p->host.blob_bytes, S, std::max(1, p->host.max_rows),
+                     p->rcap, p->pcap, nwarps);
+}
+
+int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, double* feats, int32_t* row_key,
+                 int32_t* n_rows, uint8_t* verdict, void* stream) {
+  if (!p || S < 1 || n < 0) return fail(GS_ERR_ARG, "bad featurize arguments");
+  if (n == 0) return GS_OK;
+  const int nwarps = 8;
+  Layout L = layout_for(p, S, nwarps);
+  if (L.total > p->max_smem)
+    return fail(GS_ERR_CAPACITY, "pipeline too large for the per-CTA shared-memory workspace (" +
+                                     std::to_string(L.total) + " > " + std::to_string(p->max_smem) + " bytes)");
+  int occ = featurize_occupancy(p->host.nd, nwarps, L.total);
+  if (occ < 1) occ = 1;
+  int64_t grid = (int64_t)p->num_sms * occ;
+  if (grid > n) grid = n;
+  int rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, L, nwarps,
+                            (int)grid, p->err, (cudaStream_t)stream);
+  if (rc) return fail(GS_ERR_ARG, "unsupported ndim");
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
+int gs_check(gs_pipeline_t p, void* stream) {
+  if (!p) return fail(GS_ERR_ARG, "null pipeline");
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  int e = 0;
+  CK(cudaMemcpy(&e, p->err, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(p->err, 0, sizeof(int)));
+  if (e & 32) return fail(GS_ERR_SCHEDULE, "illegal decision log (bad func / consumer / duplicate / no fusion source)");
+  if (e) return fail(GS_ERR_CAPACITY, "candidate exceeded a device workspace capacity (flags " + std::to_string(e) + ")");
+  return GS_OK;
+}
+
+int gs_cost(gs_pipeline_t p, const double* feats, const int32_t* row_key, const int32_t* n_rows, int64_t n,
+            double* total, double* row_cost, double* basis_gh, void* stream) {
+  if (!p || !p->net.sched_w) return fail(GS_ERR_ARG, "weights not set (gs_set_weights)");
+  int rc = launch_cost(p->net, p->stage_of_func, feats, row_key, n_rows, n, std::max(1, p->host.max_rows), total,
+                       row_cost, basis_gh, p->num_sms, (cudaStream_t)stream);
+  if (rc) return fail(GS_ERR_ARG, "unsupported network dims");
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
+int gs_struct_hash(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, int depth, uint64_t* out,
+                   void* stream) {
+  if (!p || depth < 0) return fail(GS_ERR_ARG, "depth must be >= 0");
+  int rc = launch_hash(dec, n, S, p->host.nf, depth, p->sorted, p->names, p->name_off, out, (cudaStream_t)stream);
+  if (rc) return fail(GS_ERR_ARG, "too many funcs for the hash kernel");
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
+int64_t gs_select_workspace_bytes(int64_t n) { return select_workspace_bytes(n); }
+
+int gs_select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, uint64_t phase_seed, void* ws,
+                   int64_t ws_bytes, int64_t* rep_idx, int64_t* n_reps, int64_t* rej_idx, int64_t* n_rejects,
+                   void* stream) {
+  int rc = select_reps(hashes, verdict, n, phase_seed, ws, ws_bytes, rep_idx, n_reps, n_rejects, rej_idx,
+                       (cudaStream_t)stream);
+  if (rc) return fail(GS_ERR_ARG, "select_reps: workspace too small or n too large");
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
+int64_t gs_topk_workspace_bytes(int64_t n) { return topk_workspace_bytes(n); }
+
+int gs_beam_topk(const double* costs, const uint64_t* pass_hash, int64_t n, const uint64_t* flagged,
+                 int64_t n_flagged, double penalty, double temperature, uint64_t phase_seed, int64_t k, void* ws,
+                 int64_t ws_bytes, int64_t* out_pos, int64_t* n_out, uint8_t* bottom, void* stream) {
+  int rc = beam_topk(costs, pass_hash, n, flagged, n_flagged, penalty, temperature, phase_seed, k, ws, ws_bytes,
+                     out_pos, n_out, bottom, (cudaStream_t)stream);
+  if (rc) return fail(GS_ERR_ARG, "beam_topk: workspace too small or k > 2048");
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
+}  // extern "C"

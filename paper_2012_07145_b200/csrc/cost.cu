@@ -1,0 +1,207 @@
+// K2 — basis (g, h) + two-tower coefficient network + g.c + h + in-order
+// stage sum, fused over a feature tile (reference costmodel.py:118-176,
+// 271-293; search.py:115-124).
+//
+// Layout: one thread per stage row; the network weights (fp64) live in
+// shared memory and are read as warp-wide broadcasts; the algorithm-side
+// tower and its head contribution are hoisted to one 64-vector per stage
+// (`hoist_kernel`, recomputed only when the weights change).  Per-row costs
+// go to a shared-memory tile and one thread per candidate adds them up in
+// row order, exactly the reference's `total += c` sequence.
+// Arithmetic is fp64 end to end (the reference is fp64; parity target 1e-5
+// relative, measured ~1e-15), the basis without FMA contraction.
+#include "gs_internal.cuh"
+
+namespace gs {
+
+constexpr double kEps = 1e-8;
+
+__global__ void hoist_kernel(NetDev net, const double* __restrict__ algo, int n_stages) {
+  int s = blockIdx.x;
+  if (s >= n_stages) return;
+  __shared__ double ea[128];
+  const int E = net.E, H = net.H;
+  for (int j = threadIdx.x; j < E; j += blockDim.x) {
+    double z = net.algo_b[j];
+    for (int i = 0; i < GS_ALGO_DIM; ++i) z = fma(algo[s * GS_ALGO_DIM + i], net.algo_w[i * E + j], z);
+    ea[j] = z > 0.0 ? z : 0.0;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < H; o += blockDim.x) {
+    double z = net.head_b[o];
+    for (int j = 0; j < E; ++j) z = fma(ea[j], net.head_w[j * H + o], z);
+    net.hoisted[s * H + o] = z;
+  }
+}
+
+__device__ __forceinline__ double softplus(double z) {
+  // numpy npy_logaddexp(0, z)
+  if (z == 0.0) return 0.6931471805599453;  // 0 + log(2)
+  const double t = -z;
+  if (t > 0) return log1p(exp(-t));
+  return z + log1p(exp(t));
+}
+
+// reference stage_cost_basis; returns h, writes g (may be null)
+__device__ double basis_dot(const double* __restrict__ f, const double* __restrict__ c, double* gout) {
+  auto F = [&](int i) { return f[i]; };
+  const bool inl = F(50) > 0;
+  double scale = __ddiv_rn(ceil(__ddiv_rn(F(46), F(49))), fmax(1.0, F(48)));
+  if (!inl) scale = __ddiv_rn(scale, __dsub_rn(1.0, F(30)));
+  const double pts = __dmul_rn(__dmul_rn(F(23), F(26)), F(1));
+  double g[GS_NUM_COEFFS];
+#pragma unroll
+  for (int i = 0; i < GS_NUM_COEFFS; ++i) g[i] = 0.0;
+  g[inl ? 3 : 1] = __dmul_rn(F(0), scale);
+  g[inl ? 4 : 19] = __dmul_rn(pts, scale);
+  const double r = F(44);
+  g[5] = __dmul_rn(r, F(5));  g[16] = __dmul_rn(r, F(6));  g[8] = __dmul_rn(r, F(7));
+  g[6] = __dmul_rn(r, F(2));  g[20] = __dmul_rn(r, F(3));  g[7] = __dmul_rn(r, F(4));
+  g[18] = __dmul_rn(r, F(11)); g[17] = __dmul_rn(r, F(12)); g[2] = __dmul_rn(r, F(13));
+  g[13] = __dmul_rn(r, F(8)); g[11] = __dmul_rn(r, F(9));  g[0] = __dmul_rn(r, F(10));
+  g[10] = __dmul_rn(F(0), F(51));
+  g[12] = __dmul_rn(F(0), F(52));
+  g[14] = __dmul_rn(F(46), F(53));
+  g[15] = __dmul_rn(F(46), F(54));
+  double gl = __dmul_rn(F(23), F(32));
+  double sl = __dmul_rn(F(23), F(31));
+  if (!inl) { gl = __ddiv_rn(gl, F(38)); sl = __ddiv_rn(sl, F(36)); }
+  const double h = __dadd_rn(gl, sl);
+  g[29] = __dmul_rn(F(23), F(33));
+  double gs = __dmul_rn(F(23), F(34));
+  if (!inl) gs = __ddiv_rn(gs, F(37));
+  g[21] = gs;
+  if (F(47) > 1) g[22] = __ddiv_rn(F(0), fmax(1.0, F(20)));
+  g[24] = F(44);
+  if (F(47) > 1) g[25] = F(45);
+  g[26] = __dmul_rn(F(45), __dsub_rn(F(47), 1.0));
+  g[9] = F(55);
+  double dot = 0.0;
+#pragma unroll
+  for (int i = 0; i < GS_NUM_COEFFS; ++i) dot = fma(g[i], c[i], dot);
+  if (gout) {
+#pragma unroll
+    for (int i = 0; i < GS_NUM_COEFFS; ++i) gout[i] = g[i];
+    gout[GS_NUM_COEFFS] = h;
+  }
+  return __dadd_rn(dot, h);
+}
+
+template <int MAXE>
+__device__ double stage_row_cost(const NetDev& net, const double* __restrict__ sw, const double* __restrict__ whs,
+                           const double* __restrict__ wo, const double* __restrict__ bs,
+                           const double* __restrict__ bo, const double* __restrict__ f, int stage,
+                           double* gout) {
+  const int E = net.E, H = net.H;
+  double es[MAXE];
+#pragma unroll
+  for (int j = 0; j < MAXE; ++j) es[j] = j < E ? bs[j] : 0.0;
+  for (int k = 0; k < GS_NUM_FEATURES; ++k) {
+    const double x = log1p(f[k]);
+#pragma unroll
+    for (int j = 0; j < MAXE; ++j) if (j < E) es[j] = fma(x, sw[k * E + j], es[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < MAXE; ++j) es[j] = es[j] > 0.0 ? es[j] : 0.0;
+  double zo[GS_NUM_COEFFS];
+#pragma unroll
+  for (int o = 0; o < GS_NUM_COEFFS; ++o) zo[o] = bo[o];
+  const double* hp = net.hoisted + (int64_t)stage * H;
+  for (int i = 0; i < H; ++i) {
+    double z = __ldg(hp + i);
+#pragma unroll
+    for (int j = 0; j < MAXE; ++j) if (j < E) z = fma(es[j], whs[j * H + i], z);
+    if (z > 0.0) {
+#pragma unroll
+      for (int o = 0; o < GS_NUM_COEFFS; ++o) zo[o] = fma(z, wo[i * GS_NUM_COEFFS + o], zo[o]);
+    }
+  }
+  double c[GS_NUM_COEFFS];
+#pragma unroll
+  for (int o = 0; o < GS_NUM_COEFFS; ++o) c[o] = softplus(zo[o]) + kEps;
+  return basis_dot(f, c, gout);
+}
+
+template <int MAXE>
+__global__ void __launch_bounds__(128) cost_kernel(NetDev net, const int32_t* __restrict__ stage_of_func,
+                                                   const double* __restrict__ feats,
+                                                   const int32_t* __restrict__ row_key,
+                                                   const int32_t* __restrict__ n_rows, int64_t n, int R, int CB,
+                                                   double* __restrict__ total, double* __restrict__ row_cost,
+                                                   double* __restrict__ basis_gh) {
+  extern __shared__ __align__(16) double smd[];
+  const int E = net.E, H = net.H;
+  double* sw = smd;                          // 56*E
+  double* whs = sw + GS_NUM_FEATURES * E;    // E*H (sched half of head_w)
+  double* wo = whs + E * H;                  // H*30
+  double* bs = wo + H * GS_NUM_COEFFS;       // E
+  double* bo = bs + E;                       // 30
+  double* buf = bo + GS_NUM_COEFFS;          // CB*R
+  for (int i = threadIdx.x; i < GS_NUM_FEATURES * E; i += blockDim.x) sw[i] = net.sched_w[i];
+  for (int i = threadIdx.x; i < E * H; i += blockDim.x) whs[i] = net.head_w[E * H + i];
+  for (int i = threadIdx.x; i < H * GS_NUM_COEFFS; i += blockDim.x) wo[i] = net.out_w[i];
+  for (int i = threadIdx.x; i < E; i += blockDim.x) bs[i] = net.sched_b[i];
+  for (int i = threadIdx.x; i < GS_NUM_COEFFS; i += blockDim.x) bo[i] = net.out_b[i];
+  __syncthreads();
+  for (int64_t c0 = (int64_t)blockIdx.x * CB; c0 < n; c0 += (int64_t)gridDim.x * CB) {
+    const int ncb = (int)((n - c0) < CB ? (n - c0) : CB);
+    for (int idx = threadIdx.x; idx < ncb * R; idx += blockDim.x) {
+      const int cl = idx / R, r = idx % R;
+      const int64_t c = c0 + cl;
+      if (r >= n_rows[c]) continue;
+      const int64_t row = c * R + r;
+      const int key = row_key[row];
+      const int stage = stage_of_func[key >> 8] + (key & 255);
+      const double v = stage_row_cost<MAXE>(net, sw, whs, wo, bs, bo, feats + row * GS_NUM_FEATURES, stage,
+                                       basis_gh ? basis_gh + row * (GS_NUM_COEFFS + 1) : nullptr);
+      buf[idx] = v;
+      if (row_cost) row_cost[row] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < ncb) {
+      const int64_t c = c0 + threadIdx.x;
+      double t = 0.0;
+      const int nr = n_rows[c];
+      for (int r = 0; r < nr; ++r) t = __dadd_rn(t, buf[threadIdx.x * R + r]);
+      total[c] = t;
+    }
+    __syncthreads();
+  }
+}
+
+int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st) {
+  if (n_stages == 0) return 0;
+  hoist_kernel<<<n_stages, 64, 0, st>>>(net, algo, n_stages);
+  return 0;
+}
+
+int cost_smem_bytes(int E, int H, int CB, int R) {
+  return (GS_NUM_FEATURES * E + E * H + H * GS_NUM_COEFFS + E + GS_NUM_COEFFS + CB * R) * 8;
+}
+
+int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
+                const int32_t* n_rows, int64_t n, int R, double* total, double* row_cost, double* basis_gh,
+                int num_sms, cudaStream_t st) {
+  if (n == 0) return 0;
+  int CB = 512 / (R > 0 ? R : 1);
+  if (CB < 1) CB = 1;
+  if (CB > 128) CB = 128;
+  const int smem = cost_smem_bytes(net.E, net.H, CB, R);
+  int64_t blocks = (n + CB - 1) / CB;
+  int64_t cap = (int64_t)num_sms * 8;
+  int grid = (int)(blocks < cap ? blocks : cap);
+  if (net.E <= 32) {
+    cudaFuncSetAttribute(cost_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cost_kernel<32><<<grid, 128, smem, st>>>(net, stage_of_func, feats, row_key, n_rows, n, R, CB, total,
+                                             row_cost, basis_gh);
+  } else if (net.E <= 64) {
+    cudaFuncSetAttribute(cost_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cost_kernel<64><<<grid, 128, smem, st>>>(net, stage_of_func, feats, row_key, n_rows, n, R, CB, total,
+                                             row_cost, basis_gh);
+  } else {
+    return -1;
+  }
+  return 0;
+}
+
+}  // namespace gs

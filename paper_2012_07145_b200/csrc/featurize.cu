@@ -1,0 +1,1176 @@
+// K1 — per-candidate resolve + 56 schedule features per stage row + prune.
+//
+// One CTA scores one candidate at a time (persistent grid over candidates):
+//   * the candidate-independent pipeline descriptor is staged ONCE per CTA
+//     from global memory into shared memory with a bulk async copy (TMA
+//     `cp.async.bulk`, SASS UBLKCP) completing on an mbarrier;
+//   * warp 0 loads the 16-byte decision records with 128-bit loads and
+//     resolves the padded-tile geometry of every func into shared memory
+//     (reference resolve.py:229-376), then the prune verdict
+//     (options.py:200-255);
+//   * all warps then take stage rows round-robin and compute the 56
+//     features of each row (featurize.py:415-617).  Warp-instruction
+//     transaction counts (featurize.py:173-196, 508-571) use the fact that a
+//     count only depends on the per-instruction address residue mod the
+//     transaction size (global) or bank period (shared): the warp builds the
+//     residue histogram of all emitted loads by cyclic convolution of per-dim
+//     histograms, then counts each distinct residue once per emulated warp
+//     with __match_any_sync / __ballot_sync / __popc on the real lanes.
+#include "gs_internal.cuh"
+#include <cuda/std/cstdint>
+
+namespace gs {
+
+struct Frame { int16_t owner, root; int32_t cur, end; int16_t plen, pad; int64_t vol; };
+
+struct WarpScr {
+  double feat[GS_NUM_FEATURES];
+  unsigned long long H[kMaxM], S[kMaxM], T[kMaxM];
+  unsigned long long acc[4][3][2];      // box x tier x (bytes, lines)
+  int16_t rl[kRowReads];
+  int8_t grp[kRowReads];
+  int8_t gtier[kRowReads];
+  int16_t gprod[kRowReads];
+  int ngroups;
+  int nr;
+};
+
+struct Misc {
+  int ndec, nreads, npath, nrows, nord, err, verdict, pad;
+};
+
+template <int ND>
+struct K1 {
+  const GsFunc* F;
+  const GsStage* ST;
+  const GsAccess* A;
+  const PipeDev* P;
+  GsDecision* dec;
+  int16_t* didx;
+  CF<ND>* cf;
+  RRead* rd;
+  int16_t* path;
+  int32_t* rdb;      // [2*ns]: begin,end of reads per global stage
+  int32_t* frd;      // [nf]: first read index of each non-inline func
+  int32_t* rows;
+  Frame* stack;
+  int64_t* volacc;
+  int16_t* touched;
+  Misc* misc;
+  int rcap, pcap;
+  int* gerr;
+};
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ int64_t wmin64(int64_t v) {
+  for (int o = 16; o; o >>= 1) { int64_t u = __shfl_xor_sync(0xffffffffu, v, o); v = u < v ? u : v; }
+  return v;
+}
+__device__ __forceinline__ int64_t wmax64(int64_t v) {
+  for (int o = 16; o; o >>= 1) { int64_t u = __shfl_xor_sync(0xffffffffu, v, o); v = u > v ? u : v; }
+  return v;
+}
+
+template <int ND>
+__device__ __forceinline__ int64_t prod_ext(const CF<ND>& c) {
+  int64_t p = 1;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) p *= c.ext[d];
+  return p;
+}
+template <int ND>
+__device__ __forceinline__ int64_t alloc_of(const CF<ND>& c) {
+  if (c.tier == T_NONE) return 0;
+  int64_t p = 1;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) p *= (int64_t)c.rhi[d] - c.rlo[d] + 1;
+  return p;
+}
+template <int ND>
+__device__ __forceinline__ void block_box(const CF<ND>& c, int32_t* lo, int32_t* hi) {
+  // resolve.py:112-122
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    if (c.kind == K_ROOT) { lo[d] = 0; hi[d] = c.bbx[d] - 1; }
+    else if (c.kind == K_BLOCK) { lo[d] = c.rlo[d]; hi[d] = c.rhi[d]; }
+    else { lo[d] = c.base[d]; hi[d] = c.base[d] + (c.ctx[d] - 1) * c.coeff[d] + c.ext[d] - 1; }
+  }
+}
+
+// chain box of [lo,hi] through a path of accesses, dimension d
+__device__ __forceinline__ void chain_iv(const GsAccess* A, const int16_t* p, int plen, int d,
+                                         int64_t& a, int64_t& b) {
+  for (int k = 0; k < plen; ++k) {
+    const GsAccess& x = A[p[k]];
+    a = a * x.s[d] + x.lo[d];
+    b = b * x.s[d] + x.hi[d];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// resolve (warp 0)
+// ---------------------------------------------------------------------------
+template <int ND>
+__device__ int8_t tier_of_producer(const K1<ND>& k, int p) {
+  int di = k.didx[p];
+  if (di < 0 || k.F[p].is_external) return T_GLOBAL;
+  int kind = k.dec[di].kind;
+  return kind == GS_ROOT ? T_GLOBAL : kind == GS_FUSE_BLOCK ? T_SHARED : T_REGISTER;
+}
+
+// Depth-first inline substitution of one stage (resolve.py:167-200).
+// mode 0: emit reads; mode 1: accumulate inline call volumes into volacc.
+template <int ND>
+__device__ void expand_stage(K1<ND>& k, int root, int gstage, int mode, int& ntouched) {
+  Misc& m = *k.misc;
+  int sp = 0;
+  int16_t* pfx = k.touched + k.P->nf;   // path prefix buffer (nf entries)
+  const GsStage& st = k.ST[gstage];
+  k.stack[0] = Frame{(int16_t)root, (int16_t)root, st.access_begin, st.access_begin + st.n_access, 0, 0, 1};
+  sp = 1;
+  while (sp > 0) {
+    Frame& fr = k.stack[sp - 1];
+    if (fr.cur == fr.end) { --sp; continue; }
+    int a = fr.cur++;
+    pfx[fr.plen] = (int16_t)a;
+    int p = k.A[a].producer;
+    int di = k.didx[p];
+    if (di >= 0 && k.dec[di].kind == GS_INLINE) {
+      int64_t vol = fr.vol * (int64_t)k.A[a].window;
+      if (mode == 1) {
+        if (k.volacc[p] == 0) k.touched[ntouched++] = (int16_t)p;
+        k.volacc[p] += vol;
+      }
+      if (sp >= k.P->nf + 1) { m.err |= E_STACK; return; }
+      const GsStage& is = k.ST[k.F[p].stage_begin];
+      k.stack[sp] = Frame{(int16_t)p, fr.root, is.access_begin, is.access_begin + is.n_access,
+                          (int16_t)(fr.plen + 1), 0, vol};
+      ++sp;
+    } else if (mode == 0) {
+      int plen = fr.plen + 1;
+      if (m.nreads >= k.rcap) { m.err |= E_READS; return; }
+      if (m.npath + plen > k.pcap || plen > 255) { m.err |= E_PATHS; return; }
+      RRead r;
+      r.owner = fr.owner; r.producer = (int16_t)p; r.root = fr.root; r.tier = tier_of_producer(k, p);
+      r.pad = 0;
+      r.plen = (uint8_t)plen; r.pbeg = (uint16_t)m.npath;
+      for (int i = 0; i < plen; ++i) k.path[m.npath + i] = pfx[i];
+      m.npath += plen;
+      k.rd[m.nreads++] = r;
+    }
+  }
+}
+
+template <int ND>
+__device__ void resolve(K1<ND>& k) {
+  const int lane = lane_id();
+  Misc& m = *k.misc;
+  const int nf = k.P->nf;
+  const GsMachine& M = k.P->m;
+  (void)M;
+  // decision index per func
+  for (int f = lane; f < nf; f += 32) { k.didx[f] = -1; k.volacc[f] = 0; k.cf[f].kind = K_ABSENT; }
+  __syncwarp();
+  if (lane == 0) {
+    int bad = 0;
+    for (int i = 0; i < m.ndec; ++i) {
+      const GsDecision& d = k.dec[i];
+      if (d.func >= nf || d.kind > GS_INLINE || k.F[d.func].is_external || k.didx[d.func] >= 0 ||
+          ((d.kind == GS_FUSE_BLOCK || d.kind == GS_FUSE_THREAD) && d.consumer >= nf))
+        bad = 1;
+      else
+        k.didx[d.func] = (int16_t)i;
+    }
+    if (bad) m.err |= E_SCHEDULE;
+    m.nreads = 0; m.npath = 0;
+    // expanded reads of every non-inline func, decision order
+    for (int i = 0; i < m.ndec && !m.err; ++i) {
+      const GsDecision& d = k.dec[i];
+      if (d.kind == GS_INLINE) continue;
+      const GsFunc& fn = k.F[d.func];
+      k.frd[d.func] = m.nreads;
+      int nt = 0;
+      for (int s = 0; s < fn.n_stages; ++s) {
+        int gsid = fn.stage_begin + s;
+        k.rdb[2 * gsid] = m.nreads;
+        expand_stage(k, d.func, gsid, 0, nt);
+        k.rdb[2 * gsid + 1] = m.nreads;
+      }
+    }
+  }
+  __syncwarp();
+  if (m.err) return;
+
+  // Pass 1: geometry of non-inline funcs in decision order (resolve.py:232-333)
+  for (int i = 0; i < m.ndec; ++i) {
+    const GsDecision d = k.dec[i];
+    if (d.kind == GS_INLINE) continue;
+    const int f = d.func;
+    const GsFunc& fn = k.F[f];
+    CF<ND> c;
+    c.consumer = (d.kind == GS_ROOT) ? -1 : (int16_t)d.consumer;
+    c.calls = 0; c.best = 0; c.k_shared = 0; c.k_threads = 0; c.n_blocks = 0;
+    c.has_serial = 0; c.serial_prod = 1;
+    if (d.kind == GS_ROOT) {
+      int32_t ser[ND], thr[ND];
+      bool tiled = (d.flags & 3) == 3;
+      int inner = 0;
+      if (!tiled) {  // provisional tiling (resolve.py:159-164)
+        inner = -1;
+        for (int dd = 0; dd < fn.ndim; ++dd) if (fn.extent[dd] >= 16) { inner = dd; break; }
+        if (inner < 0) inner = 0;
+      }
+      int64_t nb = 1, nt = 1, sp = 1;
+#pragma unroll
+      for (int dd = 0; dd < ND; ++dd) {
+        int e = dd < fn.ndim ? fn.extent[dd] : 1;
+        ser[dd] = tiled ? d.serial[dd] : 1;
+        thr[dd] = tiled ? d.thread[dd] : (dd == inner ? (e < 32 ? e : 32) : 1);
+        int64_t st = (int64_t)ser[dd] * thr[dd];
+        int64_t b = (e + st - 1) / st;
+        if (b < 1) b = 1;
+        nb *= b; nt *= thr[dd]; sp *= ser[dd];
+        c.rlo[dd] = 0; c.rhi[dd] = (int32_t)(b * st - 1);
+        c.tlo[dd] = c.rlo[dd]; c.thi[dd] = c.rhi[dd];
+        c.ctx[dd] = thr[dd]; c.base[dd] = 0; c.coeff[dd] = ser[dd]; c.ext[dd] = ser[dd];
+        c.bbx[dd] = (int32_t)st;
+      }
+      c.kind = K_ROOT; c.tier = T_GLOBAL; c.kernel = (int16_t)f; c.realizations = 1;
+      c.n_threads = (int32_t)nt; c.unrolled = sp < 16; c.has_serial = 1; c.serial_prod = (int32_t)sp;
+      c.n_blocks = nb; c.k_threads = (int32_t)nt; c.k_shared = 0;
+      if (lane == 0) k.cf[f] = c;
+      __syncwarp();
+      continue;
+    }
+    // fused: scan processed consumers' reads for producer == f (resolve.py:379-393)
+    const int end = k.frd[f];
+    int first = 0x7fffffff;
+    for (int j0 = 0; j0 < end; j0 += 32) {
+      int j = j0 + lane;
+      bool hit = j < end && k.rd[j].producer == f;
+      unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (bal) { first = j0 + __ffs(bal) - 1; break; }
+    }
+    if (first == 0x7fffffff) { if (lane == 0) m.err |= E_SCHEDULE; __syncwarp(); return; }
+    const int16_t src_root = k.rd[first].root;
+    const CF<ND> cg0 = k.cf[src_root];
+    int64_t lo[ND], hi[ND], tlo[ND], thi[ND];
+#pragma unroll
+    for (int dd = 0; dd < ND; ++dd) { lo[dd] = tlo[dd] = INT64_MAX; hi[dd] = thi[dd] = INT64_MIN; }
+    int64_t ts0[ND];
+#pragma unroll
+    for (int dd = 0; dd < ND; ++dd) ts0[dd] = 1;
+    {
+      const RRead& r0 = k.rd[first];
+      for (int q = 0; q < r0.plen; ++q)
+#pragma unroll
+        for (int dd = 0; dd < ND; ++dd) ts0[dd] *= k.A[k.path[r0.pbeg + q]].s[dd];
+    }
+    for (int j0 = 0; j0 < end; j0 += 32) {
+      int j = j0 + lane;
+      bool hit = j < end && k.rd[j].producer == f;
+      if (hit) {
+        const int16_t root = k.rd[j].root;
+        const CF<ND>& cg = (d.kind == GS_FUSE_THREAD) ? cg0 : k.cf[root];
+        const RRead& r = k.rd[j];
+        int32_t blo[ND], bhi[ND];
+        if (d.kind == GS_FUSE_BLOCK) block_box(cg, blo, bhi);
+        else {
+#pragma unroll
+          for (int dd = 0; dd < ND; ++dd) { blo[dd] = cg.base[dd]; bhi[dd] = cg.base[dd] + cg.ext[dd] - 1; }
+        }
+#pragma unroll
+        for (int dd = 0; dd < ND; ++dd) {
+          int64_t a = blo[dd], b = bhi[dd];
+          chain_iv(k.A, k.path + r.pbeg, r.plen, dd, a, b);
+          lo[dd] = a < lo[dd] ? a : lo[dd]; hi[dd] = b > hi[dd] ? b : hi[dd];
+          int64_t ta = cg.tlo[dd], tb = cg.thi[dd];
+          chain_iv(k.A, k.path + r.pbeg, r.plen, dd, ta, tb);
+          tlo[dd] = ta < tlo[dd] ? ta : tlo[dd]; thi[dd] = tb > thi[dd] ? tb : thi[dd];
+        }
+      }
+    }
+#pragma unroll
+    for (int dd = 0; dd < ND; ++dd) {
+      lo[dd] = wmin64(lo[dd]); hi[dd] = wmax64(hi[dd]);
+      tlo[dd] = wmin64(tlo[dd]); thi[dd] = wmax64(thi[dd]);
+    }
+    CF<ND>& K = k.cf[cg0.kernel];
+    if (d.kind == GS_FUSE_BLOCK) {
+      int64_t nt = 1, sp = 1;
+#pragma unroll
+      for (int dd = 0; dd < ND; ++dd) {
+        int s = (d.flags & 1) ? d.serial[dd] : 1;
+        int64_t t = (hi[dd] - lo[dd] + 1 + s - 1) / s;
+        if (t < 1) t = 1;
+        c.rlo[dd] = (int32_t)lo[dd];
+        c.rhi[dd] = (int32_t)(lo[dd] + t * s - 1);
+        c.tlo[dd] = (int32_t)tlo[dd];
+        int64_t th = tlo[dd] + t * s - 1;
+        c.thi[dd] = (int32_t)(thi[dd] > th ? thi[dd] : th);
+        c.ctx[dd] = (int32_t)t; c.base[dd] = c.rlo[dd]; c.coeff[dd] = s; c.ext[dd] = s;
+        c.bbx[dd] = 0;
+        nt *= t; sp *= s;
+      }
+      c.kind = K_BLOCK; c.tier = T_SHARED; c.kernel = cg0.kernel; c.realizations = K.n_blocks;
+      c.n_threads = (int32_t)nt; c.unrolled = sp < 16; c.has_serial = 1; c.serial_prod = (int32_t)sp;
+      __syncwarp();
+      if (lane == 0) {
+        k.cf[f] = c;
+        if (c.n_threads > K.k_threads) K.k_threads = c.n_threads;
+        K.k_shared += alloc_of(c) * fn.elem_bytes;
+      }
+    } else {
+      int64_t pe = 1;
+#pragma unroll
+      for (int dd = 0; dd < ND; ++dd) {
+        c.rlo[dd] = (int32_t)lo[dd]; c.rhi[dd] = (int32_t)hi[dd];
+        c.tlo[dd] = (int32_t)tlo[dd]; c.thi[dd] = (int32_t)thi[dd];
+        c.ctx[dd] = cg0.ctx[dd]; c.base[dd] = c.rlo[dd];
+        c.coeff[dd] = (int32_t)(cg0.coeff[dd] * ts0[dd]);
+        c.ext[dd] = (int32_t)(hi[dd] - lo[dd] + 1);
+        c.bbx[dd] = 0;
+        pe *= c.ext[dd];
+      }
+      c.kind = K_THREAD; c.tier = T_REGISTER; c.kernel = cg0.kernel;
+      c.realizations = K.n_blocks * (int64_t)cg0.n_threads; c.n_threads = cg0.n_threads;
+      c.unrolled = pe < 16; c.has_serial = 0; c.serial_prod = 1;
+      __syncwarp();
+      if (lane == 0) {
+        k.cf[f] = c;
+        if (c.n_threads > K.k_threads) K.k_threads = c.n_threads;
+      }
+    }
+    __syncwarp();
+  }
+
+  // externals and unscheduled producers (resolve.py:396-425)
+  const int nreads = m.nreads;
+  for (int f = 0; f < nf; ++f) {
+    const GsFunc& fn = k.F[f];
+    if (!(fn.is_external || k.didx[f] < 0)) continue;
+    int64_t lo[ND], hi[ND];
+#pragma unroll
+    for (int dd = 0; dd < ND; ++dd) { lo[dd] = INT64_MAX; hi[dd] = INT64_MIN; }
+    bool any = false;
+    for (int j0 = 0; j0 < nreads; j0 += 32) {
+      int j = j0 + lane;
+      bool hit = j < nreads && k.rd[j].producer == f;
+      if (hit) {
+        const CF<ND>& cg = k.cf[k.rd[j].root];
+        const RRead& r = k.rd[j];
+#pragma unroll
+        for (int dd = 0; dd < ND; ++dd) {
+          int64_t a = cg.tlo[dd], b = cg.thi[dd];
+          chain_iv(k.A, k.path + r.pbeg, r.plen, dd, a, b);
+          lo[dd] = a < lo[dd] ? a : lo[dd]; hi[dd] = b > hi[dd] ? b : hi[dd];
+        }
+      }
+      any |= __any_sync(0xffffffffu, hit);
+    }
+#pragma unroll
+    for (int dd = 0; dd < ND; ++dd) { lo[dd] = wmin64(lo[dd]); hi[dd] = wmax64(hi[dd]); }
+    if (lane == 0) {
+      CF<ND> c;
+      c.kind = K_EXTERNAL; c.tier = T_GLOBAL; c.unrolled = 0; c.has_serial = 0;
+      c.kernel = -1; c.consumer = -1; c.n_threads = 1; c.serial_prod = 1; c.k_threads = 0;
+      c.realizations = 0; c.calls = 0; c.best = 0; c.n_blocks = 0; c.k_shared = 0;
+#pragma unroll
+      for (int dd = 0; dd < ND; ++dd) {
+        int e = dd < fn.ndim ? fn.extent[dd] : 1;
+        c.rlo[dd] = any ? (int32_t)lo[dd] : 0; c.rhi[dd] = any ? (int32_t)hi[dd] : e - 1;
+        c.tlo[dd] = c.rlo[dd]; c.thi[dd] = c.rhi[dd];
+        c.ctx[dd] = 1; c.base[dd] = 0; c.coeff[dd] = 0; c.ext[dd] = 1; c.bbx[dd] = 0;
+      }
+      k.cf[f] = c;
+    }
+  }
+  __syncwarp();
+
+  // Pass 2: inline call accounting (resolve.py:337-349) + inline records
+  if (lane == 0) {
+    for (int i = 0; i < m.ndec && !m.err; ++i) {
+      const GsDecision& d = k.dec[i];
+      if (d.kind == GS_INLINE) continue;
+      const GsFunc& fn = k.F[d.func];
+      const CF<ND>& c = k.cf[d.func];
+      int64_t pb = prod_ext(c) * c.n_threads * k.cf[c.kernel].n_blocks;
+      for (int s = 0; s < fn.n_stages; ++s) {
+        int nt = 0;
+        expand_stage(k, d.func, fn.stage_begin + s, 1, nt);
+        for (int t = 0; t < nt; ++t) {
+          int iname = k.touched[t];
+          int64_t calls = k.volacc[iname] * pb;
+          k.volacc[iname] = 0;
+          CF<ND>& ic = k.cf[iname];
+          if (ic.kind != K_INLINE) { ic.kind = K_INLINE; ic.calls = 0; ic.best = 0; ic.consumer = -1; }
+          ic.calls += calls;
+          if (calls > ic.best) { ic.best = calls; ic.consumer = (int16_t)d.func; }
+        }
+      }
+    }
+    for (int i = 0; i < m.ndec; ++i) {
+      const GsDecision& d = k.dec[i];
+      if (d.kind != GS_INLINE) continue;
+      CF<ND>& ic = k.cf[d.func];
+      if (ic.kind != K_INLINE) { ic.kind = K_INLINE; ic.calls = 0; ic.best = 0; ic.consumer = -1; }
+      int prim = ic.consumer;
+      ic.tier = T_NONE; ic.has_serial = 0; ic.serial_prod = 1; ic.realizations = 0;
+      ic.k_threads = 0; ic.n_blocks = 0; ic.k_shared = 0;
+      if (prim >= 0) {
+        const CF<ND>& h = k.cf[prim];
+        ic.kernel = h.kernel; ic.n_threads = h.n_threads; ic.unrolled = h.unrolled;
+        for (int dd = 0; dd < ND; ++dd) ic.ctx[dd] = h.ctx[dd];
+      } else {
+        ic.kernel = -1; ic.n_threads = 1; ic.unrolled = 1;
+        for (int dd = 0; dd < ND; ++dd) ic.ctx[dd] = 1;
+      }
+      for (int dd = 0; dd < ND; ++dd) {
+        ic.rlo[dd] = 0; ic.rhi[dd] = -1; ic.tlo[dd] = 0; ic.thi[dd] = -1;
+        ic.base[dd] = 0; ic.coeff[dd] = 0; ic.ext[dd] = 1; ic.bbx[dd] = 0;
+      }
+    }
+    // row list: non-inline decision order (every stage), then inline
+    int nr = 0;
+    for (int i = 0; i < m.ndec; ++i) {
+      const GsDecision& d = k.dec[i];
+      if (d.kind == GS_INLINE) continue;
+      for (int s = 0; s < k.F[d.func].n_stages; ++s) k.rows[nr++] = (d.func << 8) | s;
+    }
+    for (int i = 0; i < m.ndec; ++i)
+      if (k.dec[i].kind == GS_INLINE) k.rows[nr++] = (k.dec[i].func << 8);
+    m.nrows = nr;
+  }
+  __syncwarp();
+}
+
+// prune verdict (options.py:200-255, machine.py:91-105); lane 0
+template <int ND>
+__device__ int prune_verdict(const K1<ND>& k) {
+  const Misc& m = *k.misc;
+  const GsMachine& M = k.P->m;
+  const GsThresholds& th = k.P->th;
+  double computed = 0, needed = 0;
+  int64_t ci = 0, ni = 0;
+  for (int i = 0; i < m.ndec; ++i) {   // non-external scheduled funcs
+    const GsDecision& d = k.dec[i];
+    const GsFunc& fn = k.F[d.func];
+    int64_t dom = 1;
+    for (int dd = 0; dd < fn.ndim; ++dd) dom *= fn.extent[dd];
+    ni += dom;
+    const CF<ND>& c = k.cf[d.func];
+    if (d.kind == GS_INLINE) ci += c.calls;
+    else ci += prod_ext(c) * c.n_threads * k.cf[c.kernel].n_blocks;
+  }
+  computed = (double)ci; needed = (double)ni;
+  if (ni && computed > th.recompute_factor * needed) return GS_PRUNE_RECOMPUTE;
+  double minb = th.min_blocks_per_sm_factor * (double)M.num_sms;
+  for (int i = 0; i < m.ndec; ++i)
+    if (k.dec[i].kind == GS_ROOT && (double)k.cf[k.dec[i].func].n_blocks < minb) return GS_PRUNE_IDLE_SMS;
+  for (int i = 0; i < m.ndec; ++i) {
+    const GsDecision& d = k.dec[i];
+    if (d.kind == GS_INLINE) continue;
+    const CF<ND>& c = k.cf[d.func];
+    int64_t w = (c.n_threads + M.warp_size - 1) / M.warp_size;
+    double util = (double)c.n_threads / (double)(w * M.warp_size);
+    if (util < th.warp_utilization_floor) return GS_PRUNE_WARP_UTIL;
+    if (c.has_serial && (int64_t)c.serial_prod > th.unroll_budget) return GS_PRUNE_SERIAL;
+    if (c.kind == K_THREAD && alloc_of(c) * k.F[d.func].elem_bytes > th.thread_alloc_bytes)
+      return GS_PRUNE_THREAD_ALLOC;
+  }
+  for (int i = 0; i < m.ndec; ++i) {
+    if (k.dec[i].kind != GS_ROOT) continue;
+    const CF<ND>& c = k.cf[k.dec[i].func];
+    if (c.k_threads > M.max_threads_per_block || c.k_shared > M.shared_mem_per_block_limit)
+      return GS_PRUNE_HW_LIMIT;
+  }
+  return GS_VALID;
+}
+
+// ---------------------------------------------------------------------------
+// exact unions of grid products (boxes.py:92-138), one lane per task
+// ---------------------------------------------------------------------------
+struct Iv { int64_t lo, hi; };
+
+// footprint of [a,b] through links of dim d (resolve.py:36-44); appends to buf
+__device__ int footprint(const GsAccess* A, const int16_t* p, int plen, int d, int64_t a, int64_t b,
+                         Iv* buf, int cap, int& err) {
+  if (cap < 1) { err |= E_LANEIV; return 0; }
+  buf[0] = Iv{a, b};
+  int n = 1;
+  for (int k = 0; k < plen; ++k) {
+    const GsAccess& x = A[p[k]];
+    const int64_t s = x.s[d], wl = x.lo[d], wh = x.hi[d];
+    if (s <= wh - wl + 1) {       // every interval maps to one interval; merge in place
+      int w = 0;
+      for (int i = 0; i < n; ++i) {
+        Iv v{buf[i].lo * s + wl, buf[i].hi * s + wh};
+        if (w && v.lo <= buf[w - 1].hi + 1) { if (v.hi > buf[w - 1].hi) buf[w - 1].hi = v.hi; }
+        else buf[w++] = v;
+      }
+      n = w;
+    } else {                      // one interval per point, already disjoint & sorted
+      int64_t tot = 0;
+      for (int i = 0; i < n; ++i) tot += buf[i].hi - buf[i].lo + 1;
+      if (tot > cap) { err |= E_LANEIV; return 0; }
+      // expand from the back so the source is not overwritten
+      int w = (int)tot;
+      for (int i = n - 1; i >= 0; --i)
+        for (int64_t xx = buf[i].hi; xx >= buf[i].lo; --xx) buf[--w] = Iv{xx * s + wl, xx * s + wh};
+      n = (int)tot;
+    }
+  }
+  return n;
+}
+
+template <int ND>
+__device__ void union_count(const GsAccess* A, const RRead* rd, const int16_t* paths,
+                            const int16_t* rl, const int8_t* grp, int nr, int g,
+                            const int32_t* blo, const int32_t* bhi,
+                            int64_t& vol, int64_t& lines, int& err) {
+  Iv buf[kLaneIv];
+  int16_t off[kGroupReads][ND], cnt[kGroupReads][ND];
+  int K = 0, used = 0;
+  for (int q = 0; q < nr; ++q) {
+    if (grp[q] != g) continue;
+    if (K >= kGroupReads) { err |= E_GROUP; vol = lines = 0; return; }
+    const RRead& r = rd[rl[q]];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      int n = footprint(A, paths + r.pbeg, r.plen, d, blo[d], bhi[d], buf + used, kLaneIv - used, err);
+      off[K][d] = (int16_t)used; cnt[K][d] = (int16_t)n; used += n;
+    }
+    ++K;
+  }
+  vol = lines = 0;
+  if (err || K == 0) return;
+  if (K == 1) {
+    int64_t outer = 1;
+    for (int d = 1; d < ND; ++d) {
+      int64_t t = 0;
+      for (int i = 0; i < cnt[0][d]; ++i) t += buf[off[0][d] + i].hi - buf[off[0][d] + i].lo + 1;
+      outer *= t;
+    }
+    int64_t t0 = 0;
+    for (int i = 0; i < cnt[0][0]; ++i) t0 += buf[off[0][0] + i].hi - buf[off[0][0] + i].lo + 1;
+    vol = t0 * outer;
+    lines = (int64_t)cnt[0][0] * outer;
+    return;
+  }
+  // outer-dim cut points (coordinate compression)
+  constexpr int kCuts = 64;
+  int64_t cuts[ND > 1 ? ND - 1 : 1][kCuts];
+  int ncut[ND > 1 ? ND - 1 : 1];
+  for (int d = 1; d < ND; ++d) {
+    int n = 0;
+    for (int q = 0; q < K; ++q)
+      for (int i = 0; i < cnt[q][d]; ++i) {
+        int64_t v2[2] = {buf[off[q][d] + i].lo, buf[off[q][d] + i].hi + 1};
+        for (int e = 0; e < 2; ++e) {
+          int64_t v = v2[e];
+          int pos = n;
+          bool dup = false;
+          for (int t = 0; t < n; ++t) { if (cuts[d - 1][t] == v) { dup = true; break; } }
+          if (dup) continue;
+          if (n >= kCuts) { err |= E_LANEIV; return; }
+          while (pos > 0 && cuts[d - 1][pos - 1] > v) { cuts[d - 1][pos] = cuts[d - 1][pos - 1]; --pos; }
+          cuts[d - 1][pos] = v;
+          ++n;
+        }
+      }
+    ncut[d - 1] = n;
+  }
+  int idx[ND > 1 ? ND - 1 : 1];
+  for (int d = 0; d < ND - 1; ++d) idx[d] = 0;
+  while (true) {
+    bool valid = true;
+    for (int d = 0; d < ND - 1; ++d) if (ncut[d] < 2) valid = false;
+    if (!valid && ND > 1) break;
+    // cell = pieces idx[d]
+    int64_t cellv = 1;
+    unsigned act = 0;
+    for (int q = 0; q < K; ++q) {
+      bool in = true;
+      for (int d = 1; d < ND && in; ++d) {
+        int64_t p0 = cuts[d - 1][idx[d - 1]];
+        bool hit = false;
+        for (int i = 0; i < cnt[q][d]; ++i) {
+          const Iv& v = buf[off[q][d] + i];
+          if (v.lo <= p0 && p0 <= v.hi) { hit = true; break; }
+        }
+        in = hit;
+      }
+      if (in) act |= 1u << q;
+    }
+    for (int d = 1; d < ND; ++d) cellv *= cuts[d - 1][idx[d - 1] + 1] - cuts[d - 1][idx[d - 1]];
+    if (act) {
+      // k-way merge of the active dim-0 lists
+      int head[kGroupReads];
+      for (int q = 0; q < K; ++q) head[q] = 0;
+      int64_t runs = 0, len = 0, cl = 0, ch = 0;
+      bool open = false;
+      while (true) {
+        int best = -1;
+        int64_t bl = 0;
+        for (int q = 0; q < K; ++q) {
+          if (!((act >> q) & 1) || head[q] >= cnt[q][0]) continue;
+          int64_t l = buf[off[q][0] + head[q]].lo;
+          if (best < 0 || l < bl) { best = q; bl = l; }
+        }
+        if (best < 0) break;
+        const Iv& v = buf[off[best][0] + head[best]];
+        ++head[best];
+        if (open && v.lo <= ch + 1) { if (v.hi > ch) ch = v.hi; }
+        else {
+          if (open) { ++runs; len += ch - cl + 1; }
+          cl = v.lo; ch = v.hi; open = true;
+        }
+      }
+      if (open) { ++runs; len += ch - cl + 1; }
+      vol += len * cellv;
+      lines += runs * cellv;
+    }
+    // advance mixed radix
+    if (ND == 1) break;
+    int d = 0;
+    while (d < ND - 1) {
+      if (++idx[d] < ncut[d] - 1) break;
+      idx[d] = 0;
+      ++d;
+    }
+    if (d == ND - 1) break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// warp-instruction transaction counts (featurize.py:173-196, 508-571)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long count_in(int64_t a, int64_t b, int r, int M) {
+  // #{x in [a,b] : x = r (mod M)}
+  if (b < a) return 0;
+  return (unsigned long long)(floordiv(b - r, M) - floordiv(a - 1 - r, M));
+}
+
+// all lanes: H[k] for k = lane + 32j, j < M/32
+template <int ND>
+__device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, int plen, bool identity,
+                                      const CF<ND>& h, const CF<ND>& prod, int eb, int tier,
+                                      const GsMachine& Mc, WarpScr& W, int& err) {
+  const int lane = lane_id();
+  const int M = tier == T_GLOBAL ? Mc.global_transaction_bytes : Mc.shared_banks * Mc.bank_width_bytes;
+  const int per = (M + 31) / 32;
+  int64_t bs[ND], ts[ND];
+  {
+    int64_t acc = eb;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      bs[d] = acc;
+      acc *= (int64_t)prod.rhi[d] - prod.rlo[d] + 1;
+      ts[d] = 1;
+      if (!identity)
+        for (int q = 0; q < plen; ++q) ts[d] *= A[path[q]].s[d];
+    }
+  }
+  for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.T[r] = (r == 0); }
+  __syncwarp();
+  for (int d = 0; d < ND; ++d) {
+    const int e = h.ext[d];
+    // per-dim histogram of relative coordinates (mod M) into H
+    if (identity || !h.unrolled) {
+      for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.H[r] = count_in(0, e - 1, r, M); }
+      __syncwarp();
+      if (!identity) {
+        for (int q = 0; q < plen; ++q) {
+          const GsAccess& x = A[path[q]];
+          const int64_t s = x.s[d], wl = x.lo[d], wh = x.hi[d];
+          // S[k] = sum_r H[r] * #{w in [wl,wh] : r*s + w = k (mod M)}
+          for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.S[r] = 0; }
+          __syncwarp();
+          for (int c = 0; c < per; ++c) {
+            unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < M && W.H[c * 32 + lane] != 0);
+            while (nz) {
+              int b = __ffs(nz) - 1; nz &= nz - 1;
+              int r = c * 32 + b;
+              unsigned long long hv = W.H[r];
+              int64_t sh = posmod((int64_t)r * s, M);
+              for (int j = 0; j < per; ++j) {
+                int k = lane + 32 * j;
+                if (k < M) W.S[k] += hv * count_in(wl, wh, (int)posmod(k - sh, M), M);
+              }
+            }
+          }
+          __syncwarp();
+          for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.H[r] = W.S[r]; }
+          __syncwarp();
+        }
+      }
+    } else {
+      // unrolled: unique points of the chain footprint of [0, e-1]
+      Iv buf[kLaneIv];
+      int n = footprint(A, path, plen, d, 0, e - 1, buf, kLaneIv, err);
+      for (int j = 0; j < per; ++j) {
+        int r = lane + 32 * j;
+        if (r >= M) continue;
+        unsigned long long c = 0;
+        for (int i = 0; i < n; ++i) c += count_in(buf[i].lo, buf[i].hi, r, M);
+        W.H[r] = c;
+      }
+      __syncwarp();
+    }
+    // scale by the byte stride of dim d, then convolve into T
+    const int64_t bm = posmod(bs[d], M);
+    for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.S[r] = 0; }
+    __syncwarp();
+    for (int j = 0; j < per; ++j) {
+      int r = lane + 32 * j;
+      if (r < M && W.H[r]) atomicAdd(&W.S[(int)posmod((int64_t)r * bm, M)], W.H[r]);
+    }
+    __syncwarp();
+    for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.H[r] = 0; }
+    __syncwarp();
+    for (int c = 0; c < per; ++c) {
+      unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < M && W.T[c * 32 + lane] != 0);
+      while (nz) {
+        int b = __ffs(nz) - 1; nz &= nz - 1;
+        int r = c * 32 + b;
+        unsigned long long tv = W.T[r];
+        for (int j = 0; j < per; ++j) {
+          int k = lane + 32 * j;
+          if (k < M) W.H[k] += tv * W.S[(int)posmod(k - r, M)];
+        }
+      }
+    }
+    __syncwarp();
+    for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.T[r] = W.H[r]; }
+    __syncwarp();
+  }
+  // count each distinct residue once per emulated warp of block 0
+  const int n_threads = h.n_threads;
+  const int nwarps = (n_threads + 31) / 32;
+  int64_t cst = kAddrBias;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) cst += ((int64_t)h.base[d] * ts[d] - prod.rlo[d]) * bs[d];
+  const bool gpow2 = (Mc.global_transaction_bytes & (Mc.global_transaction_bytes - 1)) == 0;
+  unsigned long long total = 0;
+  for (int w = 0; w < nwarps; ++w) {
+    int t = w * 32 + lane;
+    const bool active = t < n_threads;
+    int64_t org = cst;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      int cd = t % h.ctx[d];
+      t /= h.ctx[d];
+      org += (int64_t)cd * h.coeff[d] * ts[d] * bs[d];
+    }
+    const unsigned amask = __ballot_sync(0xffffffffu, active);
+    for (int c = 0; c < per; ++c) {
+      unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < M && W.T[c * 32 + lane] != 0);
+      while (nz) {
+        int b = __ffs(nz) - 1; nz &= nz - 1;
+        int r = c * 32 + b;
+        const unsigned long long mult = W.T[r];
+        const unsigned long long a = (unsigned long long)(org + r);
+        unsigned cnt;
+        if (tier == T_GLOBAL) {
+          unsigned long long seg = gpow2 ? (a >> (__ffs(Mc.global_transaction_bytes) - 1))
+                                         : a / (unsigned long long)Mc.global_transaction_bytes;
+          if (!active) seg = ~0ull - lane;
+          unsigned lm = __match_any_sync(0xffffffffu, seg);
+          bool lead = active && (__ffs(lm) - 1 == lane);
+          cnt = __popc(__ballot_sync(0xffffffffu, lead));
+        } else {
+          unsigned long long word = a / (unsigned long long)Mc.bank_width_bytes;
+          unsigned bank = (unsigned)(word % (unsigned long long)Mc.shared_banks);
+          if (!active) { word = ~0ull - lane; bank = 0x80000000u + lane; }
+          unsigned lm = __match_any_sync(0xffffffffu, word);
+          bool lead = active && (__ffs(lm) - 1 == lane);
+          unsigned leaders = __ballot_sync(0xffffffffu, lead);
+          unsigned bm = __match_any_sync(0xffffffffu, bank);
+          unsigned per_bank = active ? __popc(bm & leaders) : 0u;
+          cnt = __reduce_max_sync(0xffffffffu, per_bank);
+        }
+        (void)amask;
+        total += mult * cnt;
+      }
+    }
+  }
+  __syncwarp();
+  return total;
+}
+
+// ---------------------------------------------------------------------------
+// one feature row (warp)
+// ---------------------------------------------------------------------------
+enum FeatIdx {
+  F_NUM_SCALARS = 0, F_PTS_PER_THREAD = 1, F_UG_REAL = 2, F_UG_THREAD = 8, F_ALLOC_G = 14,
+  F_G_AT_TASK = 17, F_GI_AT_TASK = 20, F_NUM_BLOCKS = 23, F_WARPS_PB = 24, F_ACTIVE_WARPS = 25,
+  F_THREADS_PB = 26, F_EXPR = 27, F_BLOCK_OCC = 28, F_WARP_UTIL = 29, F_IDLE = 30,
+  F_SH_LOADS = 31, F_GL_LOADS = 32, F_SH_STORES = 33, F_GL_STORES = 34, F_SH_ST_EFF = 35,
+  F_SH_LD_EFF = 36, F_GL_ST_EFF = 37, F_GL_LD_EFF = 38, F_WS_THREAD = 39, F_SH_OCC = 40,
+  F_SH_LIMIT = 41, F_MAX_WARP_OCC = 42, F_MAX_BLOCK_OCC = 43, F_NUM_REAL = 44, F_NUM_PROD = 45,
+  F_NUM_TASKS = 46, F_INNER_PAR = 47, F_TASKS_PER_CORE = 48, F_NUM_CORES = 49, F_INLINED = 50,
+  F_UB_POINT = 51, F_UL_POINT = 52, F_UB_TASK = 53, F_UL_TASK = 54, F_WORKING_SET = 55
+};
+
+template <int ND>
+__device__ void parallel_feats(double* v, const GsMachine& M, int n, const CF<ND>& kern) {
+  // featurize.py:317-363
+  const int64_t kt = kern.k_threads, ws = M.warp_size;
+  const int64_t aw = (n + ws - 1) / ws;
+  v[F_NUM_BLOCKS] = (double)kern.n_blocks;
+  v[F_WARPS_PB] = (double)((kt + ws - 1) / ws);
+  v[F_ACTIVE_WARPS] = (double)aw;
+  v[F_THREADS_PB] = (double)n;
+  v[F_WARP_UTIL] = (double)n / (double)(ws * aw);
+  v[F_IDLE] = (double)(ws * aw - n) / (double)M.max_threads_per_block;
+  v[F_BLOCK_OCC] = (double)kt / (double)M.max_threads_per_block;
+  int64_t wpb = (kt + ws - 1) / ws;
+  if (wpb < 1) wpb = 1;
+  int64_t by_shared;
+  if (kern.k_shared > 0) {
+    by_shared = M.shared_mem_per_sm / kern.k_shared;
+    if (by_shared < 1) by_shared = 1;
+    double o = (double)kern.k_shared / (double)M.shared_mem_per_block_limit;
+    v[F_SH_OCC] = o < 1.0 ? o : 1.0;
+  } else {
+    by_shared = M.max_active_blocks_per_sm;
+    v[F_SH_OCC] = 0.0;
+  }
+  int64_t mb = M.max_active_blocks_per_sm;
+  v[F_SH_LIMIT] = (double)(by_shared < mb ? by_shared : mb) / (double)mb;
+  int64_t act = mb;
+  if (by_shared < act) act = by_shared;
+  if (M.max_active_warps_per_sm / wpb < act) act = M.max_active_warps_per_sm / wpb;
+  if (act < 1) act = 1;
+  int64_t awsm = act * wpb;
+  if (awsm > M.max_active_warps_per_sm) awsm = M.max_active_warps_per_sm;
+  v[F_MAX_WARP_OCC] = (double)awsm / (double)M.max_active_warps_per_sm;
+  v[F_MAX_BLOCK_OCC] = (double)act / (double)mb;
+  v[F_NUM_TASKS] = (double)kern.n_blocks;
+  v[F_INNER_PAR] = (double)n;
+  v[F_NUM_CORES] = (double)M.num_sms;
+  v[F_TASKS_PER_CORE] = (double)kern.n_blocks / (double)M.num_sms;
+}
+
+template <int ND>
+__device__ void row_features(K1<ND>& k, WarpScr& W, int func, int si, bool inl, double* out) {
+  const int lane = lane_id();
+  const GsMachine& M = k.P->m;
+  Misc& m = *k.misc;
+  const CF<ND>& g = k.cf[func];
+  const GsFunc& fn = k.F[func];
+  const int gstage = fn.stage_begin + si;
+  int err = 0;
+  // defaults (featurize.py:78-147)
+  for (int i = lane; i < GS_NUM_FEATURES; i += 32) W.feat[i] = 0.0;
+  __syncwarp();
+  if (lane == 0) {
+    double* v = W.feat;
+    v[F_EXPR] = 1.0; v[F_BLOCK_OCC] = 1.0; v[F_WARP_UTIL] = 1.0;
+    v[F_SH_ST_EFF] = v[F_SH_LD_EFF] = v[F_GL_ST_EFF] = v[F_GL_LD_EFF] = 1.0;
+    v[F_SH_LIMIT] = 1.0; v[F_MAX_WARP_OCC] = 1.0; v[F_MAX_BLOCK_OCC] = 1.0;
+    v[F_INNER_PAR] = 1.0; v[F_NUM_CORES] = 1.0;
+    v[F_EXPR] = (double)k.ST[gstage].branching;
+  }
+  __syncwarp();
+  const CF<ND>* hp = inl ? (g.consumer >= 0 ? &k.cf[g.consumer] : nullptr) : &g;
+  if (inl && hp == nullptr) {
+    if (lane == 0) {
+      W.feat[F_INLINED] = (double)(g.calls > 1 ? g.calls : 1);
+      W.feat[F_NUM_SCALARS] = (double)g.calls;
+    }
+    __syncwarp();
+    for (int i = lane; i < GS_NUM_FEATURES; i += 32) out[i] = W.feat[i];
+    return;
+  }
+  const CF<ND>& h = *hp;
+  const CF<ND>& kern = k.cf[h.kernel];
+  // ---- reads attributed to this row, in order
+  int lo_r = inl ? 0 : k.rdb[2 * gstage], hi_r = inl ? m.nreads : k.rdb[2 * gstage + 1];
+  int nr = 0;
+  for (int j0 = lo_r; j0 < hi_r; j0 += 32) {
+    int j = j0 + lane;
+    bool hit = j < hi_r && k.rd[j].owner == func;
+    unsigned bal = __ballot_sync(0xffffffffu, hit);
+    int pos = nr + __popc(bal & ((1u << lane) - 1));
+    if (hit && pos < kRowReads) W.rl[pos] = (int16_t)j;
+    nr += __popc(bal);
+  }
+  if (nr > kRowReads) { if (lane == 0) atomicOr(k.gerr, E_ROWREADS); nr = kRowReads; }
+  __syncwarp();
+  if (lane == 0) {
+    int ng = 0;
+    for (int q = 0; q < nr; ++q) {
+      const RRead& r = k.rd[W.rl[q]];
+      int gi = -1;
+      for (int t = 0; t < ng; ++t) if (W.gtier[t] == r.tier && W.gprod[t] == r.producer) { gi = t; break; }
+      if (gi < 0) { gi = ng++; W.gtier[gi] = r.tier; W.gprod[gi] = r.producer; }
+      W.grp[q] = (int8_t)gi;
+    }
+    W.ngroups = ng;
+    W.nr = nr;
+    for (int b = 0; b < 4; ++b) for (int t = 0; t < 3; ++t) W.acc[b][t][0] = W.acc[b][t][1] = 0;
+    parallel_feats(W.feat, M, h.n_threads, kern);
+  }
+  __syncwarp();
+  const int ng = W.ngroups;
+  // ---- unions: tasks (box, group); boxes 0 region, 1 lane, 2 point, 3 block
+  const int nbox_tasks = 4 * ng;
+  for (int t = lane; t < nbox_tasks; t += 32) {
+    const int box = t / ng, gi = t % ng;
+    if (box == 0 && inl) continue;
+    int32_t blo[ND], bhi[ND];
+    if (box == 0) { for (int d = 0; d < ND; ++d) { blo[d] = g.rlo[d]; bhi[d] = g.rhi[d]; } }
+    else if (box == 1) { for (int d = 0; d < ND; ++d) { blo[d] = h.base[d]; bhi[d] = h.base[d] + h.ext[d] - 1; } }
+    else if (box == 2) { for (int d = 0; d < ND; ++d) { blo[d] = bhi[d] = h.base[d]; } }
+    else block_box(h, blo, bhi);
+    int64_t vol, lines;
+    union_count<ND>(k.A, k.rd, k.path, W.rl, W.grp, nr, gi, blo, bhi, vol, lines, err);
+    const int eb = k.F[W.gprod[gi]].elem_bytes;
+    atomicAdd(&W.acc[box][W.gtier[gi]][0], (unsigned long long)(vol * eb));
+    atomicAdd(&W.acc[box][W.gtier[gi]][1], (unsigned long long)lines);
+  }
+  __syncwarp();
+  // ---- loads (block 0 of the host's kernel)
+  unsigned long long ld[2] = {0, 0};
+  for (int q = 0; q < nr; ++q) {
+    const RRead& r = k.rd[W.rl[q]];
+    if (r.tier != T_GLOBAL && r.tier != T_SHARED) continue;
+    ld[r.tier] += warp_tx<ND>(k.A, k.path + r.pbeg, r.plen, false, h, k.cf[r.producer],
+                              k.F[r.producer].elem_bytes, r.tier, M, W, err);
+  }
+  unsigned long long st = 0;
+  if (!inl && (g.tier == T_GLOBAL || g.tier == T_SHARED))
+    st = warp_tx<ND>(k.A, nullptr, 0, true, g, g, fn.elem_bytes, g.tier, M, W, err);
+  // ---- working set at thread: fuse_at_thread children (featurize.py:482-492)
+  int64_t wsc = 0;
+  if (!inl) {
+    for (int f2 = lane; f2 < k.P->nf; f2 += 32) {
+      const CF<ND>& o = k.cf[f2];
+      if (o.kind == K_THREAD && o.consumer == func) wsc += alloc_of(o) * k.F[f2].elem_bytes;
+    }
+    for (int o = 16; o; o >>= 1) wsc += __shfl_xor_sync(0xffffffffu, wsc, o);
+  }
+  int lerr = err;
+  for (int o = 16; o; o >>= 1) lerr |= __shfl_xor_sync(0xffffffffu, lerr, o);
+  if (lane == 0) {
+    if (lerr) atomicOr(k.gerr, lerr);
+    double* v = W.feat;
+    const int gtx = M.global_transaction_bytes, stx = M.shared_banks * M.bank_width_bytes;
+    auto A_ = [&](int b, int t, int w) { return (double)W.acc[b][t][w]; };
+    for (int t = 0; t < 3; ++t) {
+      v[F_UG_THREAD + t] = A_(1, t, 0);
+      v[F_UG_THREAD + 3 + t] = A_(1, t, 1);
+    }
+    v[F_GL_LOADS] = (double)ld[0];
+    v[F_SH_LOADS] = (double)ld[1];
+    const double used_g = A_(3, 0, 0), used_s = A_(3, 1, 0);
+    if (v[F_GL_LOADS] > 0) { double e = used_g / (v[F_GL_LOADS] * gtx); v[F_GL_LD_EFF] = e < 1.0 ? e : 1.0; }
+    if (v[F_SH_LOADS] > 0) { double e = used_s / (v[F_SH_LOADS] * stx); v[F_SH_LD_EFF] = e < 1.0 ? e : 1.0; }
+    v[F_UB_TASK] = A_(3, 0, 0) + A_(3, 1, 0) + A_(3, 2, 0);
+    v[F_UL_TASK] = A_(3, 0, 1) + A_(3, 1, 1) + A_(3, 2, 1);
+    v[F_UB_POINT] = A_(2, 0, 0) + A_(2, 1, 0) + A_(2, 2, 0);
+    v[F_UL_POINT] = A_(2, 0, 1) + A_(2, 1, 1) + A_(2, 2, 1);
+    // the reference sums ints, so do the sums in integers
+    v[F_UB_TASK] = (double)(W.acc[3][0][0] + W.acc[3][1][0] + W.acc[3][2][0]);
+    v[F_UL_TASK] = (double)(W.acc[3][0][1] + W.acc[3][1][1] + W.acc[3][2][1]);
+    v[F_UB_POINT] = (double)(W.acc[2][0][0] + W.acc[2][1][0] + W.acc[2][2][0]);
+    v[F_UL_POINT] = (double)(W.acc[2][0][1] + W.acc[2][1][1] + W.acc[2][2][1]);
+    if (inl) {
+      v[F_INLINED] = (double)g.calls;
+      v[F_NUM_SCALARS] = (double)g.calls;
+      const int64_t den = kern.n_blocks * (int64_t)h.n_threads;
+      v[F_PTS_PER_THREAD] = den ? (double)g.calls / (double)den : 0.0;
+    } else {
+      const int64_t ppt = prod_ext(g), ppb = ppt * g.n_threads;
+      v[F_NUM_SCALARS] = (double)(ppb * kern.n_blocks);
+      v[F_PTS_PER_THREAD] = (double)ppt;
+      v[F_NUM_REAL] = v[F_NUM_PROD] = (double)g.realizations;
+      for (int t = 0; t < 3; ++t) {
+        v[F_UG_REAL + t] = A_(0, t, 0);
+        v[F_UG_REAL + 3 + t] = A_(0, t, 1);
+      }
+      int64_t alloc[3] = {0, 0, 0};
+      for (int gi = 0; gi < ng; ++gi)
+        alloc[W.gtier[gi]] += alloc_of(k.cf[W.gprod[gi]]) * k.F[W.gprod[gi]].elem_bytes;
+      for (int t = 0; t < 3; ++t) v[F_ALLOC_G + t] = (double)alloc[t];
+      const int eb = fn.elem_bytes;
+      const int64_t written = ppb * eb;
+      int32_t blo[ND], bhi[ND];
+      block_box(g, blo, bhi);
+      v[F_G_AT_TASK + g.tier] = (double)written;
+      v[F_GI_AT_TASK + g.tier] = (double)(((int64_t)bhi[0] - blo[0] + 1) * eb);
+      if (g.tier == T_GLOBAL) v[F_GL_STORES] = (double)st;
+      else if (g.tier == T_SHARED) v[F_SH_STORES] = (double)st;
+      if (g.tier == T_GLOBAL && st > 0) {
+        double e = (double)written / (double)(st * (unsigned long long)gtx); v[F_GL_ST_EFF] = e < 1.0 ? e : 1.0;
+      } else if (g.tier == T_SHARED && st > 0) {
+        double e = (double)written / (double)(st * (unsigned long long)stx); v[F_SH_ST_EFF] = e < 1.0 ? e : 1.0;
+      }
+      const int64_t al = alloc_of(g);
+      int64_t wsi = (g.tier == T_REGISTER ? al * eb : 0) + wsc;
+      double wsd = (double)wsi;
+      if (g.unrolled) { wsd += v[F_UG_THREAD + 0]; wsd += v[F_UG_THREAD + 1]; }
+      v[F_WS_THREAD] = wsd;
+      v[F_WORKING_SET] = (double)(al * eb);
+    }
+  }
+  __syncwarp();
+  for (int i = lane; i < GS_NUM_FEATURES; i += 32) out[i] = W.feat[i];
+}
+
+// ---------------------------------------------------------------------------
+// kernel
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void bulk_stage(void* dst_smem, const void* src, int bytes, uint64_t* bar) {
+  // TMA bulk copy global -> shared, completion on an mbarrier (single thread)
+  unsigned dst = (unsigned)__cvta_generic_to_shared(dst_smem);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+  asm volatile("fence.mbarrier_init.release.cluster;");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes));
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void bulk_wait(uint64_t* bar) {
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(b) : "memory");
+  }
+}
+
+template <int ND>
+__global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob,
+                                                        const GsDecision* __restrict__ dec, int64_t n, int S,
+                                                        double* __restrict__ feats, int32_t* __restrict__ row_key,
+                                                        int32_t* __restrict__ n_rows, uint8_t* __restrict__ verdict,
+                                                        Layout L, int* gerr) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x >> 5, lane = lane_id(), nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) bulk_stage(sm + L.blob, blob, P->blob_bytes, &bar);
+  K1<ND> k;
+  k.P = P;
+  k.F = reinterpret_cast<const GsFunc*>(sm + L.blob);
+  k.ST = reinterpret_cast<const GsStage*>(sm + L.blob + P->off_stages);
+  k.A = reinterpret_cast<const GsAccess*>(sm + L.blob + P->off_access);
+  k.dec = reinterpret_cast<GsDecision*>(sm + L.dec);
+  k.didx = reinterpret_cast<int16_t*>(sm + L.didx);
+  k.cf = reinterpret_cast<CF<ND>*>(sm + L.cf);
+  k.rd = reinterpret_cast<RRead*>(sm + L.reads);
+  k.path = reinterpret_cast<int16_t*>(sm + L.paths);
+  k.rdb = reinterpret_cast<int32_t*>(sm + L.rdb);
+  k.frd = reinterpret_cast<int32_t*>(sm + L.frd);
+  k.rows = reinterpret_cast<int32_t*>(sm + L.rows);
+  k.stack = reinterpret_cast<Frame*>(sm + L.stack);
+  k.volacc = reinterpret_cast<int64_t*>(sm + L.volacc);
+  k.touched = reinterpret_cast<int16_t*>(sm + L.touched);
+  k.misc = reinterpret_cast<Misc*>(sm + L.misc);
+  k.rcap = L.rcap; k.pcap = L.pcap; k.gerr = gerr;
+  WarpScr& W = *reinterpret_cast<WarpScr*>(sm + L.warps + warp * L.warp_bytes);
+  bulk_wait(&bar);
+  __syncthreads();
+  for (int64_t c = blockIdx.x; c < n; c += gridDim.x) {
+    if (warp == 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(dec + c * S);
+      uint4* dst = reinterpret_cast<uint4*>(k.dec);
+      for (int i = lane; i < S; i += 32) dst[i] = __ldg(src + i);   // 128-bit loads
+      __syncwarp();
+      unsigned cnt = 0;
+      for (int i0 = 0; i0 < S; i0 += 32) {
+        int i = i0 + lane;
+        unsigned b = __ballot_sync(0xffffffffu, i < S && k.dec[i].func != 0xFFFF);
+        cnt += __popc(b);
+      }
+      if (lane == 0) { k.misc->ndec = (int)cnt; k.misc->err = 0; k.misc->nrows = 0; }
+      __syncwarp();
+      resolve<ND>(k);
+      if (lane == 0) {
+        int v = k.misc->err ? 255 : prune_verdict<ND>(k);
+        if (k.misc->err) { atomicOr(gerr, k.misc->err); k.misc->nrows = 0; }
+        verdict[c] = (uint8_t)v;
+        n_rows[c] = k.misc->nrows;
+      }
+    }
+    __syncthreads();
+    const int nr = k.misc->nrows;
+    for (int r = warp; r < nr; r += nw) {
+      const int key = k.rows[r];
+      const int f = key >> 8, si = key & 255;
+      row_features<ND>(k, W, f, si, k.cf[f].kind == K_INLINE, feats + ((int64_t)c * L.R + r) * GS_NUM_FEATURES);
+      if (lane == 0) row_key[c * L.R + r] = key;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace gs
+
+// ---------------------------------------------------------------------------
+// host launch helpers (used by api.cu)
+// ---------------------------------------------------------------------------
+namespace gs {
+
+template <int ND>
+static int cf_size() { return (int)sizeof(CF<ND>); }
+
+Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rcap, int pcap, int nwarps) {
+  auto al = [](int x) { return (x + 15) & ~15; };
+  Layout L{};
+  int o = 0;
+  L.blob = o; o += al(blob_bytes);
+  L.dec = o; o += al(S * 16);
+  L.didx = o; o += al(nf * 2);
+  int cfs = nd == 1 ? cf_size<1>() : nd == 2 ? cf_size<2>() : nd == 3 ? cf_size<3>() : cf_size<4>();
+  L.cf = o; o += al(nf * cfs);
+  L.reads = o; o += al(rcap * (int)sizeof(RRead));
+  L.paths = o; o += al(pcap * 2);
+  L.rdb = o; o += al(2 * ns * 4);
+  L.frd = o; o += al(nf * 4);
+  L.rows = o; o += al(R * 4);
+  L.stack = o; o += al((nf + 2) * (int)sizeof(Frame));
+  L.volacc = o; o += al(nf * 8);
+  L.touched = o; o += al(2 * nf * 2 + 2);
+  L.misc = o; o += al((int)sizeof(Misc));
+  L.warp_bytes = al((int)sizeof(WarpScr));
+  L.warps = o; o += nwarps * L.warp_bytes;
+  L.total = o;
+  L.rcap = rcap; L.pcap = pcap; L.S = S; L.R = R;
+  return L;
+}
+
+int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
+                     double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, const Layout& L,
+                     int nwarps, int grid, int* gerr, cudaStream_t st) {
+  dim3 b(nwarps * 32);
+  switch (nd) {
+#define GS_CASE(D)                                                                                  \
+  case D:                                                                                           \
+    cudaFuncSetAttribute(featurize_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total); \
+    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, L, gerr); \
+    break;
+    GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4)
+#undef GS_CASE
+    default: return -1;
+  }
+  return 0;
+}
+
+int featurize_occupancy(int nd, int nwarps, int smem) {
+  int nb = 0;
+  switch (nd) {
+    case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, featurize_kernel<1>, nwarps * 32, smem); break;
+    case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, featurize_kernel<2>, nwarps * 32, smem); break;
+    case 3: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, featurize_kernel<3>, nwarps * 32, smem); break;
+    default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, featurize_kernel<4>, nwarps * 32, smem); break;
+  }
+  return nb;
+}
+
+}  // namespace gs

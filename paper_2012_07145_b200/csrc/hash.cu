@@ -1,0 +1,171 @@
+// K3 — structural hash = blake2b-64 over the bytes of Python repr() of the
+// canonical decision tuple (reference loopnest.py:131-165).  One thread per
+// candidate streams the repr bytes straight into the blake2b compressor:
+// func names come from a pre-rendered repr table (host), walked in Python
+// str order (name_rank), so no string sorting happens on the device.
+#include "gs_internal.cuh"
+
+namespace gs {
+
+constexpr int kHashMaxFuncs = 1024;
+
+__constant__ uint64_t kIV[8] = {0x6a09e667f3bcc908ULL, 0xbb67ae8584caa73bULL, 0x3c6ef372fe94f82bULL,
+                                0xa54ff53a5f1d36f1ULL, 0x510e527fade682d1ULL, 0x9b05688c2b3e6c1fULL,
+                                0x1f83d9abfb41bd6bULL, 0x5be0cd19137e2179ULL};
+__constant__ uint8_t kSigma[12][16] = {
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+    {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4}, {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+    {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13}, {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+    {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11}, {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+    {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5}, {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
+
+__device__ __forceinline__ uint64_t rotr(uint64_t x, int n) { return (x >> n) | (x << (64 - n)); }
+
+struct Blake {
+  uint64_t h[8];
+  uint64_t m[16];   // current block (little-endian words)
+  uint64_t t;       // bytes compressed so far
+  int fill;         // bytes in the current block
+
+  __device__ void init() {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[i] = kIV[i];
+    h[0] ^= 0x01010000ULL ^ 8ULL;   // digest 8 bytes, no key
+    t = 0; fill = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) m[i] = 0;
+  }
+  __device__ void compress(bool last) {
+    uint64_t v[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { v[i] = h[i]; v[i + 8] = kIV[i]; }
+    v[12] ^= t;
+    if (last) v[14] = ~v[14];
+#pragma unroll
+    for (int r = 0; r < 12; ++r) {
+      const uint8_t* s = kSigma[r];
+#define G(a, b, c, d, x, y)                      \
+  v[a] = v[a] + v[b] + m[s[x]];                  \
+  v[d] = rotr(v[d] ^ v[a], 32);                  \
+  v[c] = v[c] + v[d];                            \
+  v[b] = rotr(v[b] ^ v[c], 24);                  \
+  v[a] = v[a] + v[b] + m[s[y]];                  \
+  v[d] = rotr(v[d] ^ v[a], 16);                  \
+  v[c] = v[c] + v[d];                            \
+  v[b] = rotr(v[b] ^ v[c], 63);
+      G(0, 4, 8, 12, 0, 1) G(1, 5, 9, 13, 2, 3) G(2, 6, 10, 14, 4, 5) G(3, 7, 11, 15, 6, 7)
+      G(0, 5, 10, 15, 8, 9) G(1, 6, 11, 12, 10, 11) G(2, 7, 8, 13, 12, 13) G(3, 4, 9, 14, 14, 15)
+#undef G
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[i] ^= v[i] ^ v[i + 8];
+  }
+  __device__ __forceinline__ void byte(uint8_t b) {
+    if (fill == 128) {
+      t += 128;
+      compress(false);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) m[i] = 0;
+      fill = 0;
+    }
+    // dynamic index into m: keep it in local memory-friendly form
+    m[fill >> 3] |= (uint64_t)b << ((fill & 7) * 8);
+    ++fill;
+  }
+  __device__ void str(const char* s) { while (*s) byte((uint8_t)*s++); }
+  __device__ void bytes(const uint8_t* p, int n) { for (int i = 0; i < n; ++i) byte(p[i]); }
+  __device__ uint64_t final() {
+    t += fill;
+    compress(true);
+    return h[0];
+  }
+};
+
+__device__ const char* kind_repr(int k) {
+  switch (k) {
+    case GS_ROOT: return "'compute_root'";
+    case GS_FUSE_BLOCK: return "'fuse_at_block'";
+    case GS_FUSE_THREAD: return "'fuse_at_thread'";
+    default: return "'inline'";
+  }
+}
+
+__global__ void hash_kernel(const GsDecision* __restrict__ dec, int64_t n, int S, int nf, int depth,
+                            const int32_t* __restrict__ sorted_funcs, const uint8_t* __restrict__ names,
+                            const int32_t* __restrict__ name_off, uint64_t* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const GsDecision* d = dec + c * S;
+  int16_t didx[kHashMaxFuncs];
+  for (int f = 0; f < nf; ++f) didx[f] = -1;
+  int nd = 0;
+  for (int i = 0; i < S && d[i].func != 0xFFFF; ++i) { didx[d[i].func] = (int16_t)i; ++nd; }
+  Blake b;
+  b.init();
+  auto name = [&](int f) { b.bytes(names + name_off[f], name_off[f + 1] - name_off[f]); };
+  if (depth == 0) {
+    b.str("('kernels', (");
+    int cnt = 0;
+    for (int q = 0; q < nf; ++q) {
+      int f = sorted_funcs[q];
+      int i = didx[f];
+      if (i < 0 || d[i].kind != GS_ROOT) continue;
+      if (cnt) b.str(", ");
+      name(f);
+      ++cnt;
+    }
+    if (cnt == 1) b.byte(',');
+    b.str("))");
+  } else {
+    b.byte('(');
+    b.byte((uint8_t)('0' + depth));
+    b.str(", (");
+    int cnt = 0;
+    for (int q = 0; q < nf; ++q) {
+      int f = sorted_funcs[q];
+      int i = didx[f];
+      if (i < 0) continue;
+      if (cnt) b.str(", ");
+      b.byte('(');
+      name(f);
+      b.str(", ");
+      b.str(kind_repr(d[i].kind));
+      b.str(", ");
+      // kernel_of (loopnest.py:87-94)
+      int kf = f, ki = i, guard = 0;
+      while (ki >= 0 && (d[ki].kind == GS_FUSE_BLOCK || d[ki].kind == GS_FUSE_THREAD) && guard++ < nf) {
+        kf = d[ki].consumer;
+        ki = kf < nf ? didx[kf] : -1;
+      }
+      if (ki < 0 || d[ki].kind == GS_INLINE) b.str("None");
+      else name(kf);
+      if (depth >= 2) {
+        b.str(", ");
+        if (d[i].consumer == 0xFFFF) b.str("None");
+        else name(d[i].consumer);
+      }
+      if (depth >= 3) {
+        b.str((d[i].flags & 1) ? ", True" : ", False");
+        b.str((d[i].flags & 2) ? ", True" : ", False");
+      }
+      b.byte(')');
+      ++cnt;
+    }
+    if (cnt == 1) b.byte(',');
+    b.str("))");
+  }
+  out[c] = b.final();
+}
+
+int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, const int32_t* sorted_funcs,
+                const uint8_t* names, const int32_t* name_off, uint64_t* out, cudaStream_t st) {
+  if (n == 0) return 0;
+  if (nf > kHashMaxFuncs) return -1;
+  if (depth > 3) depth = 3;
+  int64_t blocks = (n + 127) / 128;
+  hash_kernel<<<(unsigned)blocks, 128, 0, st>>>(dec, n, S, nf, depth, sorted_funcs, names, name_off, out);
+  return 0;
+}
+
+}  // namespace gs

@@ -1,0 +1,164 @@
+"""Device-side scoring engine: one object per (pipeline, machine, thresholds).
+
+Thin stream-ordered wrappers around the C ABI.  Device memory and streams
+come from PyTorch (plumbing only); all arithmetic happens in the sm_100a
+kernels of libgs_sched.so.  Nothing here falls back to a CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .descriptor import DECISION_DTYPE, PackedPipeline
+from .params import DEFAULT_THRESHOLDS, MachineParams
+
+NF = 56
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Scorer:
+    """Featurize, cost, hash, bucket and cut candidate batches on one GPU."""
+
+    def __init__(self, graph, params=None, thresholds=None, weights=None, device=None):
+        if not torch.cuda.is_available():
+            raise _lib.GsError("no CUDA device: the scoring path runs only on the GPU")
+        self.lib = _lib.load()
+        self.device = torch.device(device or "cuda")
+        self.params = params or MachineParams()
+        self.thresholds = thresholds or DEFAULT_THRESHOLDS
+        self.packed = PackedPipeline(graph, self.params, self.thresholds)
+        self.handle = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.gs_pipeline_create(C.byref(self.packed.desc), C.byref(self.handle)))
+        self.R = max(1, self.lib.gs_pipeline_max_rows(self.handle))
+        self.S = max(1, self.packed.max_decisions())
+        self._weights_key = None
+        if weights is not None:
+            self.set_weights(weights)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.lib.gs_pipeline_destroy(self.handle)
+        except Exception:
+            pass
+
+    # -- weights --------------------------------------------------------------
+    def set_weights(self, weights):
+        key = id(weights)
+        if key == self._weights_key:
+            return
+        t = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in weights.tensors.items()}
+        E, H = t["algo_b"].shape[0], t["head_b"].shape[0]
+        arrs = [t[n] for n in ("algo_w", "algo_b", "sched_w", "sched_b", "head_w", "head_b",
+                               "out_w", "out_b")]
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.gs_set_weights(self.handle, E, H,
+                                               *[C.c_void_p(a.ctypes.data) for a in arrs]))
+        self._weights_key = key
+        self._weights_ref = weights
+
+    # -- inputs ---------------------------------------------------------------
+    def upload(self, candidates, pin=False) -> torch.Tensor:
+        arr = self.packed.pack(candidates, self.S)
+        return self.to_device(arr, pin)
+
+    def to_device(self, arr: np.ndarray, pin=False) -> torch.Tensor:
+        assert arr.dtype == DECISION_DTYPE
+        host = torch.from_numpy(arr.view(np.uint8).reshape(arr.shape[0], -1))
+        if pin:
+            host = host.pin_memory()
+        return host.to(self.device, non_blocking=pin)
+
+    # -- K1 -------------------------------------------------------------------
+    def featurize(self, dec: torch.Tensor, out=None):
+        n = dec.shape[0]
+        S = dec.shape[1] // 16
+        if out is None:
+            out = dict(
+                feats=torch.empty((n, self.R, NF), dtype=torch.float64, device=self.device),
+                row_key=torch.empty((n, self.R), dtype=torch.int32, device=self.device),
+                n_rows=torch.empty((n,), dtype=torch.int32, device=self.device),
+                verdict=torch.empty((n,), dtype=torch.uint8, device=self.device))
+        _lib.check(self.lib.gs_featurize(self.handle, _ptr(dec), n, S, _ptr(out["feats"]),
+                                         _ptr(out["row_key"]), _ptr(out["n_rows"]),
+                                         _ptr(out["verdict"]), _stream()))
+        return out
+
+    def check(self):
+        """Synchronize and raise on any device-side capacity / schedule error."""
+        _lib.check(self.lib.gs_check(self.handle, _stream()))
+
+    # -- K2 -------------------------------------------------------------------
+    def cost(self, f, rows=False, basis=False, total=None):
+        n = f["feats"].shape[0]
+        if total is None:
+            total = torch.empty((n,), dtype=torch.float64, device=self.device)
+        rc = torch.empty((n, self.R), dtype=torch.float64, device=self.device) if rows else None
+        gh = torch.empty((n, self.R, 31), dtype=torch.float64, device=self.device) if basis else None
+        _lib.check(self.lib.gs_cost(self.handle, _ptr(f["feats"]), _ptr(f["row_key"]),
+                                    _ptr(f["n_rows"]), n, _ptr(total), _ptr(rc), _ptr(gh), _stream()))
+        return total, rc, gh
+
+    # -- K3 -------------------------------------------------------------------
+    def struct_hash(self, dec: torch.Tensor, depth: int, out=None):
+        if depth < 0:
+            raise ValueError("depth must be >= 0")
+        n = dec.shape[0]
+        if out is None:
+            out = torch.empty((n,), dtype=torch.int64, device=self.device)
+        _lib.check(self.lib.gs_struct_hash(self.handle, _ptr(dec), n, dec.shape[1] // 16, depth,
+                                           _ptr(out), _stream()))
+        return out
+
+    # -- K4 -------------------------------------------------------------------
+    def select(self, hashes: torch.Tensor, verdict: torch.Tensor, phase_seed: int, rejects=True):
+        n = hashes.shape[0]
+        wsb = self.lib.gs_select_workspace_bytes(n)
+        ws = torch.empty((wsb,), dtype=torch.uint8, device=self.device)
+        rep = torch.empty((max(1, n),), dtype=torch.int64, device=self.device)
+        rej = torch.empty((max(1, n),), dtype=torch.int64, device=self.device) if rejects else None
+        cnt = torch.zeros((2,), dtype=torch.int64, device=self.device)
+        _lib.check(self.lib.gs_select_reps(_ptr(hashes), _ptr(verdict), n,
+                                           C.c_uint64(phase_seed & 0xFFFFFFFFFFFFFFFF), _ptr(ws), wsb,
+                                           _ptr(rep), C.c_void_p(cnt.data_ptr()), _ptr(rej),
+                                           C.c_void_p(cnt.data_ptr() + 8), _stream()))
+        return rep, rej, cnt
+
+    # -- K5 -------------------------------------------------------------------
+    def beam_topk(self, costs, pass_hash, flagged, penalty, temperature, phase_seed, k,
+                  bottom=True):
+        n = costs.shape[0]
+        wsb = self.lib.gs_topk_workspace_bytes(n)
+        ws = torch.empty((wsb,), dtype=torch.uint8, device=self.device)
+        pos = torch.empty((max(1, min(k, n)),), dtype=torch.int64, device=self.device)
+        cnt = torch.zeros((1,), dtype=torch.int64, device=self.device)
+        bot = torch.empty((max(1, n),), dtype=torch.uint8, device=self.device) if bottom else None
+        fl = flagged if flagged is not None and flagged.numel() else None
+        _lib.check(self.lib.gs_beam_topk(_ptr(costs), _ptr(pass_hash), n, _ptr(fl),
+                                         0 if fl is None else fl.numel(), float(penalty),
+                                         float(temperature),
+                                         C.c_uint64(phase_seed & 0xFFFFFFFFFFFFFFFF), k, _ptr(ws),
+                                         wsb, _ptr(pos), _ptr(cnt), _ptr(bot), _stream()))
+        return pos, cnt, bot
+
+
+def u64_sorted_tensor(values, device) -> torch.Tensor:
+    """Sorted uint64 values as an int64 tensor holding the same bits."""
+    arr = np.array(sorted(int(v) & 0xFFFFFFFFFFFFFFFF for v in values), dtype=np.uint64)
+    return torch.from_numpy(arr.view(np.int64)).to(device)
+
+
+def as_u64(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint64)
