@@ -165,13 +165,15 @@ int gs_select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n,
  * totals of the reps (rep order); pass_hash: hash at pass depth per rep;
  * flagged: sorted array of flagged hashes at that depth.  Writes the first
  * k rep positions (ascending key, ties by rep order) to out_pos and the
- * count to *n_out (k <= 2048).  bottom (nullable) gets 1 for reps in the
+ * count to *n_out.  tie_band > 0: keys within that relative distance
+ * are ordered by rep position (the reference's stable order of exact
+ * ties, which its BLAS-order fp64 sums hit by rounding).  bottom (nullable) gets 1 for reps in the
  * bottom half by unpenalized cost (stable), the memo-flag set of
  * search.py:196-200.  Workspace: gs_topk_workspace_bytes(n). */
 int64_t gs_topk_workspace_bytes(int64_t n);
 int gs_beam_topk(const double* costs, const uint64_t* pass_hash, int64_t n,
                  const uint64_t* flagged, int64_t n_flagged, double penalty,
-                 double temperature, uint64_t phase_seed, int64_t k,
+                 double temperature, uint64_t phase_seed, int64_t k, double tie_band,
                  void* workspace, int64_t ws_bytes, int64_t* out_pos,
                  int64_t* n_out, uint8_t* bottom, void* stream);
 

@@ -50,7 +50,7 @@ def load(path: str = LIB_PATH):
         "gs_select_workspace_bytes": (i64, [i64]),
         "gs_select_reps": (i32, [V, V, i64, u64, V, i64, V, V, V, V, V]),
         "gs_topk_workspace_bytes": (i64, [i64]),
-        "gs_beam_topk": (i32, [V, V, i64, V, i64, dbl, dbl, u64, i64, V, i64, V, V, V, V]),
+        "gs_beam_topk": (i32, [V, V, i64, V, i64, dbl, dbl, u64, i64, dbl, V, i64, V, V, V, V]),
         "gs_check": (i32, [P, V]),
     }
     for name, (res, args) in sig.items():

@@ -24,8 +24,8 @@ int select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, uint6
                 cudaStream_t st);
 int64_t topk_workspace_bytes(int64_t n);
 int beam_topk(const double* costs, const uint64_t* ph, int64_t n, const uint64_t* flagged, int64_t nflag,
-              double penalty, double temperature, uint64_t phase_seed, int64_t k, void* ws, int64_t ws_bytes,
-              int64_t* out_pos, int64_t* n_out, uint8_t* bottom, cudaStream_t st);
+              double penalty, double temperature, uint64_t phase_seed, int64_t k, double band, void* ws,
+              int64_t ws_bytes, int64_t* out_pos, int64_t* n_out, uint8_t* bottom, cudaStream_t st);
 }  // namespace gs
 
 using namespace gs;
@@ -237,9 +237,9 @@ int gs_select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, ui
 int64_t gs_topk_workspace_bytes(int64_t n) { return topk_workspace_bytes(n); }
 
 int gs_beam_topk(const double* costs, const uint64_t* pass_hash, int64_t n, const uint64_t* flagged,
-                 int64_t n_flagged, double penalty, double temperature, uint64_t phase_seed, int64_t k, void* ws,
+                 int64_t n_flagged, double penalty, double temperature, uint64_t phase_seed, int64_t k, double tie_band, void* ws,
                  int64_t ws_bytes, int64_t* out_pos, int64_t* n_out, uint8_t* bottom, void* stream) {
-  int rc = beam_topk(costs, pass_hash, n, flagged, n_flagged, penalty, temperature, phase_seed, k, ws, ws_bytes,
+  int rc = beam_topk(costs, pass_hash, n, flagged, n_flagged, penalty, temperature, phase_seed, k, tie_band, ws, ws_bytes,
                      out_pos, n_out, bottom, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "beam_topk: workspace too small or k > 2048");
   CK(cudaGetLastError());

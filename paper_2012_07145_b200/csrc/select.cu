@@ -463,26 +463,139 @@ __global__ void __launch_bounds__(kTopNT) topk_kernel(const uint64_t* __restrict
   }
 }
 
+// k > kSortCap (e.g. sampling-free exhaustive searches): full stable sort
+__global__ void bottom_from_sorted(const uint32_t* __restrict__ order, int64_t n, uint8_t* __restrict__ bottom) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) bottom[order[i]] = (n > 1 && i >= n / 2) ? 1 : 0;
+}
+__global__ void copy_pos(const uint32_t* __restrict__ order, int64_t k, int64_t* __restrict__ out,
+                         int64_t* __restrict__ n_out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) out[i] = order[i];
+  if (i == 0) *n_out = k;
+}
+
+// Tie band: after an exact sort by key, adjacent keys within `band`
+// (relative) join one group; the final order is (group, position).  The
+// reference orders exact ties by representative position (stable sort); its
+// fp64 sums of permuted per-stage costs tie by rounding luck, which ours
+// (ulp-different row costs) cannot reproduce bit for bit.
+__global__ void band_flags(const uint64_t* __restrict__ skey, const double* __restrict__ kval,
+                           const uint32_t* __restrict__ order, int64_t n, double band,
+                           uint32_t* __restrict__ brk) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == 0) { brk[i] = 0; return; }
+  const double a = kval[order[i - 1]], b = kval[order[i]];
+  const double m = fmax(fabs(a), fabs(b));
+  brk[i] = (b - a) > band * m ? 1u : 0u;
+  (void)skey;
+}
+__global__ void band_keys(const uint32_t* __restrict__ gid, const uint32_t* __restrict__ order, int64_t n,
+                          uint64_t* __restrict__ key2) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) key2[i] = ((uint64_t)gid[i] << 32) | order[i];
+}
+
+static size_t sort_temp_bytes(int64_t n) {
+  size_t a = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
+  return a;
+}
+
 int64_t topk_workspace_bytes(int64_t n) {
   if (n < 1) n = 1;
-  return (int64_t)(align256(8 * n) * 2 + align256(8 * n) + align256(n));
+  size_t scan = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, scan, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
+  size_t sk = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, sk, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int)n);
+  size_t tmp = std::max(std::max(scan, sk), sort_temp_bytes(n));
+  return (int64_t)(align256(8 * n) * 6 + align256(n) + align256(4 * n) * 4 + align256(tmp));
+}
+
+struct TopkWs {
+  uint64_t *key, *ckey, *kout, *key2, *key2o;
+  double* kval;
+  uint8_t* sel;
+  uint32_t *vin, *vout, *brk, *gid;
+  void* tmp;
+  size_t tmp_bytes;
+};
+
+// order[i] = position of the i-th element by (band group of key, position)
+static void band_order(TopkWs& w, const uint64_t* key, const double* val, int64_t n, double band,
+                       cudaStream_t st) {
+  const unsigned G = (unsigned)((n + 255) / 256);
+  iota_kernel<<<G, 256, 0, st>>>(w.vin, n);
+  size_t tb = w.tmp_bytes;
+  cub::DeviceRadixSort::SortPairs(w.tmp, tb, key, w.kout, w.vin, w.vout, (int)n, 0, 64, st);
+  band_flags<<<G, 256, 0, st>>>(w.kout, val, w.vout, n, band, w.brk);
+  tb = w.tmp_bytes;
+  cub::DeviceScan::InclusiveSum(w.tmp, tb, w.brk, w.gid, (int)n, st);
+  band_keys<<<G, 256, 0, st>>>(w.gid, w.vout, n, w.key2);
+  tb = w.tmp_bytes;
+  cub::DeviceRadixSort::SortKeys(w.tmp, tb, w.key2, w.key2o, (int)n, 0, 64, st);
+}
+
+__global__ void pos_from_key2(const uint64_t* __restrict__ key2o, int64_t k, int64_t* __restrict__ out,
+                              int64_t* __restrict__ n_out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) out[i] = (int64_t)(key2o[i] & 0xFFFFFFFFull);
+  if (i == 0) *n_out = k;
+}
+__global__ void bottom_from_key2(const uint64_t* __restrict__ key2o, int64_t n, uint8_t* __restrict__ bottom) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) bottom[key2o[i] & 0xFFFFFFFFull] = (n > 1 && i >= n / 2) ? 1 : 0;
 }
 
 int beam_topk(const double* costs, const uint64_t* ph, int64_t n, const uint64_t* flagged, int64_t nflag,
-              double penalty, double temperature, uint64_t phase_seed, int64_t k, void* ws, int64_t ws_bytes,
-              int64_t* out_pos, int64_t* n_out, uint8_t* bottom, cudaStream_t st) {
+              double penalty, double temperature, uint64_t phase_seed, int64_t k, double band, void* ws,
+              int64_t ws_bytes, int64_t* out_pos, int64_t* n_out, uint8_t* bottom, cudaStream_t st) {
   if (n <= 0) { cudaMemsetAsync(n_out, 0, 8, st); return 0; }
   if (topk_workspace_bytes(n) > ws_bytes) return -2;
-  if (k > kSortCap) return -3;
+  if (n >= (int64_t)0xFFFFFFFF) return -3;
+  if (k > n) k = n;
   char* p = (char*)ws;
-  uint64_t* key = (uint64_t*)p; p += align256(8 * n);
-  uint64_t* ckey = (uint64_t*)p; p += align256(8 * n);
-  double* kval = (double*)p; p += align256(8 * n);
-  uint8_t* sel = (uint8_t*)p;
+  TopkWs w;
+  w.key = (uint64_t*)p; p += align256(8 * n);
+  w.ckey = (uint64_t*)p; p += align256(8 * n);
+  w.kval = (double*)p; p += align256(8 * n);
+  w.kout = (uint64_t*)p; p += align256(8 * n);
+  w.key2 = (uint64_t*)p; p += align256(8 * n);
+  w.key2o = (uint64_t*)p; p += align256(8 * n);
+  w.sel = (uint8_t*)p; p += align256(n);
+  w.vin = (uint32_t*)p; p += align256(4 * n);
+  w.vout = (uint32_t*)p; p += align256(4 * n);
+  w.brk = (uint32_t*)p; p += align256(4 * n);
+  w.gid = (uint32_t*)p; p += align256(4 * n);
+  w.tmp = p;
+  w.tmp_bytes = (size_t)(ws_bytes - (int64_t)(p - (char*)ws));
   const unsigned G = (unsigned)((n + 255) / 256);
-  keys_kernel<<<G, 256, 0, st>>>(costs, ph, n, flagged, nflag, penalty, key, ckey, kval);
-  if (temperature > 0) gumbel_kernel<<<1, 32, 0, st>>>(kval, key, n, temperature, phase_seed);
-  topk_kernel<<<1, kTopNT, 0, st>>>(key, ckey, n, k, sel, out_pos, n_out, bottom);
+  keys_kernel<<<G, 256, 0, st>>>(costs, ph, n, flagged, nflag, penalty, w.key, w.ckey, w.kval);
+  if (temperature > 0) gumbel_kernel<<<1, 32, 0, st>>>(w.kval, w.key, n, temperature, phase_seed);
+  if (band > 0) {
+    band_order(w, w.key, w.kval, n, band, st);
+    pos_from_key2<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(w.key2o, k, out_pos, n_out);
+    if (bottom) {
+      band_order(w, w.ckey, costs, n, band, st);
+      bottom_from_key2<<<G, 256, 0, st>>>(w.key2o, n, bottom);
+    }
+    return 0;
+  }
+  if (k <= kSortCap) {   // exact keys: hand-written single-CTA radix select + bitonic sort
+    topk_kernel<<<1, kTopNT, 0, st>>>(w.key, w.ckey, n, k, w.sel, out_pos, n_out, bottom);
+    return 0;
+  }
+  iota_kernel<<<G, 256, 0, st>>>(w.vin, n);
+  size_t tb = w.tmp_bytes;
+  cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.key, w.kout, w.vin, w.vout, (int)n, 0, 64, st);
+  copy_pos<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(w.vout, k, out_pos, n_out);
+  if (bottom) {
+    tb = w.tmp_bytes;
+    cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.ckey, w.kout, w.vin, w.vout, (int)n, 0, 64, st);
+    bottom_from_sorted<<<G, 256, 0, st>>>(w.vout, n, bottom);
+  }
   return 0;
 }
 

@@ -17,6 +17,11 @@ from .descriptor import DECISION_DTYPE, PackedPipeline
 from .params import DEFAULT_THRESHOLDS, MachineParams
 
 NF = 56
+# Relative distance under which two cut keys count as tied and keep
+# representative order (see csrc/select.cu band_flags).  Our fp64 totals sit
+# within ~1e-15 of the reference's; its ties between permuted per-stage cost
+# multisets are rounding coincidences we cannot reproduce bit for bit.
+TIE_BAND = 1e-12
 
 
 def _ptr(t):
@@ -138,7 +143,7 @@ class Scorer:
 
     # -- K5 -------------------------------------------------------------------
     def beam_topk(self, costs, pass_hash, flagged, penalty, temperature, phase_seed, k,
-                  bottom=True):
+                  bottom=True, tie_band=TIE_BAND):
         n = costs.shape[0]
         wsb = self.lib.gs_topk_workspace_bytes(n)
         ws = torch.empty((wsb,), dtype=torch.uint8, device=self.device)
@@ -149,7 +154,8 @@ class Scorer:
         _lib.check(self.lib.gs_beam_topk(_ptr(costs), _ptr(pass_hash), n, _ptr(fl),
                                          0 if fl is None else fl.numel(), float(penalty),
                                          float(temperature),
-                                         C.c_uint64(phase_seed & 0xFFFFFFFFFFFFFFFF), k, _ptr(ws),
+                                         C.c_uint64(phase_seed & 0xFFFFFFFFFFFFFFFF), k,
+                                         float(tie_band), _ptr(ws),
                                          wsb, _ptr(pos), _ptr(cnt), _ptr(bot), _stream()))
         return pos, cnt, bot
 

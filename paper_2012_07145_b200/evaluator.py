@@ -1,0 +1,161 @@
+"""Drop-in surface for the reference search (`gpusched`).
+
+* `GpuCostEvaluator` — subclass of `gpusched.search.CostEvaluator`
+  (search.py:90-124; the search type-checks with isinstance at
+  search.py:302-303, 331-332, 351-352) whose `stage_basis` / `cost` run the
+  sm_100a path.  When `gpusched` is not importable it derives from a local
+  mirror with the same surface, so this package also stands alone.
+* `gpu_cut` — same signature and results as `gpusched.search._cut`
+  (search.py:168-201); `install()` swaps it into the module global the
+  search resolves at call time (search.py:254), so the unchanged search,
+  freeze pre-pass and driver batch whole phases onto the GPU.
+"""
+
+from __future__ import annotations
+
+import contextlib
+
+import numpy as np
+import torch
+
+from .cut import beam_cut
+from .engine import Scorer
+from .params import DEFAULT_THRESHOLDS
+
+try:  # the reference is the user's own installation; optional here
+    from gpusched.search import CostEvaluator as _Base  # type: ignore
+    from gpusched.options import PruneReport as _PruneReport  # type: ignore
+    HAVE_REFERENCE = True
+except Exception:  # pragma: no cover - standalone use
+    HAVE_REFERENCE = False
+
+    class _Base:  # mirror of search.py:90-101
+        def __init__(self, weights, params):
+            self.weights = weights
+            self.params = params
+            self._basis_cache = {}
+
+    class _PruneReport:  # mirror of options.py:44-57
+        REASONS = ("excessive_recompute", "idle_sms", "poor_warp_utilization",
+                   "serial_too_large", "thread_alloc_dynamic_or_large", "hardware_limit")
+
+        def __init__(self, reason, detail):
+            if reason not in self.REASONS:
+                raise ValueError(f"unknown prune reason {reason!r}")
+            self.reason, self.detail = reason, detail
+
+
+_SCORERS: dict = {}
+
+
+def scorer_for(graph, params, thresholds, weights) -> Scorer:
+    """One device pipeline per (graph, machine, thresholds); weights are
+    re-uploaded whenever the weights object changes (driver.py:110, 219)."""
+    key = (id(graph), params, thresholds)
+    sc = _SCORERS.get(key)
+    if sc is None or sc.packed.graph is not graph:
+        sc = Scorer(graph, params, thresholds)
+        _SCORERS[key] = sc
+    sc.set_weights(weights)
+    return sc
+
+
+class GpuCostEvaluator(_Base):
+    """`CostEvaluator` whose featurization and costing run on the B200."""
+
+    def __init__(self, weights, params, thresholds=None):
+        _Base.__init__(self, weights, params)
+        self.thresholds = thresholds or DEFAULT_THRESHOLDS
+
+    def _run(self, state, graph):
+        sc = scorer_for(graph, self.params, self.thresholds, self.weights)
+        dec = sc.upload([state])
+        f = sc.featurize(dec)
+        total, rows, gh = sc.cost(f, rows=True, basis=True)
+        sc.check()
+        n = int(f["n_rows"][0].item())
+        keys = sc.packed.row_keys(f["row_key"][0, :n].cpu().numpy())
+        return sc, f, n, keys, float(total[0].item()), rows[0, :n].cpu().numpy(), gh[0, :n].cpu().numpy()
+
+    def _fill_cache(self, sc, f, n, keys, gh, state, graph):
+        key = (id(graph), state.decisions)
+        if key in self._basis_cache:
+            return self._basis_cache[key]
+        feats = f["feats"][0, :n].cpu().numpy()
+        algo = sc.packed.algo
+        hit = []
+        for r, k in enumerate(keys):
+            xa = algo[sc.packed.stage_index[k]].copy()
+            hit.append((k, xa, feats[r].copy(), gh[r, :30].copy(), float(gh[r, 30])))
+        self._basis_cache[key] = hit
+        return hit
+
+    def stage_basis(self, state, graph):
+        key = (id(graph), state.decisions)
+        hit = self._basis_cache.get(key)
+        if hit is None:
+            sc, f, n, keys, _t, _r, gh = self._run(state, graph)
+            hit = self._fill_cache(sc, f, n, keys, gh, state, graph)
+        return hit
+
+    def cost(self, state, graph):
+        sc, f, n, keys, total, rows, gh = self._run(state, graph)
+        self._fill_cache(sc, f, n, keys, gh, state, graph)
+        return total, {k: float(c) for k, c in zip(keys, rows)}
+
+    def cost_batch(self, states, graph):
+        """Totals (np.float64[N]) and prune verdicts for a list of states."""
+        sc = scorer_for(graph, self.params, self.thresholds, self.weights)
+        dec = sc.upload(states)
+        f = sc.featurize(dec)
+        total, _, _ = sc.cost(f)
+        sc.check()
+        return total.cpu().numpy(), f["verdict"].cpu().numpy()
+
+
+def gpu_cut(candidates, evaluator, graph, config, pass_index, memo, phase_seed, validate):
+    """Drop-in for `gpusched.search._cut` (search.py:168-201).
+
+    `validate` is the reference prune closure over `config.thresholds`
+    (search.py:246-247); the same rules run on the GPU with those thresholds.
+    """
+    if not candidates:
+        return [], []
+    weights = getattr(evaluator, "weights", None)
+    sc = scorer_for(graph, evaluator.params, config.thresholds, weights)
+    dec = sc.upload(candidates)
+    flagged = [h for d, h in memo.flagged if d == pass_index]
+    res = beam_cut(sc, dec, pass_index, phase_seed, flagged, config.beam_size,
+                   config.penalty_factor, config.explore_temperature, config.num_passes,
+                   sampling=config.sampling)
+    reports = [_PruneReport(reason, f"GPU prune verdict for candidate {i} of this phase")
+               for i, reason in res.rejects]
+    for depth, h in res.memo_new:
+        memo.record(depth, h)
+    beam = [candidates[i].with_cost(c) for i, c in zip(res.beam, res.costs)]
+    return beam, reports
+
+
+def install(search_module=None):
+    """Route the reference search's phase cuts through the GPU.  Returns the
+    previous `_cut` so callers can restore it."""
+    if search_module is None:
+        import gpusched.search as search_module  # type: ignore
+    prev = search_module._cut
+    search_module._cut = gpu_cut
+    return prev
+
+
+@contextlib.contextmanager
+def installed(search_module=None):
+    if search_module is None:
+        import gpusched.search as search_module  # type: ignore
+    prev = install(search_module)
+    try:
+        yield
+    finally:
+        search_module._cut = prev
+
+
+def as_numpy(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy()
