@@ -111,6 +111,8 @@ typedef struct GsPipeline* gs_pipeline_t;
 
 const char* gs_last_error(void);
 int gs_version(void);
+/* Number of this library's own kernel launches so far (process-wide). */
+int64_t gs_launch_count(void);
 
 /* Pack + upload a pipeline; replaces the per-call `PipelineGraph` walk of
  * featurize.py:275-303 / resolve.py:207-226. */
@@ -131,7 +133,8 @@ int gs_set_weights(gs_pipeline_t p, int embed_dim, int hidden_dim,
  * stride S).  Replaces featurize() (featurize.py:275-303) and prune()
  * (options.py:200-255).  Outputs, per candidate c and row r < n_rows[c]:
  * feats[(c*R + r)*56 + k] (fp64, FEATURE_ORDER), row_key[c*R + r] =
- * func << 8 | stage, verdict[c].  R = gs_pipeline_max_rows(). */
+ * func << 8 | stage, verdict[c].  R = gs_pipeline_max_rows().  With
+ * feats == NULL only the resolve + prune verdict (and n_rows) are produced. */
 int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
                  double* feats, int32_t* row_key, int32_t* n_rows,
                  uint8_t* verdict, void* stream);

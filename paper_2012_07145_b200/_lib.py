@@ -15,7 +15,7 @@ from .descriptor import GsPipelineDesc
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libgs_sched.so")
 
-EXPORTS = ("gs_last_error", "gs_version", "gs_pipeline_create", "gs_pipeline_destroy",
+EXPORTS = ("gs_last_error", "gs_version", "gs_launch_count", "gs_pipeline_create", "gs_pipeline_destroy",
            "gs_pipeline_max_rows", "gs_set_weights", "gs_featurize", "gs_cost",
            "gs_struct_hash", "gs_select_workspace_bytes", "gs_select_reps",
            "gs_topk_workspace_bytes", "gs_beam_topk", "gs_check")
@@ -40,6 +40,7 @@ def load(path: str = LIB_PATH):
     sig = {
         "gs_last_error": (C.c_char_p, []),
         "gs_version": (i32, []),
+        "gs_launch_count": (i64, []),
         "gs_pipeline_create": (i32, [C.POINTER(GsPipelineDesc), C.POINTER(P)]),
         "gs_pipeline_destroy": (i32, [P]),
         "gs_pipeline_max_rows": (i32, [P]),

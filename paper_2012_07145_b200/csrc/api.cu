@@ -64,6 +64,7 @@ extern "C" {
 
 const char* gs_last_error(void) { return g_err.c_str(); }
 int gs_version(void) { return 1; }
+int64_t gs_launch_count(void) { return (int64_t)g_launch_count.load(); }
 
 int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
   if (!d || !out || d->n_funcs <= 0 || d->n_funcs > 0x7FFF || d->n_stages < 0 || d->n_access < 0)

@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(128) cost_kernel(NetDev net, const int32_t* __
 
 int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st) {
   if (n_stages == 0) return 0;
-  hoist_kernel<<<n_stages, 64, 0, st>>>(net, algo, n_stages);
+  hoist_kernel<<<n_stages, 64, 0, st>>>(net, algo, n_stages); g_launch_count++;
   return 0;
 }
 
@@ -193,11 +193,11 @@ int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* f
   if (net.E <= 32) {
     cudaFuncSetAttribute(cost_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cost_kernel<32><<<grid, 128, smem, st>>>(net, stage_of_func, feats, row_key, n_rows, n, R, CB, total,
-                                             row_cost, basis_gh);
+                                             row_cost, basis_gh); g_launch_count++;
   } else if (net.E <= 64) {
     cudaFuncSetAttribute(cost_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cost_kernel<64><<<grid, 128, smem, st>>>(net, stage_of_func, feats, row_key, n_rows, n, R, CB, total,
-                                             row_cost, basis_gh);
+                                             row_cost, basis_gh); g_launch_count++;
   } else {
     return -1;
   }

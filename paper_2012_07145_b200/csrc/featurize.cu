@@ -1099,7 +1099,7 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
       }
     }
     __syncthreads();
-    const int nr = k.misc->nrows;
+    const int nr = feats ? k.misc->nrows : 0;   // feats == NULL: prune verdict only
     for (int r = warp; r < nr; r += nw) {
       const int key = k.rows[r];
       const int f = key >> 8, si = key & 255;
@@ -1153,7 +1153,7 @@ int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDeci
 #define GS_CASE(D)                                                                                  \
   case D:                                                                                           \
     cudaFuncSetAttribute(featurize_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total); \
-    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, L, gerr); \
+    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, L, gerr); g_launch_count++; \
     break;
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4)
 #undef GS_CASE

@@ -2,9 +2,13 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <atomic>
 #include "../../include/gs_sched.h"
 
 namespace gs {
+
+// Count of this library's own kernel launches (host side), for the bench.
+inline std::atomic<long long> g_launch_count{0};
 
 constexpr int kWarp = 32;
 constexpr int kMaxM = 128;          // largest residue modulus (transaction / bank period)

@@ -164,7 +164,7 @@ int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, cons
   if (nf > kHashMaxFuncs) return -1;
   if (depth > 3) depth = 3;
   int64_t blocks = (n + 127) / 128;
-  hash_kernel<<<(unsigned)blocks, 128, 0, st>>>(dec, n, S, nf, depth, sorted_funcs, names, name_off, out);
+  hash_kernel<<<(unsigned)blocks, 128, 0, st>>>(dec, n, S, nf, depth, sorted_funcs, names, name_off, out); g_launch_count++;
   return 0;
 }
 

@@ -255,25 +255,25 @@ int select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, uint6
   const unsigned G = (unsigned)((n + T - 1) / T);
   cudaMemsetAsync(w.taken, 0, 4 * n, st);
   cudaMemsetAsync(w.rejn, 0, 4 * n, st);
-  iota_kernel<<<G, T, 0, st>>>(w.vals_in, n);
+  iota_kernel<<<G, T, 0, st>>>(w.vals_in, n); g_launch_count++;
   size_t cb = w.cub_bytes;
   cub::DeviceRadixSort::SortPairs(w.cub, cb, hashes, w.keys_out, w.vals_in, w.vals_out, (int)n, 0, 64, st);
-  head_kernel<<<G, T, 0, st>>>(w.keys_out, n, w.head);
+  head_kernel<<<G, T, 0, st>>>(w.keys_out, n, w.head); g_launch_count++;
   cb = w.cub_bytes;
   cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.bid, (int)n, st);
-  starts_kernel<<<G, T, 0, st>>>(w.head, w.bid, n, w.starts, w.nb);
-  quota_kernel<<<G, T, 0, st>>>(w.starts, w.nb, n, w.quota);
+  starts_kernel<<<G, T, 0, st>>>(w.head, w.bid, n, w.starts, w.nb); g_launch_count++;
+  quota_kernel<<<G, T, 0, st>>>(w.starts, w.nb, n, w.quota); g_launch_count++;
   cb = w.cub_bytes;
   cub::DeviceScan::ExclusiveSum(w.cub, cb, w.quota, w.qoff, (int)n, st);
   walk_kernel<<<G, 64, 0, st>>>(w.keys_out, w.vals_out, w.starts, w.nb, w.qoff, w.quota, verdict, phase_seed,
-                                w.perm, w.slot, w.taken, w.rej, w.rejn);
+                                w.perm, w.slot, w.taken, w.rej, w.rejn); g_launch_count++;
   // zero unused tails so the scans see only live buckets
   cb = w.cub_bytes;
   cub::DeviceScan::ExclusiveSum(w.cub, cb, w.taken, w.toff, (int)n, st);
   cb = w.cub_bytes;
   cub::DeviceScan::ExclusiveSum(w.cub, cb, w.rejn, w.roff, (int)n, st);
   gather_kernel<<<G, T, 0, st>>>(w.nb, n, w.qoff, w.taken, w.toff, w.slot, rep_idx, w.starts, w.rejn, w.roff,
-                                 w.rej, rej_idx, n_reps, n_rejects);
+                                 w.rej, rej_idx, n_reps, n_rejects); g_launch_count++;
   return 0;
 }
 
@@ -527,13 +527,13 @@ struct TopkWs {
 static void band_order(TopkWs& w, const uint64_t* key, const double* val, int64_t n, double band,
                        cudaStream_t st) {
   const unsigned G = (unsigned)((n + 255) / 256);
-  iota_kernel<<<G, 256, 0, st>>>(w.vin, n);
+  iota_kernel<<<G, 256, 0, st>>>(w.vin, n); g_launch_count++;
   size_t tb = w.tmp_bytes;
   cub::DeviceRadixSort::SortPairs(w.tmp, tb, key, w.kout, w.vin, w.vout, (int)n, 0, 64, st);
-  band_flags<<<G, 256, 0, st>>>(w.kout, val, w.vout, n, band, w.brk);
+  band_flags<<<G, 256, 0, st>>>(w.kout, val, w.vout, n, band, w.brk); g_launch_count++;
   tb = w.tmp_bytes;
   cub::DeviceScan::InclusiveSum(w.tmp, tb, w.brk, w.gid, (int)n, st);
-  band_keys<<<G, 256, 0, st>>>(w.gid, w.vout, n, w.key2);
+  band_keys<<<G, 256, 0, st>>>(w.gid, w.vout, n, w.key2); g_launch_count++;
   tb = w.tmp_bytes;
   cub::DeviceRadixSort::SortKeys(w.tmp, tb, w.key2, w.key2o, (int)n, 0, 64, st);
 }
@@ -572,29 +572,29 @@ int beam_topk(const double* costs, const uint64_t* ph, int64_t n, const uint64_t
   w.tmp = p;
   w.tmp_bytes = (size_t)(ws_bytes - (int64_t)(p - (char*)ws));
   const unsigned G = (unsigned)((n + 255) / 256);
-  keys_kernel<<<G, 256, 0, st>>>(costs, ph, n, flagged, nflag, penalty, w.key, w.ckey, w.kval);
-  if (temperature > 0) gumbel_kernel<<<1, 32, 0, st>>>(w.kval, w.key, n, temperature, phase_seed);
+  keys_kernel<<<G, 256, 0, st>>>(costs, ph, n, flagged, nflag, penalty, w.key, w.ckey, w.kval); g_launch_count++;
+  if (temperature > 0) { gumbel_kernel<<<1, 32, 0, st>>>(w.kval, w.key, n, temperature, phase_seed); g_launch_count++; }
   if (band > 0) {
     band_order(w, w.key, w.kval, n, band, st);
-    pos_from_key2<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(w.key2o, k, out_pos, n_out);
+    pos_from_key2<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(w.key2o, k, out_pos, n_out); g_launch_count++;
     if (bottom) {
       band_order(w, w.ckey, costs, n, band, st);
-      bottom_from_key2<<<G, 256, 0, st>>>(w.key2o, n, bottom);
+      bottom_from_key2<<<G, 256, 0, st>>>(w.key2o, n, bottom); g_launch_count++;
     }
     return 0;
   }
   if (k <= kSortCap) {   // exact keys: hand-written single-CTA radix select + bitonic sort
-    topk_kernel<<<1, kTopNT, 0, st>>>(w.key, w.ckey, n, k, w.sel, out_pos, n_out, bottom);
+    topk_kernel<<<1, kTopNT, 0, st>>>(w.key, w.ckey, n, k, w.sel, out_pos, n_out, bottom); g_launch_count++;
     return 0;
   }
-  iota_kernel<<<G, 256, 0, st>>>(w.vin, n);
+  iota_kernel<<<G, 256, 0, st>>>(w.vin, n); g_launch_count++;
   size_t tb = w.tmp_bytes;
   cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.key, w.kout, w.vin, w.vout, (int)n, 0, 64, st);
-  copy_pos<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(w.vout, k, out_pos, n_out);
+  copy_pos<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(w.vout, k, out_pos, n_out); g_launch_count++;
   if (bottom) {
     tb = w.tmp_bytes;
     cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.ckey, w.kout, w.vin, w.vout, (int)n, 0, 64, st);
-    bottom_from_sorted<<<G, 256, 0, st>>>(w.vout, n, bottom);
+    bottom_from_sorted<<<G, 256, 0, st>>>(w.vout, n, bottom); g_launch_count++;
   }
   return 0;
 }

@@ -87,6 +87,15 @@ class Scorer:
         return host.to(self.device, non_blocking=pin)
 
     # -- K1 -------------------------------------------------------------------
+    def prune(self, dec: torch.Tensor) -> torch.Tensor:
+        """Resolve + prune verdicts only (K1 without feature rows)."""
+        n = dec.shape[0]
+        verdict = torch.empty((n,), dtype=torch.uint8, device=self.device)
+        nrows = torch.empty((n,), dtype=torch.int32, device=self.device)
+        _lib.check(self.lib.gs_featurize(self.handle, _ptr(dec), n, dec.shape[1] // 16, C.c_void_p(0),
+                                         C.c_void_p(0), _ptr(nrows), _ptr(verdict), _stream()))
+        return verdict
+
     def featurize(self, dec: torch.Tensor, out=None):
         n = dec.shape[0]
         S = dec.shape[1] // 16

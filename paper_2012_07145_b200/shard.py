@@ -1,0 +1,111 @@
+"""One beam step over a candidate batch, on one GPU or bucket-sharded over
+several (one process per GPU, NCCL over NVLink for the exchange).
+
+Sharding: every rank holds the batch's decision records and
+hashes all of them at the pass depth (cheap).  A structural-hash bucket is
+owned by rank `hash % world`, so buckets never straddle ranks; each rank
+featurizes, prunes and costs only its buckets' candidates (the expensive
+part) and draws their representatives with the same per-bucket PCG64
+streams the reference uses.  Representative records (hash, cost, candidate
+index, local order) are exchanged with one all-gather; every rank merges
+them into the global (hash ascending, permutation position) order and cuts
+the identical beam.  The only collective on the data path is that
+all-gather of a few KB per rank.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+SIGN = -0x8000000000000000  # flips int64 order into uint64 order
+
+
+class StepPlan:
+    def __init__(self, scorer, n, world, rank, pass_index, phase_seed, beam, penalty, num_passes,
+                 tie_band):
+        self.sc, self.n, self.world, self.rank = scorer, n, world, rank
+        self.pass_index, self.phase_seed, self.beam = pass_index, phase_seed, beam
+        self.penalty, self.num_passes, self.tie_band = penalty, num_passes, tie_band
+        self.fbuf = None
+        self.local_count = n
+
+    def _features(self, d):
+        m = d.shape[0]
+        if self.fbuf is None or self.fbuf["feats"].shape[0] != m:
+            self.fbuf = None
+            torch.cuda.empty_cache()
+            self.fbuf = self.sc.featurize(d)
+        else:
+            self.sc.featurize(d, out=self.fbuf)
+        return self.fbuf
+
+    def run(self, dec, k1_times=None):
+        sc = self.sc
+        h = sc.struct_hash(dec, self.pass_index)
+        if self.world > 1:
+            mine = torch.nonzero(torch.remainder(h, self.world) == self.rank).flatten()
+            d = dec.index_select(0, mine)
+            hl = h.index_select(0, mine)
+        else:
+            mine, d, hl = None, dec, h
+        self.local_count = d.shape[0]
+        if k1_times is not None:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+        f = self._features(d)
+        if k1_times is not None:
+            b.record()
+        total, _, _ = sc.cost(f)
+        rep, _, cnt = sc.select(hl, f["verdict"], self.phase_seed, rejects=False)
+        nrep = int(cnt[0].item())
+        rep = rep[:nrep]
+        costs = total.index_select(0, rep)
+        ph = hl.index_select(0, rep)
+        cand = rep if mine is None else mine.index_select(0, rep)
+        if self.world > 1:
+            costs, ph, cand = self._exchange(costs, ph, cand, nrep)
+        if k1_times is not None:
+            torch.cuda.synchronize()
+            k1_times.append(a.elapsed_time(b))
+        pos, kcnt, bot = sc.beam_topk(costs, ph, None, self.penalty, 0.0, self.phase_seed,
+                                      min(self.beam, costs.shape[0]), tie_band=self.tie_band)
+        beam = cand.index_select(0, pos[:int(kcnt.item())])
+        # bad-hash memo: hashes of the bottom half at every pass depth
+        if costs.shape[0] > 1:
+            bdec = dec.index_select(0, cand.index_select(0, torch.nonzero(bot).flatten()))
+            memo = [sc.struct_hash(bdec, dpt) for dpt in range(1, self.num_passes + 1)]
+        else:
+            memo = []
+        return {"beam": beam.cpu().tolist(), "total": total, "verdict": f["verdict"], "memo": memo,
+                "n_reps": int(costs.shape[0])}
+
+    def _exchange(self, costs, ph, cand, nrep):
+        import torch.distributed as dist
+        rec = torch.stack([ph, costs.view(torch.int64), cand,
+                           torch.arange(nrep, device=costs.device, dtype=torch.int64)], dim=1)
+        counts = torch.tensor([nrep], device=costs.device, dtype=torch.int64)
+        allc = torch.empty(self.world, device=costs.device, dtype=torch.int64)
+        dist.all_gather_into_tensor(allc, counts)
+        mx = int(allc.max().item())
+        pad = torch.zeros((mx, 4), device=costs.device, dtype=torch.int64)
+        pad[:nrep] = rec
+        allr = torch.empty((self.world * mx, 4), device=costs.device, dtype=torch.int64)
+        dist.all_gather_into_tensor(allr, pad)
+        keep = torch.cat([torch.arange(r * mx, r * mx + int(allc[r]), device=costs.device)
+                          for r in range(self.world)])
+        allr = allr.index_select(0, keep)
+        # global representative order: (hash as uint64 ascending, local order)
+        order = torch.sort(allr[:, 0] ^ SIGN, stable=True).indices
+        allr = allr.index_select(0, order)
+        return allr[:, 1].view(torch.float64).contiguous(), allr[:, 0].contiguous(), allr[:, 2].contiguous()
+
+    def run_host(self, host_u8):
+        """Public batch entry with host buffers: H2D records, one step, D2H of
+        every candidate's total + verdict and the beam."""
+        dec = host_u8.to(self.sc.device, non_blocking=True)
+        out = self.run(dec)
+        tot = out["total"].cpu()
+        ver = out["verdict"].cpu()
+        return {"h2d_bytes": host_u8.numel(), "d2h_bytes": tot.numel() * 8 + ver.numel() + 8 * len(out["beam"]),
+                "beam": out["beam"]}
