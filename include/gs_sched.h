@@ -135,6 +135,16 @@ int gs_set_weights(gs_pipeline_t p, int embed_dim, int hidden_dim,
  * feats[(c*R + r)*56 + k] (fp64, FEATURE_ORDER), row_key[c*R + r] =
  * func << 8 | stage, verdict[c].  R = gs_pipeline_max_rows().  With
  * feats == NULL only the resolve + prune verdict (and n_rows) are produced. */
+/* Exact sibling reuse in K1 (default on): each CTA walks a contiguous range
+ * of candidates; when a candidate's decision structure (func, kind,
+ * consumer per record) equals its predecessor's, the structural resolve is
+ * reused, every func's geometry record is compared bit for bit with the
+ * predecessor's, and a row is recomputed only if its own / host / kernel /
+ * read-producer / thread-child records changed — otherwise its features are
+ * copied, which is bit-identical by construction.  0 disables (every row of
+ * every candidate is computed). */
+int gs_set_reuse(gs_pipeline_t p, int enable);
+
 int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
                  double* feats, int32_t* row_key, int32_t* n_rows,
                  uint8_t* verdict, void* stream);

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libgs_sched.so")
 
 EXPORTS = ("gs_last_error", "gs_version", "gs_launch_count", "gs_pipeline_create", "gs_pipeline_destroy",
-           "gs_pipeline_max_rows", "gs_set_weights", "gs_featurize", "gs_cost",
+           "gs_pipeline_max_rows", "gs_set_weights", "gs_set_reuse", "gs_featurize", "gs_cost",
            "gs_struct_hash", "gs_select_workspace_bytes", "gs_select_reps",
            "gs_topk_workspace_bytes", "gs_beam_topk", "gs_check")
 
@@ -45,6 +45,7 @@ def load(path: str = LIB_PATH):
         "gs_pipeline_destroy": (i32, [P]),
         "gs_pipeline_max_rows": (i32, [P]),
         "gs_set_weights": (i32, [P, i32, i32] + [V] * 8),
+        "gs_set_reuse": (i32, [P, i32]),
         "gs_featurize": (i32, [P, V, i64, i32, V, V, V, V, V]),
         "gs_cost": (i32, [P, V, V, V, i64, V, V, V, V]),
         "gs_struct_hash": (i32, [P, V, i64, i32, i32, V, V]),

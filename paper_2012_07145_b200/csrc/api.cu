@@ -10,7 +10,7 @@ namespace gs {
 Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rcap, int pcap, int nwarps);
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, const Layout& L,
-                     int nwarps, int grid, int* gerr, cudaStream_t st);
+                     int nwarps, int grid, int* gerr, int reuse, cudaStream_t st);
 int featurize_occupancy(int nd, int nwarps, int smem);
 int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st);
 int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
@@ -58,6 +58,8 @@ struct GsPipeline {
   int num_sms = 0;
   int max_smem = 0;
   int rcap = 0, pcap = 0;
+  int reuse = 1;
+  int nwarps = 8;
 };
 
 extern "C" {
@@ -96,8 +98,41 @@ int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
   if (h.ns) memcpy(blob.data() + h.off_stages, d->stages, h.ns * sizeof(GsStage));
   if (h.na) memcpy(blob.data() + h.off_access, d->access, h.na * sizeof(GsAccess));
   // capacities for expanded reads / chain paths (per candidate, in shared memory)
-  p->rcap = std::min(4096, 4 * h.na + 64);
-  p->pcap = std::min(65535, 6 * p->rcap);
+  // Capacity bound for expanded reads / path entries of ANY decision log:
+  // a stage of func g is expanded at most Q(g) times, Q(g) = 1 when g can
+  // not be inlined, else max(1, sum of Q(consumer) over accesses reading g);
+  // each access then appears in at most Q(its consumer) paths.
+  {
+    std::vector<int> Q(h.nf, 0), state(h.nf, 0), self(h.nf, 0);
+    for (int a = 0; a < h.na; ++a)
+      if (d->access[a].producer == d->access[a].consumer) self[d->access[a].producer] = 1;
+    std::vector<std::vector<int>> readers(h.nf);
+    for (int a = 0; a < h.na; ++a) readers[d->access[a].producer].push_back(d->access[a].consumer);
+    // iterative post-order over the consumer DAG
+    for (int root = 0; root < h.nf; ++root) {
+      if (state[root] == 2) continue;
+      std::vector<std::pair<int, size_t>> st{{root, 0}};
+      state[root] = 1;
+      while (!st.empty()) {
+        auto& [g, it] = st.back();
+        const bool elig = !d->funcs[g].is_output && !d->funcs[g].is_external && d->funcs[g].n_stages == 1 && !self[g];
+        if (elig && it < readers[g].size()) {
+          int c = readers[g][it++];
+          if (state[c] == 0) { state[c] = 1; st.push_back({c, 0}); }
+          continue;
+        }
+        long long q = 0;
+        if (elig) for (int c : readers[g]) q += Q[c];
+        Q[g] = (int)std::min<long long>(std::max<long long>(1, q), 1 << 20);
+        state[g] = 2;
+        st.pop_back();
+      }
+    }
+    long long bound = 0;
+    for (int a = 0; a < h.na; ++a) bound += Q[d->access[a].consumer];
+    p->rcap = (int)std::min<long long>(4096, bound + 32);
+    p->pcap = (int)std::min<long long>(65535, bound + 32);
+  }
   cudaDeviceProp prop;
   int dev = 0;
   CK(cudaGetDevice(&dev));
@@ -173,11 +208,17 @@ static Layout layout_for(gs_pipeline_t p, int S, int nwarps) {
                      p->rcap, p->pcap, nwarps);
 }
 
+int gs_set_reuse(gs_pipeline_t p, int enable) {
+  if (!p) return fail(GS_ERR_ARG, "null pipeline");
+  p->reuse = enable ? 1 : 0;
+  return GS_OK;
+}
+
 int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, double* feats, int32_t* row_key,
                  int32_t* n_rows, uint8_t* verdict, void* stream) {
   if (!p || S < 1 || n < 0) return fail(GS_ERR_ARG, "bad featurize arguments");
   if (n == 0) return GS_OK;
-  const int nwarps = 8;
+  const int nwarps = p->nwarps;
   Layout L = layout_for(p, S, nwarps);
   if (L.total > p->max_smem)
     return fail(GS_ERR_CAPACITY, "pipeline too large for the per-CTA shared-memory workspace (" +
@@ -187,7 +228,7 @@ int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, doubl
   int64_t grid = (int64_t)p->num_sms * occ;
   if (grid > n) grid = n;
   int rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, L, nwarps,
-                            (int)grid, p->err, (cudaStream_t)stream);
+                            (int)grid, p->err, p->reuse, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "unsupported ndim");
   CK(cudaGetLastError());
   return GS_OK;

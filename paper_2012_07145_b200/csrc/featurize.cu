@@ -23,6 +23,8 @@ namespace gs {
 
 struct Frame { int16_t owner, root; int32_t cur, end; int16_t plen, pad; int64_t vol; };
 
+struct ICall { int16_t root, iname, stage, pad; int64_t vol; };   // per (root stage, inline func)
+
 struct WarpScr {
   double feat[GS_NUM_FEATURES];
   unsigned long long H[kMaxM], S[kMaxM], T[kMaxM];
@@ -36,7 +38,7 @@ struct WarpScr {
 };
 
 struct Misc {
-  int ndec, nreads, npath, nrows, nord, err, verdict, pad;
+  int ndec, nreads, npath, nrows, nicall, err, verdict, same_struct, prev_valid, ndirty, pad0, pad1;
 };
 
 template <int ND>
@@ -45,9 +47,11 @@ struct K1 {
   const GsStage* ST;
   const GsAccess* A;
   const PipeDev* P;
-  GsDecision* dec;
+  GsDecision* dec;   // current decision records
+  GsDecision* pdec;  // previous candidate's
   int16_t* didx;
-  CF<ND>* cf;
+  CF<ND>* cf;        // current geometry
+  CF<ND>* pcf;       // previous candidate's geometry
   RRead* rd;
   int16_t* path;
   int32_t* rdb;      // [2*ns]: begin,end of reads per global stage
@@ -56,6 +60,13 @@ struct K1 {
   Frame* stack;
   int64_t* volacc;
   int16_t* touched;
+  ICall* icall;
+  int32_t* srcb;     // [nf+1] CSR: reads by producer
+  int16_t* srcl;     // [rcap]
+  int32_t* rdepb;    // [R+1] CSR: funcs (besides host/kernel) a row depends on
+  int16_t* rdep;     // [rcap + nf]
+  uint8_t* dirty;    // [nf]
+  int16_t* rowlist;  // [R] rows to recompute this candidate
   Misc* misc;
   int rcap, pcap;
   int* gerr;
@@ -112,7 +123,13 @@ __device__ __forceinline__ void chain_iv(const GsAccess* A, const int16_t* p, in
 }
 
 // ---------------------------------------------------------------------------
-// resolve (warp 0)
+// resolve (warp 0), split in two:
+//   structure — depends only on (func, kind, consumer) of each decision:
+//               expanded reads + chain paths, rows, inline call volumes per
+//               (root stage, inline func), producer->reads and row-dependency
+//               CSRs; rebuilt only when the structure changes;
+//   geometry  — per-func padded-tile geometry (needs tilings), kernel
+//               aggregates, inline totals / primaries.
 // ---------------------------------------------------------------------------
 template <int ND>
 __device__ int8_t tier_of_producer(const K1<ND>& k, int p) {
@@ -122,16 +139,15 @@ __device__ int8_t tier_of_producer(const K1<ND>& k, int p) {
   return kind == GS_ROOT ? T_GLOBAL : kind == GS_FUSE_BLOCK ? T_SHARED : T_REGISTER;
 }
 
-// Depth-first inline substitution of one stage (resolve.py:167-200).
-// mode 0: emit reads; mode 1: accumulate inline call volumes into volacc.
+// Depth-first inline substitution of one stage (resolve.py:167-200): emits
+// the reads and accumulates inline call volumes (volacc, first-touch order).
 template <int ND>
-__device__ void expand_stage(K1<ND>& k, int root, int gstage, int mode, int& ntouched) {
+__device__ void expand_stage(K1<ND>& k, int root, int gstage, int& ntouched) {
   Misc& m = *k.misc;
-  int sp = 0;
-  int16_t* pfx = k.touched + k.P->nf;   // path prefix buffer (nf entries)
+  int16_t* pfx = k.touched + k.P->nf;   // path prefix buffer (nf + 1 entries)
   const GsStage& st = k.ST[gstage];
   k.stack[0] = Frame{(int16_t)root, (int16_t)root, st.access_begin, st.access_begin + st.n_access, 0, 0, 1};
-  sp = 1;
+  int sp = 1;
   while (sp > 0) {
     Frame& fr = k.stack[sp - 1];
     if (fr.cur == fr.end) { --sp; continue; }
@@ -141,16 +157,14 @@ __device__ void expand_stage(K1<ND>& k, int root, int gstage, int mode, int& nto
     int di = k.didx[p];
     if (di >= 0 && k.dec[di].kind == GS_INLINE) {
       int64_t vol = fr.vol * (int64_t)k.A[a].window;
-      if (mode == 1) {
-        if (k.volacc[p] == 0) k.touched[ntouched++] = (int16_t)p;
-        k.volacc[p] += vol;
-      }
+      if (k.volacc[p] == 0) k.touched[ntouched++] = (int16_t)p;
+      k.volacc[p] += vol;
       if (sp >= k.P->nf + 1) { m.err |= E_STACK; return; }
       const GsStage& is = k.ST[k.F[p].stage_begin];
       k.stack[sp] = Frame{(int16_t)p, fr.root, is.access_begin, is.access_begin + is.n_access,
                           (int16_t)(fr.plen + 1), 0, vol};
       ++sp;
-    } else if (mode == 0) {
+    } else {
       int plen = fr.plen + 1;
       if (m.nreads >= k.rcap) { m.err |= E_READS; return; }
       if (m.npath + plen > k.pcap || plen > 255) { m.err |= E_PATHS; return; }
@@ -165,46 +179,81 @@ __device__ void expand_stage(K1<ND>& k, int root, int gstage, int mode, int& nto
   }
 }
 
+// lane 0
 template <int ND>
-__device__ void resolve(K1<ND>& k) {
-  const int lane = lane_id();
+__device__ void resolve_structure(K1<ND>& k) {
   Misc& m = *k.misc;
   const int nf = k.P->nf;
-  const GsMachine& M = k.P->m;
-  (void)M;
-  // decision index per func
-  for (int f = lane; f < nf; f += 32) { k.didx[f] = -1; k.volacc[f] = 0; k.cf[f].kind = K_ABSENT; }
-  __syncwarp();
-  if (lane == 0) {
-    int bad = 0;
-    for (int i = 0; i < m.ndec; ++i) {
-      const GsDecision& d = k.dec[i];
-      if (d.func >= nf || d.kind > GS_INLINE || k.F[d.func].is_external || k.didx[d.func] >= 0 ||
-          ((d.kind == GS_FUSE_BLOCK || d.kind == GS_FUSE_THREAD) && d.consumer >= nf))
-        bad = 1;
-      else
-        k.didx[d.func] = (int16_t)i;
-    }
-    if (bad) m.err |= E_SCHEDULE;
-    m.nreads = 0; m.npath = 0;
-    // expanded reads of every non-inline func, decision order
-    for (int i = 0; i < m.ndec && !m.err; ++i) {
-      const GsDecision& d = k.dec[i];
-      if (d.kind == GS_INLINE) continue;
-      const GsFunc& fn = k.F[d.func];
-      k.frd[d.func] = m.nreads;
+  m.nreads = 0; m.npath = 0; m.nicall = 0;
+  for (int f = 0; f < nf; ++f) k.volacc[f] = 0;
+  for (int i = 0; i < m.ndec && !m.err; ++i) {
+    const GsDecision& d = k.dec[i];
+    if (d.kind == GS_INLINE) continue;
+    const GsFunc& fn = k.F[d.func];
+    k.frd[d.func] = m.nreads;
+    for (int s = 0; s < fn.n_stages && !m.err; ++s) {
+      int gsid = fn.stage_begin + s;
       int nt = 0;
-      for (int s = 0; s < fn.n_stages; ++s) {
-        int gsid = fn.stage_begin + s;
-        k.rdb[2 * gsid] = m.nreads;
-        expand_stage(k, d.func, gsid, 0, nt);
-        k.rdb[2 * gsid + 1] = m.nreads;
+      k.rdb[2 * gsid] = m.nreads;
+      expand_stage(k, d.func, gsid, nt);
+      k.rdb[2 * gsid + 1] = m.nreads;
+      for (int t = 0; t < nt; ++t) {
+        int iname = k.touched[t];
+        if (m.nicall >= k.pcap) { m.err |= E_PATHS; break; }
+        k.icall[m.nicall++] = ICall{(int16_t)d.func, (int16_t)iname, (int16_t)s, 0, k.volacc[iname]};
+        k.volacc[iname] = 0;
       }
     }
   }
-  __syncwarp();
   if (m.err) return;
+  // reads grouped by producer, read order kept (CSR)
+  for (int f = 0; f <= nf; ++f) k.srcb[f] = 0;
+  for (int j = 0; j < m.nreads; ++j) k.srcb[k.rd[j].producer + 1]++;
+  for (int f = 0; f < nf; ++f) k.srcb[f + 1] += k.srcb[f];
+  for (int f = 0; f < nf; ++f) k.volacc[f] = k.srcb[f];   // fill cursors (reuse scratch)
+  for (int j = 0; j < m.nreads; ++j) k.srcl[k.volacc[k.rd[j].producer]++] = (int16_t)j;
+  for (int f = 0; f < nf; ++f) k.volacc[f] = 0;
+  // rows: non-inline decision order (every stage), then inline (featurize.py:292-303)
+  int nr = 0;
+  for (int i = 0; i < m.ndec; ++i) {
+    const GsDecision& d = k.dec[i];
+    if (d.kind == GS_INLINE) continue;
+    for (int s = 0; s < k.F[d.func].n_stages; ++s) k.rows[nr++] = (d.func << 8) | s;
+  }
+  for (int i = 0; i < m.ndec; ++i)
+    if (k.dec[i].kind == GS_INLINE) k.rows[nr++] = (k.dec[i].func << 8);
+  m.nrows = nr;
+  // per-row dependencies besides its own func / host / kernel: producers of
+  // the reads it owns and its fuse_at_thread children
+  int nd = 0;
+  for (int r = 0; r < nr; ++r) {
+    k.rdepb[r] = nd;
+    const int f = k.rows[r] >> 8, si = k.rows[r] & 255;
+    const bool inl = k.dec[k.didx[f]].kind == GS_INLINE;
+    int lo = inl ? 0 : k.rdb[2 * (k.F[f].stage_begin + si)];
+    int hi = inl ? m.nreads : k.rdb[2 * (k.F[f].stage_begin + si) + 1];
+    for (int j = lo; j < hi; ++j)
+      if (k.rd[j].owner == f && nd < k.rcap + nf) k.rdep[nd++] = k.rd[j].producer;
+    if (!inl)
+      for (int i = 0; i < m.ndec; ++i)
+        if (k.dec[i].kind == GS_FUSE_THREAD && k.dec[i].consumer == f && nd < k.rcap + nf)
+          k.rdep[nd++] = (int16_t)k.dec[i].func;
+  }
+  k.rdepb[nr] = nd;
+}
 
+template <int ND>
+__device__ __forceinline__ void zero_cf(CF<ND>& c) {
+  int32_t* w = reinterpret_cast<int32_t*>(&c);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(CF<ND>) / 4); ++i) w[i] = 0;
+}
+
+template <int ND>
+__device__ void resolve_geometry(K1<ND>& k) {
+  const int lane = lane_id();
+  Misc& m = *k.misc;
+  const int nf = k.P->nf;
   // Pass 1: geometry of non-inline funcs in decision order (resolve.py:232-333)
   for (int i = 0; i < m.ndec; ++i) {
     const GsDecision d = k.dec[i];
@@ -212,12 +261,12 @@ __device__ void resolve(K1<ND>& k) {
     const int f = d.func;
     const GsFunc& fn = k.F[f];
     CF<ND> c;
+    zero_cf(c);
     c.consumer = (d.kind == GS_ROOT) ? -1 : (int16_t)d.consumer;
-    c.calls = 0; c.best = 0; c.k_shared = 0; c.k_threads = 0; c.n_blocks = 0;
-    c.has_serial = 0; c.serial_prod = 1;
+    c.serial_prod = 1;
     if (d.kind == GS_ROOT) {
       int32_t ser[ND], thr[ND];
-      bool tiled = (d.flags & 3) == 3;
+      const bool tiled = (d.flags & 3) == 3;
       int inner = 0;
       if (!tiled) {  // provisional tiling (resolve.py:159-164)
         inner = -1;
@@ -246,51 +295,43 @@ __device__ void resolve(K1<ND>& k) {
       __syncwarp();
       continue;
     }
-    // fused: scan processed consumers' reads for producer == f (resolve.py:379-393)
-    const int end = k.frd[f];
-    int first = 0x7fffffff;
-    for (int j0 = 0; j0 < end; j0 += 32) {
-      int j = j0 + lane;
-      bool hit = j < end && k.rd[j].producer == f;
-      unsigned bal = __ballot_sync(0xffffffffu, hit);
-      if (bal) { first = j0 + __ffs(bal) - 1; break; }
-    }
-    if (first == 0x7fffffff) { if (lane == 0) m.err |= E_SCHEDULE; __syncwarp(); return; }
-    const int16_t src_root = k.rd[first].root;
-    const CF<ND> cg0 = k.cf[src_root];
-    int64_t lo[ND], hi[ND], tlo[ND], thi[ND];
+    // fusion sources: reads of f issued by funcs resolved before it (resolve.py:379-393)
+    const int sb = k.srcb[f], se = k.srcb[f + 1];
+    int first = -1;
+    for (int q = sb; q < se; ++q)
+      if (k.didx[k.rd[k.srcl[q]].root] < i) { first = k.srcl[q]; break; }
+    if (first < 0) { if (lane == 0) m.err |= E_SCHEDULE; __syncwarp(); return; }
+    const CF<ND> cg0 = k.cf[k.rd[first].root];
+    int64_t lo[ND], hi[ND], tlo[ND], thi[ND], ts0[ND];
 #pragma unroll
-    for (int dd = 0; dd < ND; ++dd) { lo[dd] = tlo[dd] = INT64_MAX; hi[dd] = thi[dd] = INT64_MIN; }
-    int64_t ts0[ND];
-#pragma unroll
-    for (int dd = 0; dd < ND; ++dd) ts0[dd] = 1;
+    for (int dd = 0; dd < ND; ++dd) { lo[dd] = tlo[dd] = INT64_MAX; hi[dd] = thi[dd] = INT64_MIN; ts0[dd] = 1; }
     {
       const RRead& r0 = k.rd[first];
       for (int q = 0; q < r0.plen; ++q)
 #pragma unroll
         for (int dd = 0; dd < ND; ++dd) ts0[dd] *= k.A[k.path[r0.pbeg + q]].s[dd];
     }
-    for (int j0 = 0; j0 < end; j0 += 32) {
-      int j = j0 + lane;
-      bool hit = j < end && k.rd[j].producer == f;
-      if (hit) {
-        const int16_t root = k.rd[j].root;
-        const CF<ND>& cg = (d.kind == GS_FUSE_THREAD) ? cg0 : k.cf[root];
-        const RRead& r = k.rd[j];
-        int32_t blo[ND], bhi[ND];
-        if (d.kind == GS_FUSE_BLOCK) block_box(cg, blo, bhi);
-        else {
+    for (int q0 = sb; q0 < se; q0 += 32) {
+      const int q = q0 + lane;
+      if (q < se) {
+        const RRead& r = k.rd[k.srcl[q]];
+        if (k.didx[r.root] < i) {
+          const CF<ND>& cg = (d.kind == GS_FUSE_THREAD) ? cg0 : k.cf[r.root];
+          int32_t blo[ND], bhi[ND];
+          if (d.kind == GS_FUSE_BLOCK) block_box(cg, blo, bhi);
+          else {
 #pragma unroll
-          for (int dd = 0; dd < ND; ++dd) { blo[dd] = cg.base[dd]; bhi[dd] = cg.base[dd] + cg.ext[dd] - 1; }
-        }
+            for (int dd = 0; dd < ND; ++dd) { blo[dd] = cg.base[dd]; bhi[dd] = cg.base[dd] + cg.ext[dd] - 1; }
+          }
 #pragma unroll
-        for (int dd = 0; dd < ND; ++dd) {
-          int64_t a = blo[dd], b = bhi[dd];
-          chain_iv(k.A, k.path + r.pbeg, r.plen, dd, a, b);
-          lo[dd] = a < lo[dd] ? a : lo[dd]; hi[dd] = b > hi[dd] ? b : hi[dd];
-          int64_t ta = cg.tlo[dd], tb = cg.thi[dd];
-          chain_iv(k.A, k.path + r.pbeg, r.plen, dd, ta, tb);
-          tlo[dd] = ta < tlo[dd] ? ta : tlo[dd]; thi[dd] = tb > thi[dd] ? tb : thi[dd];
+          for (int dd = 0; dd < ND; ++dd) {
+            int64_t a = blo[dd], b = bhi[dd];
+            chain_iv(k.A, k.path + r.pbeg, r.plen, dd, a, b);
+            lo[dd] = a < lo[dd] ? a : lo[dd]; hi[dd] = b > hi[dd] ? b : hi[dd];
+            int64_t ta = cg.tlo[dd], tb = cg.thi[dd];
+            chain_iv(k.A, k.path + r.pbeg, r.plen, dd, ta, tb);
+            tlo[dd] = ta < tlo[dd] ? ta : tlo[dd]; thi[dd] = tb > thi[dd] ? tb : thi[dd];
+          }
         }
       }
     }
@@ -313,7 +354,6 @@ __device__ void resolve(K1<ND>& k) {
         int64_t th = tlo[dd] + t * s - 1;
         c.thi[dd] = (int32_t)(thi[dd] > th ? thi[dd] : th);
         c.ctx[dd] = (int32_t)t; c.base[dd] = c.rlo[dd]; c.coeff[dd] = s; c.ext[dd] = s;
-        c.bbx[dd] = 0;
         nt *= t; sp *= s;
       }
       c.kind = K_BLOCK; c.tier = T_SHARED; c.kernel = cg0.kernel; c.realizations = K.n_blocks;
@@ -333,7 +373,6 @@ __device__ void resolve(K1<ND>& k) {
         c.ctx[dd] = cg0.ctx[dd]; c.base[dd] = c.rlo[dd];
         c.coeff[dd] = (int32_t)(cg0.coeff[dd] * ts0[dd]);
         c.ext[dd] = (int32_t)(hi[dd] - lo[dd] + 1);
-        c.bbx[dd] = 0;
         pe *= c.ext[dd];
       }
       c.kind = K_THREAD; c.tier = T_REGISTER; c.kernel = cg0.kernel;
@@ -348,79 +387,61 @@ __device__ void resolve(K1<ND>& k) {
     __syncwarp();
   }
 
-  // externals and unscheduled producers (resolve.py:396-425)
-  const int nreads = m.nreads;
-  for (int f = 0; f < nf; ++f) {
+  // externals and unscheduled producers (resolve.py:396-425): lane per func
+  for (int f = lane; f < nf; f += 32) {
     const GsFunc& fn = k.F[f];
     if (!(fn.is_external || k.didx[f] < 0)) continue;
     int64_t lo[ND], hi[ND];
 #pragma unroll
     for (int dd = 0; dd < ND; ++dd) { lo[dd] = INT64_MAX; hi[dd] = INT64_MIN; }
-    bool any = false;
-    for (int j0 = 0; j0 < nreads; j0 += 32) {
-      int j = j0 + lane;
-      bool hit = j < nreads && k.rd[j].producer == f;
-      if (hit) {
-        const CF<ND>& cg = k.cf[k.rd[j].root];
-        const RRead& r = k.rd[j];
-#pragma unroll
-        for (int dd = 0; dd < ND; ++dd) {
-          int64_t a = cg.tlo[dd], b = cg.thi[dd];
-          chain_iv(k.A, k.path + r.pbeg, r.plen, dd, a, b);
-          lo[dd] = a < lo[dd] ? a : lo[dd]; hi[dd] = b > hi[dd] ? b : hi[dd];
-        }
-      }
-      any |= __any_sync(0xffffffffu, hit);
-    }
-#pragma unroll
-    for (int dd = 0; dd < ND; ++dd) { lo[dd] = wmin64(lo[dd]); hi[dd] = wmax64(hi[dd]); }
-    if (lane == 0) {
-      CF<ND> c;
-      c.kind = K_EXTERNAL; c.tier = T_GLOBAL; c.unrolled = 0; c.has_serial = 0;
-      c.kernel = -1; c.consumer = -1; c.n_threads = 1; c.serial_prod = 1; c.k_threads = 0;
-      c.realizations = 0; c.calls = 0; c.best = 0; c.n_blocks = 0; c.k_shared = 0;
+    const int sb = k.srcb[f], se = k.srcb[f + 1];
+    for (int q = sb; q < se; ++q) {
+      const RRead& r = k.rd[k.srcl[q]];
+      const CF<ND>& cg = k.cf[r.root];
 #pragma unroll
       for (int dd = 0; dd < ND; ++dd) {
-        int e = dd < fn.ndim ? fn.extent[dd] : 1;
-        c.rlo[dd] = any ? (int32_t)lo[dd] : 0; c.rhi[dd] = any ? (int32_t)hi[dd] : e - 1;
-        c.tlo[dd] = c.rlo[dd]; c.thi[dd] = c.rhi[dd];
-        c.ctx[dd] = 1; c.base[dd] = 0; c.coeff[dd] = 0; c.ext[dd] = 1; c.bbx[dd] = 0;
+        int64_t a = cg.tlo[dd], b = cg.thi[dd];
+        chain_iv(k.A, k.path + r.pbeg, r.plen, dd, a, b);
+        lo[dd] = a < lo[dd] ? a : lo[dd]; hi[dd] = b > hi[dd] ? b : hi[dd];
       }
-      k.cf[f] = c;
     }
+    CF<ND> c;
+    zero_cf(c);
+    c.kind = K_EXTERNAL; c.tier = T_GLOBAL; c.kernel = -1; c.consumer = -1; c.n_threads = 1; c.serial_prod = 1;
+#pragma unroll
+    for (int dd = 0; dd < ND; ++dd) {
+      int e = dd < fn.ndim ? fn.extent[dd] : 1;
+      c.rlo[dd] = se > sb ? (int32_t)lo[dd] : 0; c.rhi[dd] = se > sb ? (int32_t)hi[dd] : e - 1;
+      c.tlo[dd] = c.rlo[dd]; c.thi[dd] = c.rhi[dd];
+      c.ctx[dd] = 1; c.ext[dd] = 1;
+    }
+    k.cf[f] = c;
   }
   __syncwarp();
 
-  // Pass 2: inline call accounting (resolve.py:337-349) + inline records
+  // inline call totals / primaries (resolve.py:337-349) and inline records
   if (lane == 0) {
-    for (int i = 0; i < m.ndec && !m.err; ++i) {
+    for (int i = 0; i < m.ndec; ++i) {
       const GsDecision& d = k.dec[i];
-      if (d.kind == GS_INLINE) continue;
-      const GsFunc& fn = k.F[d.func];
-      const CF<ND>& c = k.cf[d.func];
-      int64_t pb = prod_ext(c) * c.n_threads * k.cf[c.kernel].n_blocks;
-      for (int s = 0; s < fn.n_stages; ++s) {
-        int nt = 0;
-        expand_stage(k, d.func, fn.stage_begin + s, 1, nt);
-        for (int t = 0; t < nt; ++t) {
-          int iname = k.touched[t];
-          int64_t calls = k.volacc[iname] * pb;
-          k.volacc[iname] = 0;
-          CF<ND>& ic = k.cf[iname];
-          if (ic.kind != K_INLINE) { ic.kind = K_INLINE; ic.calls = 0; ic.best = 0; ic.consumer = -1; }
-          ic.calls += calls;
-          if (calls > ic.best) { ic.best = calls; ic.consumer = (int16_t)d.func; }
-        }
-      }
+      if (d.kind != GS_INLINE) continue;
+      CF<ND>& ic = k.cf[d.func];
+      zero_cf(ic);
+      ic.kind = K_INLINE; ic.consumer = -1;
+    }
+    for (int e = 0; e < m.nicall; ++e) {
+      const ICall& x = k.icall[e];
+      const CF<ND>& c = k.cf[x.root];
+      const int64_t calls = x.vol * prod_ext(c) * c.n_threads * k.cf[c.kernel].n_blocks;
+      CF<ND>& ic = k.cf[x.iname];
+      ic.calls += calls;
+      if (calls > ic.best) { ic.best = calls; ic.consumer = x.root; }
     }
     for (int i = 0; i < m.ndec; ++i) {
       const GsDecision& d = k.dec[i];
       if (d.kind != GS_INLINE) continue;
       CF<ND>& ic = k.cf[d.func];
-      if (ic.kind != K_INLINE) { ic.kind = K_INLINE; ic.calls = 0; ic.best = 0; ic.consumer = -1; }
-      int prim = ic.consumer;
-      ic.tier = T_NONE; ic.has_serial = 0; ic.serial_prod = 1; ic.realizations = 0;
-      ic.k_threads = 0; ic.n_blocks = 0; ic.k_shared = 0;
+      const int prim = ic.consumer;
+      ic.tier = T_NONE; ic.serial_prod = 1;
       if (prim >= 0) {
         const CF<ND>& h = k.cf[prim];
         ic.kernel = h.kernel; ic.n_threads = h.n_threads; ic.unrolled = h.unrolled;
@@ -429,23 +450,38 @@ __device__ void resolve(K1<ND>& k) {
         ic.kernel = -1; ic.n_threads = 1; ic.unrolled = 1;
         for (int dd = 0; dd < ND; ++dd) ic.ctx[dd] = 1;
       }
-      for (int dd = 0; dd < ND; ++dd) {
-        ic.rlo[dd] = 0; ic.rhi[dd] = -1; ic.tlo[dd] = 0; ic.thi[dd] = -1;
-        ic.base[dd] = 0; ic.coeff[dd] = 0; ic.ext[dd] = 1; ic.bbx[dd] = 0;
-      }
+      for (int dd = 0; dd < ND; ++dd) { ic.rhi[dd] = -1; ic.thi[dd] = -1; ic.ext[dd] = 1; }
     }
-    // row list: non-inline decision order (every stage), then inline
-    int nr = 0;
-    for (int i = 0; i < m.ndec; ++i) {
-      const GsDecision& d = k.dec[i];
-      if (d.kind == GS_INLINE) continue;
-      for (int s = 0; s < k.F[d.func].n_stages; ++s) k.rows[nr++] = (d.func << 8) | s;
-    }
-    for (int i = 0; i < m.ndec; ++i)
-      if (k.dec[i].kind == GS_INLINE) k.rows[nr++] = (k.dec[i].func << 8);
-    m.nrows = nr;
   }
   __syncwarp();
+}
+
+// warp 0: decision validation + structure (if changed) + geometry
+template <int ND>
+__device__ void resolve(K1<ND>& k) {
+  const int lane = lane_id();
+  Misc& m = *k.misc;
+  const int nf = k.P->nf;
+  if (!m.same_struct) {
+    for (int f = lane; f < nf; f += 32) k.didx[f] = -1;
+    __syncwarp();
+    if (lane == 0) {
+      int bad = 0;
+      for (int i = 0; i < m.ndec; ++i) {
+        const GsDecision& d = k.dec[i];
+        if (d.func >= nf || d.kind > GS_INLINE || k.F[d.func].is_external || k.didx[d.func] >= 0 ||
+            ((d.kind == GS_FUSE_BLOCK || d.kind == GS_FUSE_THREAD) && d.consumer >= nf))
+          bad = 1;
+        else
+          k.didx[d.func] = (int16_t)i;
+      }
+      if (bad) m.err |= E_SCHEDULE;
+      if (!m.err) resolve_structure(k);
+    }
+    __syncwarp();
+    if (m.err) return;
+  }
+  resolve_geometry(k);
 }
 
 // prune verdict (options.py:200-255, machine.py:91-105); lane 0
@@ -454,7 +490,6 @@ __device__ int prune_verdict(const K1<ND>& k) {
   const Misc& m = *k.misc;
   const GsMachine& M = k.P->m;
   const GsThresholds& th = k.P->th;
-  double computed = 0, needed = 0;
   int64_t ci = 0, ni = 0;
   for (int i = 0; i < m.ndec; ++i) {   // non-external scheduled funcs
     const GsDecision& d = k.dec[i];
@@ -466,9 +501,8 @@ __device__ int prune_verdict(const K1<ND>& k) {
     if (d.kind == GS_INLINE) ci += c.calls;
     else ci += prod_ext(c) * c.n_threads * k.cf[c.kernel].n_blocks;
   }
-  computed = (double)ci; needed = (double)ni;
-  if (ni && computed > th.recompute_factor * needed) return GS_PRUNE_RECOMPUTE;
-  double minb = th.min_blocks_per_sm_factor * (double)M.num_sms;
+  if (ni && (double)ci > th.recompute_factor * (double)ni) return GS_PRUNE_RECOMPUTE;
+  const double minb = th.min_blocks_per_sm_factor * (double)M.num_sms;
   for (int i = 0; i < m.ndec; ++i)
     if (k.dec[i].kind == GS_ROOT && (double)k.cf[k.dec[i].func].n_blocks < minb) return GS_PRUNE_IDLE_SMS;
   for (int i = 0; i < m.ndec; ++i) {
@@ -1050,7 +1084,7 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
                                                         const GsDecision* __restrict__ dec, int64_t n, int S,
                                                         double* __restrict__ feats, int32_t* __restrict__ row_key,
                                                         int32_t* __restrict__ n_rows, uint8_t* __restrict__ verdict,
-                                                        Layout L, int* gerr) {
+                                                        Layout L, int* gerr, int reuse) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar;
   const int warp = threadIdx.x >> 5, lane = lane_id(), nw = blockDim.x >> 5;
@@ -1061,8 +1095,10 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
   k.ST = reinterpret_cast<const GsStage*>(sm + L.blob + P->off_stages);
   k.A = reinterpret_cast<const GsAccess*>(sm + L.blob + P->off_access);
   k.dec = reinterpret_cast<GsDecision*>(sm + L.dec);
+  k.pdec = reinterpret_cast<GsDecision*>(sm + L.pdec);
   k.didx = reinterpret_cast<int16_t*>(sm + L.didx);
   k.cf = reinterpret_cast<CF<ND>*>(sm + L.cf);
+  k.pcf = reinterpret_cast<CF<ND>*>(sm + L.pcf);
   k.rd = reinterpret_cast<RRead*>(sm + L.reads);
   k.path = reinterpret_cast<int16_t*>(sm + L.paths);
   k.rdb = reinterpret_cast<int32_t*>(sm + L.rdb);
@@ -1071,41 +1107,126 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
   k.stack = reinterpret_cast<Frame*>(sm + L.stack);
   k.volacc = reinterpret_cast<int64_t*>(sm + L.volacc);
   k.touched = reinterpret_cast<int16_t*>(sm + L.touched);
+  k.icall = reinterpret_cast<ICall*>(sm + L.icall);
+  k.srcb = reinterpret_cast<int32_t*>(sm + L.srcb);
+  k.srcl = reinterpret_cast<int16_t*>(sm + L.srcl);
+  k.rdepb = reinterpret_cast<int32_t*>(sm + L.rdepb);
+  k.rdep = reinterpret_cast<int16_t*>(sm + L.rdep);
+  k.dirty = reinterpret_cast<uint8_t*>(sm + L.dirty);
+  k.rowlist = reinterpret_cast<int16_t*>(sm + L.rowlist);
   k.misc = reinterpret_cast<Misc*>(sm + L.misc);
   k.rcap = L.rcap; k.pcap = L.pcap; k.gerr = gerr;
   WarpScr& W = *reinterpret_cast<WarpScr*>(sm + L.warps + warp * L.warp_bytes);
+  uint8_t* rflag = reinterpret_cast<uint8_t*>(sm + L.rflag);
+  const int nf = P->nf;
+  // contiguous candidate range per CTA: consecutive candidates of a beam
+  // step are siblings, which is what the geometry diff below exploits
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t c0 = (int64_t)blockIdx.x * per;
+  const int64_t c1 = c0 + per < n ? c0 + per : n;
+  if (threadIdx.x == 0) { k.misc->prev_valid = 0; k.misc->same_struct = 0; k.misc->ndec = 0; }
   bulk_wait(&bar);
   __syncthreads();
-  for (int64_t c = blockIdx.x; c < n; c += gridDim.x) {
+  for (int64_t c = c0; c < c1; ++c) {
     if (warp == 0) {
       const uint4* src = reinterpret_cast<const uint4*>(dec + c * S);
       uint4* dst = reinterpret_cast<uint4*>(k.dec);
       for (int i = lane; i < S; i += 32) dst[i] = __ldg(src + i);   // 128-bit loads
       __syncwarp();
-      unsigned cnt = 0;
+      unsigned cnt = 0, diff = 0;
       for (int i0 = 0; i0 < S; i0 += 32) {
-        int i = i0 + lane;
-        unsigned b = __ballot_sync(0xffffffffu, i < S && k.dec[i].func != 0xFFFF);
-        cnt += __popc(b);
+        const int i = i0 + lane;
+        const bool live = i < S && k.dec[i].func != 0xFFFF;
+        cnt += __popc(__ballot_sync(0xffffffffu, live));
+        bool d = false;
+        if (i < S) {
+          const GsDecision& a = k.dec[i];
+          const GsDecision& b = k.pdec[i];
+          d = a.func != b.func || a.consumer != b.consumer || a.kind != b.kind;
+        }
+        diff |= __ballot_sync(0xffffffffu, d);
       }
-      if (lane == 0) { k.misc->ndec = (int)cnt; k.misc->err = 0; k.misc->nrows = 0; }
+      if (lane == 0) {
+        Misc& m = *k.misc;
+        m.same_struct = reuse && m.prev_valid && diff == 0 && (int)cnt == m.ndec;
+        m.ndec = (int)cnt; m.err = 0;
+        if (!m.same_struct) m.nrows = 0;
+      }
       __syncwarp();
       resolve<ND>(k);
       if (lane == 0) {
-        int v = k.misc->err ? 255 : prune_verdict<ND>(k);
-        if (k.misc->err) { atomicOr(gerr, k.misc->err); k.misc->nrows = 0; }
+        Misc& m = *k.misc;
+        int v = m.err ? 255 : prune_verdict<ND>(k);
+        if (m.err) { atomicOr(gerr, m.err); m.nrows = 0; }
         verdict[c] = (uint8_t)v;
-        n_rows[c] = k.misc->nrows;
+        n_rows[c] = m.nrows;
       }
     }
     __syncthreads();
-    const int nr = feats ? k.misc->nrows : 0;   // feats == NULL: prune verdict only
-    for (int r = warp; r < nr; r += nw) {
+    const Misc& m = *k.misc;
+    const int nr = feats ? m.nrows : 0;   // feats == NULL: prune verdict only
+    const bool diffable = m.same_struct && !m.err;
+    // which funcs' geometry changed since the previous candidate
+    if (diffable) {
+      constexpr int WPF = (int)(sizeof(CF<ND>) / 4);
+      for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+        const int32_t* a = reinterpret_cast<const int32_t*>(&k.cf[f]);
+        const int32_t* b = reinterpret_cast<const int32_t*>(&k.pcf[f]);
+        bool d = false;
+#pragma unroll 4
+        for (int w = 0; w < WPF; ++w) d |= a[w] != b[w];
+        k.dirty[f] = d;
+      }
+    }
+    __syncthreads();
+    // rows to recompute: own func, host, host kernel, read producers and
+    // fuse_at_thread children unchanged => features are bit-identical
+    for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+      bool d = true;
+      if (diffable) {
+        const int f = k.rows[r] >> 8;
+        const CF<ND>& g = k.cf[f];
+        const int host = g.kind == K_INLINE ? g.consumer : f;
+        d = k.dirty[f];
+        if (host >= 0) { d |= k.dirty[host]; if (k.cf[host].kernel >= 0) d |= k.dirty[k.cf[host].kernel]; }
+        for (int q = k.rdepb[r]; q < k.rdepb[r + 1] && !d; ++q) d |= k.dirty[k.rdep[q]];
+      }
+      rflag[r] = d;
+    }
+    __syncthreads();
+    if (warp == 0) {   // compact the dirty rows
+      int cntd = 0;
+      for (int r0 = 0; r0 < nr; r0 += 32) {
+        const int r = r0 + lane;
+        const bool d = r < nr && rflag[r];
+        const unsigned b = __ballot_sync(0xffffffffu, d);
+        if (d) k.rowlist[cntd + __popc(b & ((1u << lane) - 1))] = (int16_t)r;
+        cntd += __popc(b);
+      }
+      if (lane == 0) k.misc->ndirty = cntd;
+    }
+    __syncthreads();
+    const int nd = k.misc->ndirty;
+    for (int q = warp; q < nd; q += nw) {
+      const int r = k.rowlist[q];
       const int key = k.rows[r];
       const int f = key >> 8, si = key & 255;
       row_features<ND>(k, W, f, si, k.cf[f].kind == K_INLINE, feats + ((int64_t)c * L.R + r) * GS_NUM_FEATURES);
-      if (lane == 0) row_key[c * L.R + r] = key;
     }
+    // clean rows: copy the previous candidate's (same CTA, already visible)
+    for (int r = warp; r < nr; r += nw) {
+      if (lane == 0) row_key[c * L.R + r] = k.rows[r];
+      if (rflag[r]) continue;
+      const double* src = feats + ((int64_t)(c - 1) * L.R + r) * GS_NUM_FEATURES;
+      double* dst = feats + ((int64_t)c * L.R + r) * GS_NUM_FEATURES;
+      for (int i = lane; i < GS_NUM_FEATURES; i += 32) dst[i] = src[i];
+    }
+    __syncthreads();
+    { GsDecision* t = k.dec; k.dec = k.pdec; k.pdec = t; }
+    { CF<ND>* t = k.cf; k.cf = k.pcf; k.pcf = t; }
+    if (threadIdx.x == 0) k.misc->prev_valid = (k.misc->err == 0) && feats != nullptr;
+    // the new "current" CF buffer must not be diffed before it is rewritten:
+    // resolve() rewrites every func's record for a same-structure candidate
     __syncthreads();
   }
 }
@@ -1126,9 +1247,11 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   int o = 0;
   L.blob = o; o += al(blob_bytes);
   L.dec = o; o += al(S * 16);
+  L.pdec = o; o += al(S * 16);
   L.didx = o; o += al(nf * 2);
   int cfs = nd == 1 ? cf_size<1>() : nd == 2 ? cf_size<2>() : nd == 3 ? cf_size<3>() : cf_size<4>();
   L.cf = o; o += al(nf * cfs);
+  L.pcf = o; o += al(nf * cfs);
   L.reads = o; o += al(rcap * (int)sizeof(RRead));
   L.paths = o; o += al(pcap * 2);
   L.rdb = o; o += al(2 * ns * 4);
@@ -1136,7 +1259,15 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   L.rows = o; o += al(R * 4);
   L.stack = o; o += al((nf + 2) * (int)sizeof(Frame));
   L.volacc = o; o += al(nf * 8);
-  L.touched = o; o += al(2 * nf * 2 + 2);
+  L.touched = o; o += al(2 * nf * 2 + 4);
+  L.icall = o; o += al(pcap * (int)sizeof(ICall));
+  L.srcb = o; o += al((nf + 1) * 4);
+  L.srcl = o; o += al(rcap * 2);
+  L.rdepb = o; o += al((R + 1) * 4);
+  L.rdep = o; o += al((rcap + nf) * 2);
+  L.dirty = o; o += al(nf);
+  L.rflag = o; o += al(R);
+  L.rowlist = o; o += al(R * 2);
   L.misc = o; o += al((int)sizeof(Misc));
   L.warp_bytes = al((int)sizeof(WarpScr));
   L.warps = o; o += nwarps * L.warp_bytes;
@@ -1147,13 +1278,14 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
 
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, const Layout& L,
-                     int nwarps, int grid, int* gerr, cudaStream_t st) {
+                     int nwarps, int grid, int* gerr, int reuse, cudaStream_t st) {
   dim3 b(nwarps * 32);
   switch (nd) {
 #define GS_CASE(D)                                                                                  \
   case D:                                                                                           \
     cudaFuncSetAttribute(featurize_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total); \
-    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, L, gerr); g_launch_count++; \
+    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, L, gerr, reuse); \
+    g_launch_count++;                                                                               \
     break;
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4)
 #undef GS_CASE

@@ -49,6 +49,7 @@ struct CF {
   int32_t bbx[ND];                // root: thread*serial (block box extent)
   int32_t serial_prod;
   int32_t k_threads;              // kernel owner only: max threads per block
+  int32_t spare[(ND & 1) ? 2 : 1];  // explicit: no padding bytes (records are memcmp'd)
   int64_t realizations;
   int64_t calls;                  // inline: total calls
   int64_t best;                   // inline: best per-consumer calls
@@ -66,7 +67,8 @@ struct RRead {                // one expanded read (resolve.py:56-79 ResolvedRea
 };
 
 struct Layout {                 // byte offsets inside dynamic shared memory (K1)
-  int blob, dec, didx, cf, reads, paths, rdb, frd, rows, stack, volacc, touched, misc, warps;
+  int blob, dec, pdec, didx, cf, pcf, reads, paths, rdb, frd, rows, stack, volacc, touched, icall, srcb,
+      srcl, rdepb, rdep, dirty, rflag, rowlist, misc, warps;
   int warp_bytes, total;
   int rcap, pcap, S, R;
 };

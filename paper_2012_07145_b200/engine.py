@@ -59,6 +59,10 @@ class Scorer:
         except Exception:
             pass
 
+    def set_reuse(self, enable: bool):
+        """Exact sibling reuse in K1 (see gs_set_reuse in include/gs_sched.h)."""
+        _lib.check(self.lib.gs_set_reuse(self.handle, int(bool(enable))))
+
     # -- weights --------------------------------------------------------------
     def set_weights(self, weights):
         key = id(weights)

@@ -1,0 +1,84 @@
+"""Sibling reuse in K1 is exact: on beam-step batches (parents x all tilings
+of a step root, consecutive siblings) the features with reuse on are
+bit-identical to reuse off, and a subsample matches the CPU oracle."""
+
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from golden_io import PARAMS, weights  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda")
+
+
+def _decisions(info, rec):
+    from paper_2012_07145_b200.descriptor import KIND_NAME
+    from paper_2012_07145_b200.schedule import Decision
+    out = []
+    for r in rec:
+        if r["func"] == 0xFFFF:
+            break
+        nd = len(info.extents[int(r["func"])])
+        out.append((info.names[int(r["func"])], Decision(
+            KIND_NAME[int(r["kind"])],
+            None if r["consumer"] == 0xFFFF else info.names[int(r["consumer"])],
+            tuple(int(x) for x in r["serial"][:nd]) if r["flags"] & 1 else None,
+            tuple(int(x) for x in r["thread"][:nd]) if r["flags"] & 2 else None)))
+    return tuple(out)
+
+
+def _run(sc, recs, reuse):
+    sc.set_reuse(reuse)
+    dec = sc.to_device(recs)
+    f = sc.featurize(dec)
+    total, _, _ = sc.cost(f)
+    sc.check()
+    return {k: v.cpu().numpy() for k, v in f.items()}, total.cpu().numpy()
+
+
+@pytest.mark.parametrize("src", ["chain100", "stencil_chain", "diamond", "conv"])
+def test_reuse_is_bit_exact(src, dev):
+    from paper_2012_07145_b200 import gen
+    from paper_2012_07145_b200.engine import Scorer
+    from paper_2012_07145_b200.params import OPEN_THRESHOLDS
+    from golden_io import candidate_set
+    if src == "chain100":
+        import bench
+        graph, recs, _ = bench._workload(3)
+        th = None
+    else:
+        graph = candidate_set(src).graph
+        par, _, _ = gen.random_schedules(graph, 6, seed=11)
+        info = gen.GraphInfo(graph)
+        steps = np.array([[i for i in range(par.shape[1]) if par[p, i]["kind"] == 0][0]
+                          for p in range(len(par))])
+        recs, _ = gen.expand_step(par, steps, graph)
+        th = OPEN_THRESHOLDS
+    sc = Scorer(graph, PARAMS, th, weights())
+    on, t_on = _run(sc, recs, True)
+    off, t_off = _run(sc, recs, False)
+    assert np.array_equal(on["n_rows"], off["n_rows"])
+    assert np.array_equal(on["verdict"], off["verdict"])
+    for i in range(len(recs)):
+        r = on["n_rows"][i]
+        assert np.array_equal(on["feats"][i, :r], off["feats"][i, :r]), (src, i)
+        assert np.array_equal(on["row_key"][i, :r], off["row_key"][i, :r])
+    assert np.array_equal(t_on, t_off)
+    # oracle on a strided subsample (siblings of different parents)
+    from oracle import features
+    info = gen.GraphInfo(graph)
+    for i in range(0, len(recs), max(1, len(recs) // 5)):
+        rows = features.featurize_rows(graph, _decisions(info, recs[i]), PARAMS)
+        want = np.array([f for _, f, _ in rows])
+        assert np.array_equal(on["feats"][i, :len(rows)], want), (src, i)
