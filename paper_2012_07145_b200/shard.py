@@ -81,24 +81,7 @@ class StepPlan:
                 "n_reps": int(costs.shape[0])}
 
     def _exchange(self, costs, ph, cand, nrep):
-        import torch.distributed as dist
-        rec = torch.stack([ph, costs.view(torch.int64), cand,
-                           torch.arange(nrep, device=costs.device, dtype=torch.int64)], dim=1)
-        counts = torch.tensor([nrep], device=costs.device, dtype=torch.int64)
-        allc = torch.empty(self.world, device=costs.device, dtype=torch.int64)
-        dist.all_gather_into_tensor(allc, counts)
-        mx = int(allc.max().item())
-        pad = torch.zeros((mx, 4), device=costs.device, dtype=torch.int64)
-        pad[:nrep] = rec
-        allr = torch.empty((self.world * mx, 4), device=costs.device, dtype=torch.int64)
-        dist.all_gather_into_tensor(allr, pad)
-        keep = torch.cat([torch.arange(r * mx, r * mx + int(allc[r]), device=costs.device)
-                          for r in range(self.world)])
-        allr = allr.index_select(0, keep)
-        # global representative order: (hash as uint64 ascending, local order)
-        order = torch.sort(allr[:, 0] ^ SIGN, stable=True).indices
-        allr = allr.index_select(0, order)
-        return allr[:, 1].view(torch.float64).contiguous(), allr[:, 0].contiguous(), allr[:, 2].contiguous()
+        return exchange_reps(costs, ph, cand, self.world)
 
     def run_host(self, host_u8):
         """Public batch entry with host buffers: H2D records, one step, D2H of
@@ -109,3 +92,40 @@ class StepPlan:
         ver = out["verdict"].cpu()
         return {"h2d_bytes": host_u8.numel(), "d2h_bytes": tot.numel() * 8 + ver.numel() + 8 * len(out["beam"]),
                 "beam": out["beam"]}
+
+
+def exchange_reps(costs, ph, cand, world, group=None):
+    """All-gather every rank's representative records and merge them into
+    the global representative order of the reference (search.py:151-164:
+    hash ascending, then permutation position inside the bucket).
+
+    Each record is 4 x int64: (hash at pass depth, fp64 cost bits, candidate
+    index, local rep order).  Buckets never straddle ranks (owner = hash %
+    world), so a stable sort by unsigned hash over the rank-major
+    concatenation reproduces the single-GPU order exactly.  Works with any
+    torch.distributed backend (NCCL on the GPU path, gloo in the CPU tests).
+    Returns (costs f64, pass hashes i64, candidate indices i64)."""
+    import torch.distributed as dist
+    nrep = int(costs.shape[0])
+    dev = costs.device
+    rec = torch.stack([ph, costs.view(torch.int64), cand,
+                       torch.arange(nrep, device=dev, dtype=torch.int64)], dim=1)
+    counts = torch.tensor([nrep], device=dev, dtype=torch.int64)
+    allc = [torch.empty_like(counts) for _ in range(world)]
+    dist.all_gather(allc, counts, group=group)
+    allc = torch.cat(allc).cpu().tolist()
+    mx = max(1, max(allc))
+    pad = torch.zeros((mx, 4), device=dev, dtype=torch.int64)
+    pad[:nrep] = rec
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    allr = merge_rep_records([p[:c] for p, c in zip(parts, allc)])
+    return allr[:, 1].view(torch.float64).contiguous(), allr[:, 0].contiguous(), allr[:, 2].contiguous()
+
+
+def merge_rep_records(parts):
+    """Rank-major concatenation of [n_r, 4] int64 records, stably sorted by
+    the unsigned 64-bit hash in column 0."""
+    allr = torch.cat(parts, dim=0)
+    order = torch.sort(allr[:, 0] ^ SIGN, stable=True).indices
+    return allr.index_select(0, order)
