@@ -142,12 +142,15 @@ int gs_set_weights(gs_pipeline_t p, int embed_dim, int hidden_dim,
  * predecessor's, and a row is recomputed only if its own / host / kernel /
  * read-producer / thread-child records changed — otherwise its features are
  * copied, which is bit-identical by construction.  0 disables (every row of
- * every candidate is computed). */
+ * every candidate is computed).  `row_src` (nullable, [N][R] int32) then
+ * names, per row, the candidate whose row was actually computed and whose
+ * features this row repeats bit for bit (itself when computed); gs_cost
+ * uses it to evaluate the network once per distinct row. */
 int gs_set_reuse(gs_pipeline_t p, int enable);
 
 int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
                  double* feats, int32_t* row_key, int32_t* n_rows,
-                 uint8_t* verdict, void* stream);
+                 uint8_t* verdict, int32_t* row_src, void* stream);
 
 /* K2: basis + two-tower network + g.c + h + in-order stage sum.  Replaces
  * CostEvaluator.cost (search.py:115-124).  row_cost/basis_gh optional
@@ -189,6 +192,12 @@ int gs_beam_topk(const double* costs, const uint64_t* pass_hash, int64_t n,
                  double temperature, uint64_t phase_seed, int64_t k, double tie_band,
                  void* workspace, int64_t ws_bytes, int64_t* out_pos,
                  int64_t* n_out, uint8_t* bottom, void* stream);
+
+/* K1 work counters accumulated since the last call (then reset);
+ * synchronizes `stream`.  out[0] candidates, [1] candidates resolved
+ * incrementally (sibling of the previous one), [2] feature rows computed,
+ * [3] feature rows emitted, [4] func geometries (re)resolved, [5] reserved. */
+int gs_stats(gs_pipeline_t p, int64_t* out, void* stream);
 
 /* Device-side error word of the last K1 launch (capacity overflow etc.);
  * synchronizes `stream`. */

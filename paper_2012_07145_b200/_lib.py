@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(HERE, "libgs_sched.so")
 EXPORTS = ("gs_last_error", "gs_version", "gs_launch_count", "gs_pipeline_create", "gs_pipeline_destroy",
            "gs_pipeline_max_rows", "gs_set_weights", "gs_set_reuse", "gs_featurize", "gs_cost",
            "gs_struct_hash", "gs_select_workspace_bytes", "gs_select_reps",
-           "gs_topk_workspace_bytes", "gs_beam_topk", "gs_check")
+           "gs_topk_workspace_bytes", "gs_beam_topk", "gs_check", "gs_stats")
 
 
 class GsError(RuntimeError):
@@ -46,7 +46,7 @@ def load(path: str = LIB_PATH):
         "gs_pipeline_max_rows": (i32, [P]),
         "gs_set_weights": (i32, [P, i32, i32] + [V] * 8),
         "gs_set_reuse": (i32, [P, i32]),
-        "gs_featurize": (i32, [P, V, i64, i32, V, V, V, V, V]),
+        "gs_featurize": (i32, [P, V, i64, i32, V, V, V, V, V, V]),
         "gs_cost": (i32, [P, V, V, V, i64, V, V, V, V]),
         "gs_struct_hash": (i32, [P, V, i64, i32, i32, V, V]),
         "gs_select_workspace_bytes": (i64, [i64]),
@@ -54,6 +54,7 @@ def load(path: str = LIB_PATH):
         "gs_topk_workspace_bytes": (i64, [i64]),
         "gs_beam_topk": (i32, [V, V, i64, V, i64, dbl, dbl, u64, i64, dbl, V, i64, V, V, V, V]),
         "gs_check": (i32, [P, V]),
+        "gs_stats": (i32, [P, V, V]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -9,8 +9,8 @@
 namespace gs {
 Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rcap, int pcap, int nwarps);
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
-                     double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, const Layout& L,
-                     int nwarps, int grid, int* gerr, int reuse, cudaStream_t st);
+                     double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
+                     const Layout& L, int nwarps, int grid, int* gerr, int reuse, cudaStream_t st);
 int featurize_occupancy(int nd, int nwarps, int smem);
 int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st);
 int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
@@ -162,8 +162,8 @@ int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
   CK(cudaMemcpy(p->names, d->name_repr, nb, cudaMemcpyHostToDevice));
   CK(cudaMalloc(&p->name_off, 4 * (h.nf + 1)));
   CK(cudaMemcpy(p->name_off, d->name_off, 4 * (h.nf + 1), cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&p->err, sizeof(int)));
-  CK(cudaMemset(p->err, 0, sizeof(int)));
+  CK(cudaMalloc(&p->err, 64));   // [0] error word, [2..] K1 work counters (u64)
+  CK(cudaMemset(p->err, 0, 64));
   *out = p;
   return GS_OK;
 }
@@ -215,7 +215,7 @@ int gs_set_reuse(gs_pipeline_t p, int enable) {
 }
 
 int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, double* feats, int32_t* row_key,
-                 int32_t* n_rows, uint8_t* verdict, void* stream) {
+                 int32_t* n_rows, uint8_t* verdict, int32_t* row_src, void* stream) {
   if (!p || S < 1 || n < 0) return fail(GS_ERR_ARG, "bad featurize arguments");
   if (n == 0) return GS_OK;
   const int nwarps = p->nwarps;
@@ -227,7 +227,7 @@ int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, doubl
   if (occ < 1) occ = 1;
   int64_t grid = (int64_t)p->num_sms * occ;
   if (grid > n) grid = n;
-  int rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, L, nwarps,
+  int rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, nwarps,
                             (int)grid, p->err, p->reuse, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "unsupported ndim");
   CK(cudaGetLastError());
@@ -261,6 +261,14 @@ int gs_struct_hash(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, int
   int rc = launch_hash(dec, n, S, p->host.nf, depth, p->sorted, p->names, p->name_off, out, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "too many funcs for the hash kernel");
   CK(cudaGetLastError());
+  return GS_OK;
+}
+
+int gs_stats(gs_pipeline_t p, int64_t* out, void* stream) {
+  if (!p || !out) return fail(GS_ERR_ARG, "null argument");
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  CK(cudaMemcpy(out, p->err + 2, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(p->err + 2, 0, 6 * sizeof(int64_t)));
   return GS_OK;
 }
 

@@ -28,6 +28,7 @@ struct ICall { int16_t root, iname, stage, pad; int64_t vol; };   // per (root s
 struct WarpScr {
   double feat[GS_NUM_FEATURES];
   unsigned long long H[kMaxM], S[kMaxM], T[kMaxM];
+  int16_t nz[kMaxM];
   unsigned long long acc[4][3][2];      // box x tier x (bytes, lines)
   int16_t rl[kRowReads];
   int8_t grp[kRowReads];
@@ -38,8 +39,11 @@ struct WarpScr {
 };
 
 struct Misc {
-  int ndec, nreads, npath, nrows, nicall, err, verdict, same_struct, prev_valid, ndirty, pad0, pad1;
+  int ndec, nreads, npath, nrows, nicall, err, verdict, same_struct, prev_valid, ndirty, ngeo, incr;
+  int64_t ni;          // structure: sum of scheduled funcs' domain volumes (prune rule 1)
 };
+
+constexpr int kMaxMaskWords = 8;   // incremental resolve for pipelines of <= 256 funcs
 
 template <int ND>
 struct K1 {
@@ -67,7 +71,19 @@ struct K1 {
   int16_t* rdep;     // [rcap + nf]
   uint8_t* dirty;    // [nf]
   int16_t* rowlist;  // [R] rows to recompute this candidate
+  // incremental resolve (structure-time metadata + per-candidate flags)
+  int16_t* kern;     // [nf] kernel owner of each non-inline func (kernel_of)
+  uint32_t* dm;      // [nf][mw] funcs whose decision records f's geometry depends on
+  uint32_t* cmask;   // [mw] funcs whose decision record changed vs the previous candidate
+  int32_t* kmb;      // [nf+1] CSR: fused members of each kernel owner
+  int16_t* kml;      // [nf]
+  int32_t* icb;      // [nf+1] CSR: icall entries per inline func (icall order)
+  int16_t* icl;      // [pcap]
+  int16_t* dlist;    // [nf] decision indices whose geometry is recomputed
+  uint8_t* gdirty;   // [nf] geometry recomputed this candidate
+  uint8_t* kdirty;   // [nf] kernel aggregates recomputed this candidate
   Misc* misc;
+  int mw;            // mask words (0 = incremental resolve off)
   int rcap, pcap;
   int* gerr;
 };
@@ -240,6 +256,83 @@ __device__ void resolve_structure(K1<ND>& k) {
           k.rdep[nd++] = (int16_t)k.dec[i].func;
   }
   k.rdepb[nr] = nd;
+
+  // prune rule 1 denominator: sum of scheduled funcs' domains (options.py:215-222)
+  int64_t ni = 0;
+  for (int i = 0; i < m.ndec; ++i) {
+    const GsFunc& fn = k.F[k.dec[i].func];
+    int64_t dom = 1;
+    for (int dd = 0; dd < fn.ndim; ++dd) dom *= fn.extent[dd];
+    ni += dom;
+  }
+  m.ni = ni;
+
+  // ---- metadata for incremental sibling resolve --------------------------
+  // kernel owner of every non-inline func: itself for roots, the owner of
+  // its first fusion source's root otherwise (= cg0.kernel in geometry)
+  for (int f = 0; f < nf; ++f) k.kern[f] = -1;
+  for (int i = 0; i < m.ndec; ++i) {
+    const GsDecision& d = k.dec[i];
+    if (d.kind == GS_INLINE) continue;
+    if (d.kind == GS_ROOT) { k.kern[d.func] = (int16_t)d.func; continue; }
+    for (int q = k.srcb[d.func]; q < k.srcb[d.func + 1]; ++q)
+      if (k.didx[k.rd[k.srcl[q]].root] < i) { k.kern[d.func] = k.kern[k.rd[k.srcl[q]].root]; break; }
+  }
+  // fused members per kernel owner (decision order)
+  for (int f = 0; f <= nf; ++f) k.kmb[f] = 0;
+  for (int i = 0; i < m.ndec; ++i) {
+    const GsDecision& d = k.dec[i];
+    if ((d.kind == GS_FUSE_BLOCK || d.kind == GS_FUSE_THREAD) && k.kern[d.func] >= 0) k.kmb[k.kern[d.func] + 1]++;
+  }
+  for (int f = 0; f < nf; ++f) k.kmb[f + 1] += k.kmb[f];
+  for (int f = 0; f < nf; ++f) k.volacc[f] = k.kmb[f];
+  for (int i = 0; i < m.ndec; ++i) {
+    const GsDecision& d = k.dec[i];
+    if ((d.kind == GS_FUSE_BLOCK || d.kind == GS_FUSE_THREAD) && k.kern[d.func] >= 0)
+      k.kml[k.volacc[k.kern[d.func]]++] = (int16_t)d.func;
+  }
+  // icall entries per inline func, icall order kept (first max wins)
+  for (int f = 0; f <= nf; ++f) k.icb[f] = 0;
+  for (int e = 0; e < m.nicall; ++e) k.icb[k.icall[e].iname + 1]++;
+  for (int f = 0; f < nf; ++f) k.icb[f + 1] += k.icb[f];
+  for (int f = 0; f < nf; ++f) k.volacc[f] = k.icb[f];
+  for (int e = 0; e < m.nicall; ++e) k.icl[k.volacc[k.icall[e].iname]++] = (int16_t)e;
+  for (int f = 0; f < nf; ++f) k.volacc[f] = 0;
+  // dependency masks: dm[f] = decision records f's geometry record depends
+  // on (transitively), in resolve order; geometry only flows forward
+  const int mw = k.mw;
+  if (mw > 0) {
+    uint32_t* dm = k.dm;
+    for (int j = 0; j < nf * mw; ++j) dm[j] = 0;
+    auto orm = [&](int dst, int src) { for (int w = 0; w < mw; ++w) dm[dst * mw + w] |= dm[src * mw + w]; };
+    for (int i = 0; i < m.ndec; ++i) {
+      const GsDecision& d = k.dec[i];
+      if (d.kind == GS_INLINE) continue;
+      const int f = d.func;
+      dm[f * mw + (f >> 5)] |= 1u << (f & 31);
+      if (d.kind == GS_ROOT) continue;
+      for (int q = k.srcb[f]; q < k.srcb[f + 1]; ++q) {
+        const int r = k.rd[k.srcl[q]].root;
+        if (k.didx[r] < i) orm(f, r);
+      }
+      if (k.kern[f] >= 0) orm(f, k.kern[f]);
+    }
+    for (int f = 0; f < nf; ++f) {
+      if (!(k.F[f].is_external || k.didx[f] < 0)) continue;
+      for (int q = k.srcb[f]; q < k.srcb[f + 1]; ++q) orm(f, k.rd[k.srcl[q]].root);
+    }
+    for (int i = 0; i < m.ndec; ++i) {
+      const GsDecision& d = k.dec[i];
+      if (d.kind != GS_INLINE) continue;
+      const int f = d.func;
+      dm[f * mw + (f >> 5)] |= 1u << (f & 31);
+      for (int q = k.icb[f]; q < k.icb[f + 1]; ++q) {
+        const int r = k.icall[k.icl[q]].root;
+        orm(f, r);
+        if (k.kern[r] >= 0) orm(f, k.kern[r]);
+      }
+    }
+  }
 }
 
 template <int ND>
@@ -249,220 +342,230 @@ __device__ __forceinline__ void zero_cf(CF<ND>& c) {
   for (int i = 0; i < (int)(sizeof(CF<ND>) / 4); ++i) w[i] = 0;
 }
 
+// Geometry of the non-inline decision i (resolve.py:232-333); warp-wide.
+// Kernel aggregates (threads per block = max, shared bytes = sum over the
+// kernel's members) are NOT accumulated here but by kernel_aggregates():
+// no member's geometry reads them, so the result is the same and a
+// sibling that changes one member recomputes only its kernel's sums.
 template <int ND>
-__device__ void resolve_geometry(K1<ND>& k) {
+__device__ bool geometry_one(K1<ND>& k, int i) {
   const int lane = lane_id();
   Misc& m = *k.misc;
-  const int nf = k.P->nf;
-  // Pass 1: geometry of non-inline funcs in decision order (resolve.py:232-333)
-  for (int i = 0; i < m.ndec; ++i) {
-    const GsDecision d = k.dec[i];
-    if (d.kind == GS_INLINE) continue;
-    const int f = d.func;
-    const GsFunc& fn = k.F[f];
-    CF<ND> c;
-    zero_cf(c);
-    c.consumer = (d.kind == GS_ROOT) ? -1 : (int16_t)d.consumer;
-    c.serial_prod = 1;
-    if (d.kind == GS_ROOT) {
-      int32_t ser[ND], thr[ND];
-      const bool tiled = (d.flags & 3) == 3;
-      int inner = 0;
-      if (!tiled) {  // provisional tiling (resolve.py:159-164)
-        inner = -1;
-        for (int dd = 0; dd < fn.ndim; ++dd) if (fn.extent[dd] >= 16) { inner = dd; break; }
-        if (inner < 0) inner = 0;
-      }
-      int64_t nb = 1, nt = 1, sp = 1;
-#pragma unroll
-      for (int dd = 0; dd < ND; ++dd) {
-        int e = dd < fn.ndim ? fn.extent[dd] : 1;
-        ser[dd] = tiled ? d.serial[dd] : 1;
-        thr[dd] = tiled ? d.thread[dd] : (dd == inner ? (e < 32 ? e : 32) : 1);
-        int64_t st = (int64_t)ser[dd] * thr[dd];
-        int64_t b = (e + st - 1) / st;
-        if (b < 1) b = 1;
-        nb *= b; nt *= thr[dd]; sp *= ser[dd];
-        c.rlo[dd] = 0; c.rhi[dd] = (int32_t)(b * st - 1);
-        c.tlo[dd] = c.rlo[dd]; c.thi[dd] = c.rhi[dd];
-        c.ctx[dd] = thr[dd]; c.base[dd] = 0; c.coeff[dd] = ser[dd]; c.ext[dd] = ser[dd];
-        c.bbx[dd] = (int32_t)st;
-      }
-      c.kind = K_ROOT; c.tier = T_GLOBAL; c.kernel = (int16_t)f; c.realizations = 1;
-      c.n_threads = (int32_t)nt; c.unrolled = sp < 16; c.has_serial = 1; c.serial_prod = (int32_t)sp;
-      c.n_blocks = nb; c.k_threads = (int32_t)nt; c.k_shared = 0;
-      if (lane == 0) k.cf[f] = c;
-      __syncwarp();
-      continue;
+  const GsDecision d = k.dec[i];
+  const int f = d.func;
+  const GsFunc& fn = k.F[f];
+  CF<ND> c;
+  zero_cf(c);
+  c.consumer = (d.kind == GS_ROOT) ? -1 : (int16_t)d.consumer;
+  c.serial_prod = 1;
+  if (d.kind == GS_ROOT) {
+    int32_t ser[ND], thr[ND];
+    const bool tiled = (d.flags & 3) == 3;
+    int inner = 0;
+    if (!tiled) {  // provisional tiling (resolve.py:159-164)
+      inner = -1;
+      for (int dd = 0; dd < fn.ndim; ++dd) if (fn.extent[dd] >= 16) { inner = dd; break; }
+      if (inner < 0) inner = 0;
     }
-    // fusion sources: reads of f issued by funcs resolved before it (resolve.py:379-393)
-    const int sb = k.srcb[f], se = k.srcb[f + 1];
-    int first = -1;
-    for (int q = sb; q < se; ++q)
-      if (k.didx[k.rd[k.srcl[q]].root] < i) { first = k.srcl[q]; break; }
-    if (first < 0) { if (lane == 0) m.err |= E_SCHEDULE; __syncwarp(); return; }
-    const CF<ND> cg0 = k.cf[k.rd[first].root];
-    int64_t lo[ND], hi[ND], tlo[ND], thi[ND], ts0[ND];
-#pragma unroll
-    for (int dd = 0; dd < ND; ++dd) { lo[dd] = tlo[dd] = INT64_MAX; hi[dd] = thi[dd] = INT64_MIN; ts0[dd] = 1; }
-    {
-      const RRead& r0 = k.rd[first];
-      for (int q = 0; q < r0.plen; ++q)
-#pragma unroll
-        for (int dd = 0; dd < ND; ++dd) ts0[dd] *= k.A[k.path[r0.pbeg + q]].s[dd];
-    }
-    for (int q0 = sb; q0 < se; q0 += 32) {
-      const int q = q0 + lane;
-      if (q < se) {
-        const RRead& r = k.rd[k.srcl[q]];
-        if (k.didx[r.root] < i) {
-          const CF<ND>& cg = (d.kind == GS_FUSE_THREAD) ? cg0 : k.cf[r.root];
-          int32_t blo[ND], bhi[ND];
-          if (d.kind == GS_FUSE_BLOCK) block_box(cg, blo, bhi);
-          else {
-#pragma unroll
-            for (int dd = 0; dd < ND; ++dd) { blo[dd] = cg.base[dd]; bhi[dd] = cg.base[dd] + cg.ext[dd] - 1; }
-          }
-#pragma unroll
-          for (int dd = 0; dd < ND; ++dd) {
-            int64_t a = blo[dd], b = bhi[dd];
-            chain_iv(k.A, k.path + r.pbeg, r.plen, dd, a, b);
-            lo[dd] = a < lo[dd] ? a : lo[dd]; hi[dd] = b > hi[dd] ? b : hi[dd];
-            int64_t ta = cg.tlo[dd], tb = cg.thi[dd];
-            chain_iv(k.A, k.path + r.pbeg, r.plen, dd, ta, tb);
-            tlo[dd] = ta < tlo[dd] ? ta : tlo[dd]; thi[dd] = tb > thi[dd] ? tb : thi[dd];
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int dd = 0; dd < ND; ++dd) {
-      lo[dd] = wmin64(lo[dd]); hi[dd] = wmax64(hi[dd]);
-      tlo[dd] = wmin64(tlo[dd]); thi[dd] = wmax64(thi[dd]);
-    }
-    CF<ND>& K = k.cf[cg0.kernel];
-    if (d.kind == GS_FUSE_BLOCK) {
-      int64_t nt = 1, sp = 1;
-#pragma unroll
-      for (int dd = 0; dd < ND; ++dd) {
-        int s = (d.flags & 1) ? d.serial[dd] : 1;
-        int64_t t = (hi[dd] - lo[dd] + 1 + s - 1) / s;
-        if (t < 1) t = 1;
-        c.rlo[dd] = (int32_t)lo[dd];
-        c.rhi[dd] = (int32_t)(lo[dd] + t * s - 1);
-        c.tlo[dd] = (int32_t)tlo[dd];
-        int64_t th = tlo[dd] + t * s - 1;
-        c.thi[dd] = (int32_t)(thi[dd] > th ? thi[dd] : th);
-        c.ctx[dd] = (int32_t)t; c.base[dd] = c.rlo[dd]; c.coeff[dd] = s; c.ext[dd] = s;
-        nt *= t; sp *= s;
-      }
-      c.kind = K_BLOCK; c.tier = T_SHARED; c.kernel = cg0.kernel; c.realizations = K.n_blocks;
-      c.n_threads = (int32_t)nt; c.unrolled = sp < 16; c.has_serial = 1; c.serial_prod = (int32_t)sp;
-      __syncwarp();
-      if (lane == 0) {
-        k.cf[f] = c;
-        if (c.n_threads > K.k_threads) K.k_threads = c.n_threads;
-        K.k_shared += alloc_of(c) * fn.elem_bytes;
-      }
-    } else {
-      int64_t pe = 1;
-#pragma unroll
-      for (int dd = 0; dd < ND; ++dd) {
-        c.rlo[dd] = (int32_t)lo[dd]; c.rhi[dd] = (int32_t)hi[dd];
-        c.tlo[dd] = (int32_t)tlo[dd]; c.thi[dd] = (int32_t)thi[dd];
-        c.ctx[dd] = cg0.ctx[dd]; c.base[dd] = c.rlo[dd];
-        c.coeff[dd] = (int32_t)(cg0.coeff[dd] * ts0[dd]);
-        c.ext[dd] = (int32_t)(hi[dd] - lo[dd] + 1);
-        pe *= c.ext[dd];
-      }
-      c.kind = K_THREAD; c.tier = T_REGISTER; c.kernel = cg0.kernel;
-      c.realizations = K.n_blocks * (int64_t)cg0.n_threads; c.n_threads = cg0.n_threads;
-      c.unrolled = pe < 16; c.has_serial = 0; c.serial_prod = 1;
-      __syncwarp();
-      if (lane == 0) {
-        k.cf[f] = c;
-        if (c.n_threads > K.k_threads) K.k_threads = c.n_threads;
-      }
-    }
-    __syncwarp();
-  }
-
-  // externals and unscheduled producers (resolve.py:396-425): lane per func
-  for (int f = lane; f < nf; f += 32) {
-    const GsFunc& fn = k.F[f];
-    if (!(fn.is_external || k.didx[f] < 0)) continue;
-    int64_t lo[ND], hi[ND];
-#pragma unroll
-    for (int dd = 0; dd < ND; ++dd) { lo[dd] = INT64_MAX; hi[dd] = INT64_MIN; }
-    const int sb = k.srcb[f], se = k.srcb[f + 1];
-    for (int q = sb; q < se; ++q) {
-      const RRead& r = k.rd[k.srcl[q]];
-      const CF<ND>& cg = k.cf[r.root];
-#pragma unroll
-      for (int dd = 0; dd < ND; ++dd) {
-        int64_t a = cg.tlo[dd], b = cg.thi[dd];
-        chain_iv(k.A, k.path + r.pbeg, r.plen, dd, a, b);
-        lo[dd] = a < lo[dd] ? a : lo[dd]; hi[dd] = b > hi[dd] ? b : hi[dd];
-      }
-    }
-    CF<ND> c;
-    zero_cf(c);
-    c.kind = K_EXTERNAL; c.tier = T_GLOBAL; c.kernel = -1; c.consumer = -1; c.n_threads = 1; c.serial_prod = 1;
+    int64_t nb = 1, nt = 1, sp = 1;
 #pragma unroll
     for (int dd = 0; dd < ND; ++dd) {
       int e = dd < fn.ndim ? fn.extent[dd] : 1;
-      c.rlo[dd] = se > sb ? (int32_t)lo[dd] : 0; c.rhi[dd] = se > sb ? (int32_t)hi[dd] : e - 1;
+      ser[dd] = tiled ? d.serial[dd] : 1;
+      thr[dd] = tiled ? d.thread[dd] : (dd == inner ? (e < 32 ? e : 32) : 1);
+      int64_t st = (int64_t)ser[dd] * thr[dd];
+      int64_t b = (e + st - 1) / st;
+      if (b < 1) b = 1;
+      nb *= b; nt *= thr[dd]; sp *= ser[dd];
+      c.rlo[dd] = 0; c.rhi[dd] = (int32_t)(b * st - 1);
       c.tlo[dd] = c.rlo[dd]; c.thi[dd] = c.rhi[dd];
-      c.ctx[dd] = 1; c.ext[dd] = 1;
+      c.ctx[dd] = thr[dd]; c.base[dd] = 0; c.coeff[dd] = ser[dd]; c.ext[dd] = ser[dd];
+      c.bbx[dd] = (int32_t)st;
     }
-    k.cf[f] = c;
+    c.kind = K_ROOT; c.tier = T_GLOBAL; c.kernel = (int16_t)f; c.realizations = 1;
+    c.n_threads = (int32_t)nt; c.unrolled = sp < 16; c.has_serial = 1; c.serial_prod = (int32_t)sp;
+    c.n_blocks = nb; c.k_threads = (int32_t)nt; c.k_shared = 0;
+    if (lane == 0) k.cf[f] = c;
+    __syncwarp();
+    return true;
   }
-  __syncwarp();
-
-  // inline call totals / primaries (resolve.py:337-349) and inline records
-  if (lane == 0) {
-    for (int i = 0; i < m.ndec; ++i) {
-      const GsDecision& d = k.dec[i];
-      if (d.kind != GS_INLINE) continue;
-      CF<ND>& ic = k.cf[d.func];
-      zero_cf(ic);
-      ic.kind = K_INLINE; ic.consumer = -1;
-    }
-    for (int e = 0; e < m.nicall; ++e) {
-      const ICall& x = k.icall[e];
-      const CF<ND>& c = k.cf[x.root];
-      const int64_t calls = x.vol * prod_ext(c) * c.n_threads * k.cf[c.kernel].n_blocks;
-      CF<ND>& ic = k.cf[x.iname];
-      ic.calls += calls;
-      if (calls > ic.best) { ic.best = calls; ic.consumer = x.root; }
-    }
-    for (int i = 0; i < m.ndec; ++i) {
-      const GsDecision& d = k.dec[i];
-      if (d.kind != GS_INLINE) continue;
-      CF<ND>& ic = k.cf[d.func];
-      const int prim = ic.consumer;
-      ic.tier = T_NONE; ic.serial_prod = 1;
-      if (prim >= 0) {
-        const CF<ND>& h = k.cf[prim];
-        ic.kernel = h.kernel; ic.n_threads = h.n_threads; ic.unrolled = h.unrolled;
-        for (int dd = 0; dd < ND; ++dd) ic.ctx[dd] = h.ctx[dd];
-      } else {
-        ic.kernel = -1; ic.n_threads = 1; ic.unrolled = 1;
-        for (int dd = 0; dd < ND; ++dd) ic.ctx[dd] = 1;
+  // fusion sources: reads of f issued by funcs resolved before it (resolve.py:379-393)
+  const int sb = k.srcb[f], se = k.srcb[f + 1];
+  int first = -1;
+  for (int q = sb; q < se; ++q)
+    if (k.didx[k.rd[k.srcl[q]].root] < i) { first = k.srcl[q]; break; }
+  if (first < 0) { if (lane == 0) m.err |= E_SCHEDULE; __syncwarp(); return false; }
+  const CF<ND> cg0 = k.cf[k.rd[first].root];
+  int64_t lo[ND], hi[ND], tlo[ND], thi[ND], ts0[ND];
+#pragma unroll
+  for (int dd = 0; dd < ND; ++dd) { lo[dd] = tlo[dd] = INT64_MAX; hi[dd] = thi[dd] = INT64_MIN; ts0[dd] = 1; }
+  {
+    const RRead& r0 = k.rd[first];
+    for (int q = 0; q < r0.plen; ++q)
+#pragma unroll
+      for (int dd = 0; dd < ND; ++dd) ts0[dd] *= k.A[k.path[r0.pbeg + q]].s[dd];
+  }
+  for (int q0 = sb; q0 < se; q0 += 32) {
+    const int q = q0 + lane;
+    if (q < se) {
+      const RRead& r = k.rd[k.srcl[q]];
+      if (k.didx[r.root] < i) {
+        const CF<ND>& cg = (d.kind == GS_FUSE_THREAD) ? cg0 : k.cf[r.root];
+        int32_t blo[ND], bhi[ND];
+        if (d.kind == GS_FUSE_BLOCK) block_box(cg, blo, bhi);
+        else {
+#pragma unroll
+          for (int dd = 0; dd < ND; ++dd) { blo[dd] = cg.base[dd]; bhi[dd] = cg.base[dd] + cg.ext[dd] - 1; }
+        }
+#pragma unroll
+        for (int dd = 0; dd < ND; ++dd) {
+          int64_t a = blo[dd], b = bhi[dd];
+          chain_iv(k.A, k.path + r.pbeg, r.plen, dd, a, b);
+          lo[dd] = a < lo[dd] ? a : lo[dd]; hi[dd] = b > hi[dd] ? b : hi[dd];
+          int64_t ta = cg.tlo[dd], tb = cg.thi[dd];
+          chain_iv(k.A, k.path + r.pbeg, r.plen, dd, ta, tb);
+          tlo[dd] = ta < tlo[dd] ? ta : tlo[dd]; thi[dd] = tb > thi[dd] ? tb : thi[dd];
+        }
       }
-      for (int dd = 0; dd < ND; ++dd) { ic.rhi[dd] = -1; ic.thi[dd] = -1; ic.ext[dd] = 1; }
     }
   }
+#pragma unroll
+  for (int dd = 0; dd < ND; ++dd) {
+    lo[dd] = wmin64(lo[dd]); hi[dd] = wmax64(hi[dd]);
+    tlo[dd] = wmin64(tlo[dd]); thi[dd] = wmax64(thi[dd]);
+  }
+  const CF<ND>& K = k.cf[cg0.kernel];
+  if (d.kind == GS_FUSE_BLOCK) {
+    int64_t nt = 1, sp = 1;
+#pragma unroll
+    for (int dd = 0; dd < ND; ++dd) {
+      int s = (d.flags & 1) ? d.serial[dd] : 1;
+      int64_t t = (hi[dd] - lo[dd] + 1 + s - 1) / s;
+      if (t < 1) t = 1;
+      c.rlo[dd] = (int32_t)lo[dd];
+      c.rhi[dd] = (int32_t)(lo[dd] + t * s - 1);
+      c.tlo[dd] = (int32_t)tlo[dd];
+      int64_t th = tlo[dd] + t * s - 1;
+      c.thi[dd] = (int32_t)(thi[dd] > th ? thi[dd] : th);
+      c.ctx[dd] = (int32_t)t; c.base[dd] = c.rlo[dd]; c.coeff[dd] = s; c.ext[dd] = s;
+      nt *= t; sp *= s;
+    }
+    c.kind = K_BLOCK; c.tier = T_SHARED; c.kernel = cg0.kernel; c.realizations = K.n_blocks;
+    c.n_threads = (int32_t)nt; c.unrolled = sp < 16; c.has_serial = 1; c.serial_prod = (int32_t)sp;
+    __syncwarp();
+    if (lane == 0) k.cf[f] = c;
+  } else {
+    int64_t pe = 1;
+#pragma unroll
+    for (int dd = 0; dd < ND; ++dd) {
+      c.rlo[dd] = (int32_t)lo[dd]; c.rhi[dd] = (int32_t)hi[dd];
+      c.tlo[dd] = (int32_t)tlo[dd]; c.thi[dd] = (int32_t)thi[dd];
+      c.ctx[dd] = cg0.ctx[dd]; c.base[dd] = c.rlo[dd];
+      c.coeff[dd] = (int32_t)(cg0.coeff[dd] * ts0[dd]);
+      c.ext[dd] = (int32_t)(hi[dd] - lo[dd] + 1);
+      pe *= c.ext[dd];
+    }
+    c.kind = K_THREAD; c.tier = T_REGISTER; c.kernel = cg0.kernel;
+    c.realizations = K.n_blocks * (int64_t)cg0.n_threads; c.n_threads = cg0.n_threads;
+    c.unrolled = pe < 16; c.has_serial = 0; c.serial_prod = 1;
+    __syncwarp();
+    if (lane == 0) k.cf[f] = c;
+  }
   __syncwarp();
+  return true;
 }
 
-// warp 0: decision validation + structure (if changed) + geometry
+// externals and unscheduled producers (resolve.py:396-425); one lane
+template <int ND>
+__device__ void external_one(K1<ND>& k, int f) {
+  const GsFunc& fn = k.F[f];
+  int64_t lo[ND], hi[ND];
+#pragma unroll
+  for (int dd = 0; dd < ND; ++dd) { lo[dd] = INT64_MAX; hi[dd] = INT64_MIN; }
+  const int sb = k.srcb[f], se = k.srcb[f + 1];
+  for (int q = sb; q < se; ++q) {
+    const RRead& r = k.rd[k.srcl[q]];
+    const CF<ND>& cg = k.cf[r.root];
+#pragma unroll
+    for (int dd = 0; dd < ND; ++dd) {
+      int64_t a = cg.tlo[dd], b = cg.thi[dd];
+      chain_iv(k.A, k.path + r.pbeg, r.plen, dd, a, b);
+      lo[dd] = a < lo[dd] ? a : lo[dd]; hi[dd] = b > hi[dd] ? b : hi[dd];
+    }
+  }
+  CF<ND> c;
+  zero_cf(c);
+  c.kind = K_EXTERNAL; c.tier = T_GLOBAL; c.kernel = -1; c.consumer = -1; c.n_threads = 1; c.serial_prod = 1;
+#pragma unroll
+  for (int dd = 0; dd < ND; ++dd) {
+    int e = dd < fn.ndim ? fn.extent[dd] : 1;
+    c.rlo[dd] = se > sb ? (int32_t)lo[dd] : 0; c.rhi[dd] = se > sb ? (int32_t)hi[dd] : e - 1;
+    c.tlo[dd] = c.rlo[dd]; c.thi[dd] = c.rhi[dd];
+    c.ctx[dd] = 1; c.ext[dd] = 1;
+  }
+  k.cf[f] = c;
+}
+
+// kernel aggregates of a root (resolve.py:325-333): one lane
+template <int ND>
+__device__ void kernel_aggregates(K1<ND>& k, int kf) {
+  CF<ND>& o = k.cf[kf];
+  int32_t kt = o.n_threads;
+  int64_t sh = 0;
+  for (int q = k.kmb[kf]; q < k.kmb[kf + 1]; ++q) {
+    const int f = k.kml[q];
+    const CF<ND>& c = k.cf[f];
+    if (c.n_threads > kt) kt = c.n_threads;
+    if (c.kind == K_BLOCK) sh += alloc_of(c) * k.F[f].elem_bytes;
+  }
+  o.k_threads = kt;
+  o.k_shared = sh;
+}
+
+// inline call totals / primary consumer (resolve.py:337-349); one lane.
+// icall entries of f are visited in icall order, so the first maximum wins
+// exactly as in the sequential pass over all entries.
+template <int ND>
+__device__ void inline_one(K1<ND>& k, int f) {
+  CF<ND>& ic = k.cf[f];
+  zero_cf(ic);
+  ic.kind = K_INLINE; ic.consumer = -1;
+  for (int q = k.icb[f]; q < k.icb[f + 1]; ++q) {
+    const ICall& x = k.icall[k.icl[q]];
+    const CF<ND>& c = k.cf[x.root];
+    const int64_t calls = x.vol * prod_ext(c) * c.n_threads * k.cf[c.kernel].n_blocks;
+    ic.calls += calls;
+    if (calls > ic.best) { ic.best = calls; ic.consumer = x.root; }
+  }
+  const int prim = ic.consumer;
+  ic.tier = T_NONE; ic.serial_prod = 1;
+  if (prim >= 0) {
+    const CF<ND>& h = k.cf[prim];
+    ic.kernel = h.kernel; ic.n_threads = h.n_threads; ic.unrolled = h.unrolled;
+    for (int dd = 0; dd < ND; ++dd) ic.ctx[dd] = h.ctx[dd];
+  } else {
+    ic.kernel = -1; ic.n_threads = 1; ic.unrolled = 1;
+    for (int dd = 0; dd < ND; ++dd) ic.ctx[dd] = 1;
+  }
+  for (int dd = 0; dd < ND; ++dd) { ic.rhi[dd] = -1; ic.thi[dd] = -1; ic.ext[dd] = 1; }
+}
+
+// warp 0: decision validation + structure (if changed) + geometry.
+//
+// Siblings (same decision structure as the previous candidate of this CTA)
+// re-resolve only the funcs whose dependency mask dm[f] meets the set of
+// decision records that changed; every other func's record is the previous
+// candidate's, which is what a full resolve would recompute bit for bit
+// (geometry is a pure function of those records).  k.dirty[f] ends up 1 iff
+// f's record may differ from the previous candidate's (rows use it).
 template <int ND>
 __device__ void resolve(K1<ND>& k) {
   const int lane = lane_id();
   Misc& m = *k.misc;
   const int nf = k.P->nf;
-  if (!m.same_struct) {
+  const bool diff = m.same_struct;            // k.cf holds the previous candidate's geometry
+  const bool incr = diff && k.mw > 0;
+  if (!diff) {
     for (int f = lane; f < nf; f += 32) k.didx[f] = -1;
     __syncwarp();
     if (lane == 0) {
@@ -481,47 +584,106 @@ __device__ void resolve(K1<ND>& k) {
     __syncwarp();
     if (m.err) return;
   }
-  resolve_geometry(k);
+  if (incr) {
+    for (int f = lane; f < nf; f += 32) {
+      bool t = false;
+      for (int w = 0; w < k.mw; ++w) t |= (k.dm[f * k.mw + w] & k.cmask[w]) != 0u;
+      k.gdirty[f] = t;
+      k.kdirty[f] = 0;
+    }
+    __syncwarp();
+    for (int f = lane; f < nf; f += 32)
+      if (k.gdirty[f] && k.kern[f] >= 0) k.kdirty[k.kern[f]] = 1;
+  } else {
+    for (int f = lane; f < nf; f += 32) { k.gdirty[f] = 1; k.kdirty[f] = 1; }
+  }
+  __syncwarp();
+  if (diff)   // keep the records about to be rewritten, for the change test
+    for (int f = lane; f < nf; f += 32)
+      if (k.gdirty[f] || k.kdirty[f]) k.pcf[f] = k.cf[f];
+  // decisions to re-resolve, in decision order
+  int cnt = 0;
+  for (int i0 = 0; i0 < m.ndec; i0 += 32) {
+    const int i = i0 + lane;
+    const bool t = i < m.ndec && k.dec[i].kind != GS_INLINE && k.gdirty[k.dec[i].func];
+    const unsigned b = __ballot_sync(0xffffffffu, t);
+    if (t) k.dlist[cnt + __popc(b & ((1u << lane) - 1))] = (int16_t)i;
+    cnt += __popc(b);
+  }
+  __syncwarp();
+  if (lane == 0) k.misc->ngeo = cnt;
+  for (int q = 0; q < cnt; ++q)
+    if (!geometry_one(k, k.dlist[q])) return;
+  for (int f = lane; f < nf; f += 32)
+    if ((k.F[f].is_external || k.didx[f] < 0) && k.gdirty[f]) external_one(k, f);
+  __syncwarp();
+  for (int f = lane; f < nf; f += 32)
+    if (k.kdirty[f] && k.didx[f] >= 0 && k.dec[k.didx[f]].kind == GS_ROOT) kernel_aggregates(k, f);
+  __syncwarp();
+  for (int f = lane; f < nf; f += 32)
+    if (k.gdirty[f] && k.didx[f] >= 0 && k.dec[k.didx[f]].kind == GS_INLINE) inline_one(k, f);
+  __syncwarp();
+  constexpr int WPF = (int)(sizeof(CF<ND>) / 4);
+  for (int f = lane; f < nf; f += 32) {
+    bool d = true;
+    if (diff) {
+      d = false;
+      if (k.gdirty[f] || k.kdirty[f]) {
+        const int32_t* a = reinterpret_cast<const int32_t*>(&k.cf[f]);
+        const int32_t* b = reinterpret_cast<const int32_t*>(&k.pcf[f]);
+        for (int w = 0; w < WPF; ++w) d |= a[w] != b[w];
+      }
+    }
+    k.dirty[f] = d;
+  }
+  __syncwarp();
 }
 
-// prune verdict (options.py:200-255, machine.py:91-105); lane 0
+// prune verdict (options.py:200-255, machine.py:91-105), warp-wide: the
+// rules are checked in the reference order (recompute, idle SMs, then per
+// func in decision order warp utilization / serial / thread allocation,
+// then hardware limits); sums are exact integers, so lane order is free.
 template <int ND>
 __device__ int prune_verdict(const K1<ND>& k) {
+  const int lane = lane_id();
   const Misc& m = *k.misc;
   const GsMachine& M = k.P->m;
   const GsThresholds& th = k.P->th;
-  int64_t ci = 0, ni = 0;
-  for (int i = 0; i < m.ndec; ++i) {   // non-external scheduled funcs
-    const GsDecision& d = k.dec[i];
-    const GsFunc& fn = k.F[d.func];
-    int64_t dom = 1;
-    for (int dd = 0; dd < fn.ndim; ++dd) dom *= fn.extent[dd];
-    ni += dom;
-    const CF<ND>& c = k.cf[d.func];
-    if (d.kind == GS_INLINE) ci += c.calls;
-    else ci += prod_ext(c) * c.n_threads * k.cf[c.kernel].n_blocks;
-  }
-  if (ni && (double)ci > th.recompute_factor * (double)ni) return GS_PRUNE_RECOMPUTE;
   const double minb = th.min_blocks_per_sm_factor * (double)M.num_sms;
-  for (int i = 0; i < m.ndec; ++i)
-    if (k.dec[i].kind == GS_ROOT && (double)k.cf[k.dec[i].func].n_blocks < minb) return GS_PRUNE_IDLE_SMS;
-  for (int i = 0; i < m.ndec; ++i) {
-    const GsDecision& d = k.dec[i];
-    if (d.kind == GS_INLINE) continue;
-    const CF<ND>& c = k.cf[d.func];
-    int64_t w = (c.n_threads + M.warp_size - 1) / M.warp_size;
-    double util = (double)c.n_threads / (double)(w * M.warp_size);
-    if (util < th.warp_utilization_floor) return GS_PRUNE_WARP_UTIL;
-    if (c.has_serial && (int64_t)c.serial_prod > th.unroll_budget) return GS_PRUNE_SERIAL;
-    if (c.kind == K_THREAD && alloc_of(c) * k.F[d.func].elem_bytes > th.thread_alloc_bytes)
-      return GS_PRUNE_THREAD_ALLOC;
+  int64_t ci = 0;
+  bool r2 = false, r6 = false;
+  int first = 0;
+  for (int i0 = 0; i0 < m.ndec; i0 += 32) {
+    const int i = i0 + lane;
+    int code = 0;
+    if (i < m.ndec) {
+      const GsDecision& d = k.dec[i];
+      const CF<ND>& c = k.cf[d.func];
+      if (d.kind == GS_INLINE) ci += c.calls;
+      else {
+        ci += prod_ext(c) * c.n_threads * k.cf[c.kernel].n_blocks;
+        const int64_t w = (c.n_threads + M.warp_size - 1) / M.warp_size;
+        const double util = (double)c.n_threads / (double)(w * M.warp_size);
+        if (util < th.warp_utilization_floor) code = GS_PRUNE_WARP_UTIL;
+        else if (c.has_serial && (int64_t)c.serial_prod > th.unroll_budget) code = GS_PRUNE_SERIAL;
+        else if (c.kind == K_THREAD && alloc_of(c) * k.F[d.func].elem_bytes > th.thread_alloc_bytes)
+          code = GS_PRUNE_THREAD_ALLOC;
+      }
+      if (d.kind == GS_ROOT) {
+        if ((double)c.n_blocks < minb) r2 = true;
+        if (c.k_threads > M.max_threads_per_block || c.k_shared > M.shared_mem_per_block_limit) r6 = true;
+      }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, code != 0);
+    if (b && !first) first = __shfl_sync(0xffffffffu, code, __ffs(b) - 1);
   }
-  for (int i = 0; i < m.ndec; ++i) {
-    if (k.dec[i].kind != GS_ROOT) continue;
-    const CF<ND>& c = k.cf[k.dec[i].func];
-    if (c.k_threads > M.max_threads_per_block || c.k_shared > M.shared_mem_per_block_limit)
-      return GS_PRUNE_HW_LIMIT;
-  }
+  for (int o = 16; o; o >>= 1) ci += __shfl_xor_sync(0xffffffffu, ci, o);
+  r2 = __any_sync(0xffffffffu, r2);
+  r6 = __any_sync(0xffffffffu, r6);
+  if (m.ni && (double)ci > th.recompute_factor * (double)m.ni) return GS_PRUNE_RECOMPUTE;
+  if (r2) return GS_PRUNE_IDLE_SMS;
+  if (first) return first;
+  if (r6) return GS_PRUNE_HW_LIMIT;
   return GS_VALID;
 }
 
@@ -683,19 +845,85 @@ __device__ void union_count(const GsAccess* A, const RRead* rd, const int16_t* p
 // ---------------------------------------------------------------------------
 // warp-instruction transaction counts (featurize.py:173-196, 508-571)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long count_in(int64_t a, int64_t b, int r, int M) {
+// Residue arithmetic modulo the transaction / bank period M: shifts and
+// masks when M is a power of two (every real machine), divisions otherwise.
+struct ModM {
+  int M, lg;
+  __device__ explicit ModM(int m) : M(m), lg(-1) {
+    if (m > 0 && (m & (m - 1)) == 0) { lg = 0; while ((1 << lg) < m) ++lg; }
+  }
+  __device__ __forceinline__ int64_t fdiv(int64_t a) const { return lg >= 0 ? (a >> lg) : floordiv(a, M); }
+  __device__ __forceinline__ int pmod(int64_t a) const {
+    return lg >= 0 ? (int)(a & (int64_t)(M - 1)) : (int)posmod(a, M);
+  }
   // #{x in [a,b] : x = r (mod M)}
-  if (b < a) return 0;
-  return (unsigned long long)(floordiv(b - r, M) - floordiv(a - 1 - r, M));
+  __device__ __forceinline__ unsigned long long count_in(int64_t a, int64_t b, int r) const {
+    if (b < a) return 0;
+    return (unsigned long long)(fdiv(b - r) - fdiv(a - 1 - r));
+  }
+};
+
+// lane origins (byte address of the instruction constant 0) of emulated warp w
+template <int ND>
+__device__ __forceinline__ int64_t warp_origin(const CF<ND>& h, const int64_t* ts, const int64_t* bs, int64_t cst,
+                                               int w, int lane, bool& active) {
+  int t = w * 32 + lane;
+  active = t < h.n_threads;
+  int64_t org = cst;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    const int cd = t % h.ctx[d];
+    t /= h.ctx[d];
+    org += (int64_t)cd * h.coeff[d] * ts[d] * bs[d];
+  }
+  return org;
 }
 
-// all lanes: H[k] for k = lane + 32j, j < M/32
+// transactions of one emulated warp for ONE instruction constant r
+// (featurize.py:173-196): global = distinct segments; shared = max over
+// banks of distinct words; warp-collective, lanes agree on the result
+__device__ __forceinline__ unsigned warp_count(unsigned long long a, bool active, int tier, const ModM& mg, int bw_lg,
+                                               int bw, int banks) {
+  const int lane = lane_id();
+  if (tier == T_GLOBAL) {
+    unsigned long long seg = mg.lg >= 0 ? (a >> mg.lg) : a / (unsigned long long)mg.M;
+    if (!active) seg = ~0ull - lane;
+    const unsigned lm = __match_any_sync(0xffffffffu, seg);
+    const bool lead = active && (__ffs(lm) - 1 == lane);
+    return __popc(__ballot_sync(0xffffffffu, lead));
+  }
+  unsigned long long word = bw_lg >= 0 ? (a >> bw_lg) : a / (unsigned long long)bw;
+  unsigned bank = (unsigned)(word % (unsigned long long)banks);
+  if (!active) { word = ~0ull - lane; bank = 0x80000000u + lane; }
+  const unsigned lm = __match_any_sync(0xffffffffu, word);
+  const bool lead = active && (__ffs(lm) - 1 == lane);
+  const unsigned leaders = __ballot_sync(0xffffffffu, lead);
+  const unsigned bm = __match_any_sync(0xffffffffu, bank);
+  const unsigned per_bank = active ? __popc(bm & leaders) : 0u;
+  return __reduce_max_sync(0xffffffffu, per_bank);
+}
+
+// Warp transactions of all load (or store) instructions of one read in
+// block 0 (featurize.py:508-571).  All lanes; returns the total.
+//
+// 1. T[k], k < M: how many emitted instructions have address constant = k
+//    (mod M), by cyclic convolution of per-dim histograms (the count of a
+//    warp instruction depends on its constant only mod M: shifting every
+//    lane by M shifts every segment / keeps every bank).
+// 2. Emulated warps whose lane-origin pattern equals another's up to a
+//    constant shift d are one "class": their counts are the class
+//    representative's at residue k + d, so the representative is evaluated
+//    once per residue against the shifted histograms of all its members.
+//    For shared memory the count depends on the residue only mod the bank
+//    width (adding whole words rotates the banks), so at most bank-width
+//    evaluations are needed per class.
 template <int ND>
 __device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, int plen, bool identity,
                                       const CF<ND>& h, const CF<ND>& prod, int eb, int tier,
                                       const GsMachine& Mc, WarpScr& W, int& err) {
   const int lane = lane_id();
   const int M = tier == T_GLOBAL ? Mc.global_transaction_bytes : Mc.shared_banks * Mc.bank_width_bytes;
+  const ModM mm(M);
   const int per = (M + 31) / 32;
   int64_t bs[ND], ts[ND];
   {
@@ -715,7 +943,7 @@ __device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, in
     const int e = h.ext[d];
     // per-dim histogram of relative coordinates (mod M) into H
     if (identity || !h.unrolled) {
-      for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.H[r] = count_in(0, e - 1, r, M); }
+      for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.H[r] = mm.count_in(0, e - 1, r); }
       __syncwarp();
       if (!identity) {
         for (int q = 0; q < plen; ++q) {
@@ -724,16 +952,27 @@ __device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, in
           // S[k] = sum_r H[r] * #{w in [wl,wh] : r*s + w = k (mod M)}
           for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.S[r] = 0; }
           __syncwarp();
-          for (int c = 0; c < per; ++c) {
-            unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < M && W.H[c * 32 + lane] != 0);
-            while (nz) {
-              int b = __ffs(nz) - 1; nz &= nz - 1;
-              int r = c * 32 + b;
-              unsigned long long hv = W.H[r];
-              int64_t sh = posmod((int64_t)r * s, M);
-              for (int j = 0; j < per; ++j) {
-                int k = lane + 32 * j;
-                if (k < M) W.S[k] += hv * count_in(wl, wh, (int)posmod(k - sh, M), M);
+          if (wh - wl + 1 < M) {       // short window: scatter each residue's taps
+            for (int j = 0; j < per; ++j) {
+              const int r = lane + 32 * j;
+              if (r >= M) continue;
+              const unsigned long long hv = W.H[r];
+              if (!hv) continue;
+              const int64_t base = (int64_t)r * s;
+              for (int64_t w = wl; w <= wh; ++w) atomicAdd(&W.S[mm.pmod(base + w)], hv);
+            }
+          } else {
+            for (int c = 0; c < per; ++c) {
+              unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < M && W.H[c * 32 + lane] != 0);
+              while (nz) {
+                const int b = __ffs(nz) - 1; nz &= nz - 1;
+                const int r = c * 32 + b;
+                const unsigned long long hv = W.H[r];
+                const int64_t sh = mm.pmod((int64_t)r * s);
+                for (int j = 0; j < per; ++j) {
+                  const int k = lane + 32 * j;
+                  if (k < M) W.S[k] += hv * mm.count_in(wl, wh, mm.pmod(k - sh));
+                }
               }
             }
           }
@@ -750,85 +989,123 @@ __device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, in
         int r = lane + 32 * j;
         if (r >= M) continue;
         unsigned long long c = 0;
-        for (int i = 0; i < n; ++i) c += count_in(buf[i].lo, buf[i].hi, r, M);
+        for (int i = 0; i < n; ++i) c += mm.count_in(buf[i].lo, buf[i].hi, r);
         W.H[r] = c;
       }
       __syncwarp();
     }
     // scale by the byte stride of dim d, then convolve into T
-    const int64_t bm = posmod(bs[d], M);
+    const int64_t bm = mm.pmod(bs[d]);
     for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.S[r] = 0; }
     __syncwarp();
     for (int j = 0; j < per; ++j) {
       int r = lane + 32 * j;
-      if (r < M && W.H[r]) atomicAdd(&W.S[(int)posmod((int64_t)r * bm, M)], W.H[r]);
+      if (r < M && W.H[r]) atomicAdd(&W.S[mm.pmod((int64_t)r * bm)], W.H[r]);
+    }
+    // nonzero residues of T, then H[k] = sum_r T[r] S[k - r] (lane per k)
+    int nnz = 0;
+    for (int c = 0; c < per; ++c) {
+      const int r = c * 32 + lane;
+      const bool t = r < M && W.T[r] != 0;
+      const unsigned b = __ballot_sync(0xffffffffu, t);
+      if (t) W.nz[nnz + __popc(b & ((1u << lane) - 1))] = (int16_t)r;
+      nnz += __popc(b);
     }
     __syncwarp();
-    for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.H[r] = 0; }
-    __syncwarp();
-    for (int c = 0; c < per; ++c) {
-      unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < M && W.T[c * 32 + lane] != 0);
-      while (nz) {
-        int b = __ffs(nz) - 1; nz &= nz - 1;
-        int r = c * 32 + b;
-        unsigned long long tv = W.T[r];
-        for (int j = 0; j < per; ++j) {
-          int k = lane + 32 * j;
-          if (k < M) W.H[k] += tv * W.S[(int)posmod(k - r, M)];
-        }
+    for (int j = 0; j < per; ++j) {
+      const int k = lane + 32 * j;
+      if (k >= M) continue;
+      unsigned long long acc = 0;
+      for (int i = 0; i < nnz; ++i) {
+        const int r = W.nz[i];
+        acc += W.T[r] * W.S[mm.pmod(k - r)];
       }
+      W.H[k] = acc;
     }
     __syncwarp();
     for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.T[r] = W.H[r]; }
     __syncwarp();
   }
-  // count each distinct residue once per emulated warp of block 0
-  const int n_threads = h.n_threads;
-  const int nwarps = (n_threads + 31) / 32;
+
+  // ---- count: warp-pattern classes ---------------------------------------
+  const int nwarps = (h.n_threads + 31) / 32;
   int64_t cst = kAddrBias;
 #pragma unroll
   for (int d = 0; d < ND; ++d) cst += ((int64_t)h.base[d] * ts[d] - prod.rlo[d]) * bs[d];
-  const bool gpow2 = (Mc.global_transaction_bytes & (Mc.global_transaction_bytes - 1)) == 0;
+  const int bw = Mc.bank_width_bytes, banks = Mc.shared_banks;
+  const int bw_lg = (bw & (bw - 1)) == 0 ? __ffs(bw) - 1 : -1;
+  // residues that matter per class: all M (global), M mod bank width (shared)
+  const bool fold = tier != T_GLOBAL && bw_lg >= 0 && bw <= 32 && (M % bw) == 0;
+  const int P = fold ? bw : M;                 // class weight vector length
+  const int pp = (P + 31) / 32;
+  // TB[e] = sum of T[r] over r = e (mod P): lane e (fold) holds it
+  unsigned long long tb = 0;
+  if (fold) {
+    for (int j = 0; j < per; ++j) {
+      const int r = lane + 32 * j;
+      const unsigned long long v = r < M ? W.T[r] : 0ull;
+      // lanes with the same residue mod bw add up (bw divides 32)
+      unsigned long long sum = v;
+      for (int o = bw; o < 32; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      tb += sum;
+    }
+  }
+  // two classes: weights in H (class 0) and S (class 1); registers are
+  // named, not indexed, so they stay out of local memory
+  for (int j = 0; j < pp; ++j) { int r = lane + 32 * j; if (r < P) { W.H[r] = 0; W.S[r] = 0; } }
+  __syncwarp();
+  int ncls = 0;
+  int64_t rel0 = 0, rel1 = 0, o00 = 0, o01 = 0;
+  unsigned am0 = 0u, am1 = 0u;
   unsigned long long total = 0;
   for (int w = 0; w < nwarps; ++w) {
-    int t = w * 32 + lane;
-    const bool active = t < n_threads;
-    int64_t org = cst;
-#pragma unroll
-    for (int d = 0; d < ND; ++d) {
-      int cd = t % h.ctx[d];
-      t /= h.ctx[d];
-      org += (int64_t)cd * h.coeff[d] * ts[d] * bs[d];
-    }
+    bool active;
+    const int64_t org = warp_origin(h, ts, bs, cst, w, lane, active);
     const unsigned amask = __ballot_sync(0xffffffffu, active);
+    const int64_t ow = __shfl_sync(0xffffffffu, org, 0);
+    const int64_t rw = org - ow;
+    int cls = -1;
+    if (ncls > 0 && amask == am0 && __all_sync(0xffffffffu, !active || rw == rel0)) cls = 0;
+    else if (ncls > 1 && amask == am1 && __all_sync(0xffffffffu, !active || rw == rel1)) cls = 1;
+    else if (ncls == 0) { cls = 0; ncls = 1; rel0 = rw; am0 = amask; o00 = ow; }
+    else if (ncls == 1) { cls = 1; ncls = 2; rel1 = rw; am1 = amask; o01 = ow; }
+    if (cls >= 0) {
+      const int64_t dlt = ow - (cls ? o01 : o00);
+      unsigned long long* wv = cls ? W.S : W.H;
+      if (fold) {
+        const int src = (int)((lane - dlt) & (int64_t)(bw - 1));
+        const unsigned long long add = __shfl_sync(0xffffffffu, tb, src);
+        if (lane < bw) wv[lane] += add;
+      } else {
+        for (int j = 0; j < per; ++j) {
+          const int k = lane + 32 * j;
+          if (k < M) wv[k] += W.T[mm.pmod(k - dlt)];
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    // a third lane pattern: evaluate this warp directly
     for (int c = 0; c < per; ++c) {
       unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < M && W.T[c * 32 + lane] != 0);
       while (nz) {
-        int b = __ffs(nz) - 1; nz &= nz - 1;
-        int r = c * 32 + b;
-        const unsigned long long mult = W.T[r];
-        const unsigned long long a = (unsigned long long)(org + r);
-        unsigned cnt;
-        if (tier == T_GLOBAL) {
-          unsigned long long seg = gpow2 ? (a >> (__ffs(Mc.global_transaction_bytes) - 1))
-                                         : a / (unsigned long long)Mc.global_transaction_bytes;
-          if (!active) seg = ~0ull - lane;
-          unsigned lm = __match_any_sync(0xffffffffu, seg);
-          bool lead = active && (__ffs(lm) - 1 == lane);
-          cnt = __popc(__ballot_sync(0xffffffffu, lead));
-        } else {
-          unsigned long long word = a / (unsigned long long)Mc.bank_width_bytes;
-          unsigned bank = (unsigned)(word % (unsigned long long)Mc.shared_banks);
-          if (!active) { word = ~0ull - lane; bank = 0x80000000u + lane; }
-          unsigned lm = __match_any_sync(0xffffffffu, word);
-          bool lead = active && (__ffs(lm) - 1 == lane);
-          unsigned leaders = __ballot_sync(0xffffffffu, lead);
-          unsigned bm = __match_any_sync(0xffffffffu, bank);
-          unsigned per_bank = active ? __popc(bm & leaders) : 0u;
-          cnt = __reduce_max_sync(0xffffffffu, per_bank);
-        }
-        (void)amask;
-        total += mult * cnt;
+        const int b = __ffs(nz) - 1; nz &= nz - 1;
+        const int r = c * 32 + b;
+        total += W.T[r] * warp_count((unsigned long long)(org + r), active, tier, mm, bw_lg, bw, banks);
+      }
+    }
+  }
+  __syncwarp();
+  for (int j = 0; j < ncls; ++j) {
+    const bool active = ((j ? am1 : am0) >> lane) & 1u;
+    const int64_t org = j ? o01 + rel1 : o00 + rel0;
+    const unsigned long long* wv = j ? W.S : W.H;
+    for (int c = 0; c < pp; ++c) {
+      unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < P && wv[c * 32 + lane] != 0);
+      while (nz) {
+        const int b = __ffs(nz) - 1; nz &= nz - 1;
+        const int r = c * 32 + b;
+        total += wv[r] * warp_count((unsigned long long)(org + r), active, tier, mm, bw_lg, bw, banks);
       }
     }
   }
@@ -1084,7 +1361,7 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
                                                         const GsDecision* __restrict__ dec, int64_t n, int S,
                                                         double* __restrict__ feats, int32_t* __restrict__ row_key,
                                                         int32_t* __restrict__ n_rows, uint8_t* __restrict__ verdict,
-                                                        Layout L, int* gerr, int reuse) {
+                                                        int32_t* __restrict__ row_src, Layout L, int* gerr, int reuse) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar;
   const int warp = threadIdx.x >> 5, lane = lane_id(), nw = blockDim.x >> 5;
@@ -1114,17 +1391,29 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
   k.rdep = reinterpret_cast<int16_t*>(sm + L.rdep);
   k.dirty = reinterpret_cast<uint8_t*>(sm + L.dirty);
   k.rowlist = reinterpret_cast<int16_t*>(sm + L.rowlist);
+  k.kern = reinterpret_cast<int16_t*>(sm + L.kern);
+  k.dm = reinterpret_cast<uint32_t*>(sm + L.dm);
+  k.cmask = reinterpret_cast<uint32_t*>(sm + L.cmask);
+  k.kmb = reinterpret_cast<int32_t*>(sm + L.kmb);
+  k.kml = reinterpret_cast<int16_t*>(sm + L.kml);
+  k.icb = reinterpret_cast<int32_t*>(sm + L.icb);
+  k.icl = reinterpret_cast<int16_t*>(sm + L.icl);
+  k.dlist = reinterpret_cast<int16_t*>(sm + L.dlist);
+  k.gdirty = reinterpret_cast<uint8_t*>(sm + L.gdirty);
+  k.kdirty = reinterpret_cast<uint8_t*>(sm + L.kdirty);
   k.misc = reinterpret_cast<Misc*>(sm + L.misc);
-  k.rcap = L.rcap; k.pcap = L.pcap; k.gerr = gerr;
+  k.rcap = L.rcap; k.pcap = L.pcap; k.gerr = gerr; k.mw = L.mw;
   WarpScr& W = *reinterpret_cast<WarpScr*>(sm + L.warps + warp * L.warp_bytes);
   uint8_t* rflag = reinterpret_cast<uint8_t*>(sm + L.rflag);
-  const int nf = P->nf;
+  int32_t* rsrc = reinterpret_cast<int32_t*>(sm + L.rsrc);
   // contiguous candidate range per CTA: consecutive candidates of a beam
-  // step are siblings, which is what the geometry diff below exploits
+  // step are siblings, which is what the incremental resolve and the row
+  // reuse below exploit
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t c0 = (int64_t)blockIdx.x * per;
   const int64_t c1 = c0 + per < n ? c0 + per : n;
   if (threadIdx.x == 0) { k.misc->prev_valid = 0; k.misc->same_struct = 0; k.misc->ndec = 0; }
+  unsigned long long st_inc = 0, st_rows = 0, st_emit = 0, st_geo = 0;   // work counters (thread 0)
   bulk_wait(&bar);
   __syncthreads();
   for (int64_t c = c0; c < c1; ++c) {
@@ -1132,6 +1421,7 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
       const uint4* src = reinterpret_cast<const uint4*>(dec + c * S);
       uint4* dst = reinterpret_cast<uint4*>(k.dec);
       for (int i = lane; i < S; i += 32) dst[i] = __ldg(src + i);   // 128-bit loads
+      if (lane < k.mw) k.cmask[lane] = 0u;
       __syncwarp();
       unsigned cnt = 0, diff = 0;
       for (int i0 = 0; i0 < S; i0 += 32) {
@@ -1143,6 +1433,12 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
           const GsDecision& a = k.dec[i];
           const GsDecision& b = k.pdec[i];
           d = a.func != b.func || a.consumer != b.consumer || a.kind != b.kind;
+          if (live && k.mw > 0 && !d) {   // same structure here: did the tiling change?
+            const uint4 x = reinterpret_cast<const uint4*>(k.dec)[i];
+            const uint4 y = reinterpret_cast<const uint4*>(k.pdec)[i];
+            if (x.x != y.x || x.y != y.y || x.z != y.z || x.w != y.w)
+              atomicOr(&k.cmask[a.func >> 5], 1u << (a.func & 31));
+          }
         }
         diff |= __ballot_sync(0xffffffffu, d);
       }
@@ -1154,9 +1450,9 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
       }
       __syncwarp();
       resolve<ND>(k);
+      const int v = k.misc->err ? 255 : prune_verdict<ND>(k);
       if (lane == 0) {
         Misc& m = *k.misc;
-        int v = m.err ? 255 : prune_verdict<ND>(k);
         if (m.err) { atomicOr(gerr, m.err); m.nrows = 0; }
         verdict[c] = (uint8_t)v;
         n_rows[c] = m.nrows;
@@ -1166,19 +1462,6 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
     const Misc& m = *k.misc;
     const int nr = feats ? m.nrows : 0;   // feats == NULL: prune verdict only
     const bool diffable = m.same_struct && !m.err;
-    // which funcs' geometry changed since the previous candidate
-    if (diffable) {
-      constexpr int WPF = (int)(sizeof(CF<ND>) / 4);
-      for (int f = threadIdx.x; f < nf; f += blockDim.x) {
-        const int32_t* a = reinterpret_cast<const int32_t*>(&k.cf[f]);
-        const int32_t* b = reinterpret_cast<const int32_t*>(&k.pcf[f]);
-        bool d = false;
-#pragma unroll 4
-        for (int w = 0; w < WPF; ++w) d |= a[w] != b[w];
-        k.dirty[f] = d;
-      }
-    }
-    __syncthreads();
     // rows to recompute: own func, host, host kernel, read producers and
     // fuse_at_thread children unchanged => features are bit-identical
     for (int r = threadIdx.x; r < nr; r += blockDim.x) {
@@ -1192,6 +1475,7 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
         for (int q = k.rdepb[r]; q < k.rdepb[r + 1] && !d; ++q) d |= k.dirty[k.rdep[q]];
       }
       rflag[r] = d;
+      if (d) rsrc[r] = (int32_t)c;
     }
     __syncthreads();
     if (warp == 0) {   // compact the dirty rows
@@ -1207,6 +1491,7 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
     }
     __syncthreads();
     const int nd = k.misc->ndirty;
+    if (threadIdx.x == 0) { st_inc += m.same_struct; st_rows += nd; st_emit += nr; st_geo += m.ngeo; }
     for (int q = warp; q < nd; q += nw) {
       const int r = k.rowlist[q];
       const int key = k.rows[r];
@@ -1215,7 +1500,10 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
     }
     // clean rows: copy the previous candidate's (same CTA, already visible)
     for (int r = warp; r < nr; r += nw) {
-      if (lane == 0) row_key[c * L.R + r] = k.rows[r];
+      if (lane == 0) {
+        row_key[c * L.R + r] = k.rows[r];
+        if (row_src) row_src[c * L.R + r] = rsrc[r];
+      }
       if (rflag[r]) continue;
       const double* src = feats + ((int64_t)(c - 1) * L.R + r) * GS_NUM_FEATURES;
       double* dst = feats + ((int64_t)c * L.R + r) * GS_NUM_FEATURES;
@@ -1223,11 +1511,13 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
     }
     __syncthreads();
     { GsDecision* t = k.dec; k.dec = k.pdec; k.pdec = t; }
-    { CF<ND>* t = k.cf; k.cf = k.pcf; k.pcf = t; }
     if (threadIdx.x == 0) k.misc->prev_valid = (k.misc->err == 0) && feats != nullptr;
-    // the new "current" CF buffer must not be diffed before it is rewritten:
-    // resolve() rewrites every func's record for a same-structure candidate
     __syncthreads();
+  }
+  if (threadIdx.x == 0 && c1 > c0) {
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(gerr + 2);
+    atomicAdd(ctr + 0, (unsigned long long)(c1 - c0));
+    atomicAdd(ctr + 1, st_inc); atomicAdd(ctr + 2, st_rows); atomicAdd(ctr + 3, st_emit); atomicAdd(ctr + 4, st_geo);
   }
 }
 
@@ -1268,6 +1558,18 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   L.dirty = o; o += al(nf);
   L.rflag = o; o += al(R);
   L.rowlist = o; o += al(R * 2);
+  L.rsrc = o; o += al(R * 4);
+  L.mw = nf <= 32 * kMaxMaskWords ? (nf + 31) / 32 : 0;
+  L.kern = o; o += al(nf * 2);
+  L.dm = o; o += al(nf * L.mw * 4);
+  L.cmask = o; o += al(kMaxMaskWords * 4);
+  L.kmb = o; o += al((nf + 1) * 4);
+  L.kml = o; o += al(nf * 2);
+  L.icb = o; o += al((nf + 1) * 4);
+  L.icl = o; o += al(pcap * 2);
+  L.dlist = o; o += al(nf * 2);
+  L.gdirty = o; o += al(nf);
+  L.kdirty = o; o += al(nf);
   L.misc = o; o += al((int)sizeof(Misc));
   L.warp_bytes = al((int)sizeof(WarpScr));
   L.warps = o; o += nwarps * L.warp_bytes;
@@ -1277,14 +1579,15 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
 }
 
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
-                     double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, const Layout& L,
+                     double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
+                     const Layout& L,
                      int nwarps, int grid, int* gerr, int reuse, cudaStream_t st) {
   dim3 b(nwarps * 32);
   switch (nd) {
 #define GS_CASE(D)                                                                                  \
   case D:                                                                                           \
     cudaFuncSetAttribute(featurize_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total); \
-    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, L, gerr, reuse); \
+    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, gerr, reuse); \
     g_launch_count++;                                                                               \
     break;
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4)

@@ -68,7 +68,9 @@ struct RRead {                // one expanded read (resolve.py:56-79 ResolvedRea
 
 struct Layout {                 // byte offsets inside dynamic shared memory (K1)
   int blob, dec, pdec, didx, cf, pcf, reads, paths, rdb, frd, rows, stack, volacc, touched, icall, srcb,
-      srcl, rdepb, rdep, dirty, rflag, rowlist, misc, warps;
+      srcl, rdepb, rdep, dirty, rflag, rowlist, rsrc, kern, dm, cmask, kmb, kml, icb, icl, dlist, gdirty,
+      kdirty, misc, warps;
+  int mw;                       // dependency-mask words per func (0 = incremental resolve off)
   int warp_bytes, total;
   int rcap, pcap, S, R;
 };

@@ -97,7 +97,7 @@ class Scorer:
         verdict = torch.empty((n,), dtype=torch.uint8, device=self.device)
         nrows = torch.empty((n,), dtype=torch.int32, device=self.device)
         _lib.check(self.lib.gs_featurize(self.handle, _ptr(dec), n, dec.shape[1] // 16, C.c_void_p(0),
-                                         C.c_void_p(0), _ptr(nrows), _ptr(verdict), _stream()))
+                                         C.c_void_p(0), _ptr(nrows), _ptr(verdict), C.c_void_p(0), _stream()))
         return verdict
 
     def featurize(self, dec: torch.Tensor, out=None):
@@ -108,11 +108,19 @@ class Scorer:
                 feats=torch.empty((n, self.R, NF), dtype=torch.float64, device=self.device),
                 row_key=torch.empty((n, self.R), dtype=torch.int32, device=self.device),
                 n_rows=torch.empty((n,), dtype=torch.int32, device=self.device),
-                verdict=torch.empty((n,), dtype=torch.uint8, device=self.device))
+                verdict=torch.empty((n,), dtype=torch.uint8, device=self.device),
+                row_src=torch.empty((n, self.R), dtype=torch.int32, device=self.device))
         _lib.check(self.lib.gs_featurize(self.handle, _ptr(dec), n, S, _ptr(out["feats"]),
                                          _ptr(out["row_key"]), _ptr(out["n_rows"]),
-                                         _ptr(out["verdict"]), _stream()))
+                                         _ptr(out["verdict"]), _ptr(out.get("row_src")), _stream()))
         return out
+
+    def stats(self):
+        """K1 work counters since the last call (see gs_stats)."""
+        out = np.zeros(6, dtype=np.int64)
+        _lib.check(self.lib.gs_stats(self.handle, C.c_void_p(out.ctypes.data), _stream()))
+        return dict(zip(("candidates", "incremental", "rows_computed", "rows", "geometries", "reserved"),
+                        out.tolist()))
 
     def check(self):
         """Synchronize and raise on any device-side capacity / schedule error."""
