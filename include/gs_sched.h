@@ -154,12 +154,21 @@ int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
 
 /* K2: basis + two-tower network + g.c + h + in-order stage sum.  Replaces
  * CostEvaluator.cost (search.py:115-124).  row_cost/basis_gh optional
- * (NULL = not written; basis_gh is [c*R + r][31] = g[30], h). */
+ * (NULL = not written; basis_gh is [c*R + r][31] = g[30], h).  With
+ * row_src (from gs_featurize, same batch) the network runs once per
+ * distinct row and every other row takes its source row's cost (exact:
+ * identical features give identical costs); row_cost is then required as
+ * [N][R] scratch and ends up holding every row's cost.  basis_gh != NULL
+ * disables the reuse. */
 int gs_cost(gs_pipeline_t p, const double* feats, const int32_t* row_key,
-            const int32_t* n_rows, int64_t n, double* total, double* row_cost,
-            double* basis_gh, void* stream);
+            const int32_t* n_rows, const int32_t* row_src, int64_t n,
+            double* total, double* row_cost, double* basis_gh, void* stream);
 
-/* K3: blake2b-64 structural hash at `depth` (loopnest.py:131-165). */
+/* K3: blake2b-64 structural hash at `depth` (loopnest.py:131-165).  A
+ * candidate whose (func, kind, consumer, serial/thread presence) fields
+ * equal its predecessor's takes the predecessor's hash (equal canonical
+ * bytes); only run heads are hashed.  Grows an internal n-byte scratch on
+ * first use with a larger n (synchronizes `stream` then). */
 int gs_struct_hash(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
                    int depth, uint64_t* out, void* stream);
 
@@ -196,7 +205,8 @@ int gs_beam_topk(const double* costs, const uint64_t* pass_hash, int64_t n,
 /* K1 work counters accumulated since the last call (then reset);
  * synchronizes `stream`.  out[0] candidates, [1] candidates resolved
  * incrementally (sibling of the previous one), [2] feature rows computed,
- * [3] feature rows emitted, [4] func geometries (re)resolved, [5] reserved. */
+ * [3] feature rows emitted, [4] func geometries (re)resolved, [5] shape of
+ * the last K1 launch: scorer warps per CTA << 32 | shared bytes per warp. */
 int gs_stats(gs_pipeline_t p, int64_t* out, void* stream);
 
 /* Device-side error word of the last K1 launch (capacity overflow etc.);

@@ -47,7 +47,7 @@ def load(path: str = LIB_PATH):
         "gs_set_weights": (i32, [P, i32, i32] + [V] * 8),
         "gs_set_reuse": (i32, [P, i32]),
         "gs_featurize": (i32, [P, V, i64, i32, V, V, V, V, V, V]),
-        "gs_cost": (i32, [P, V, V, V, i64, V, V, V, V]),
+        "gs_cost": (i32, [P, V, V, V, V, i64, V, V, V, V]),
         "gs_struct_hash": (i32, [P, V, i64, i32, i32, V, V]),
         "gs_select_workspace_bytes": (i64, [i64]),
         "gs_select_reps": (i32, [V, V, i64, u64, V, i64, V, V, V, V, V]),

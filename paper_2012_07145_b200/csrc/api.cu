@@ -11,13 +11,13 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
                      const Layout& L, int nwarps, int grid, int* gerr, int reuse, cudaStream_t st);
-int featurize_occupancy(int nd, int nwarps, int smem);
+int featurize_warps(const Layout& L1, int max_smem);
 int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st);
 int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
-                const int32_t* n_rows, int64_t n, int R, double* total, double* row_cost, double* basis_gh,
-                int num_sms, cudaStream_t st);
+                const int32_t* n_rows, const int32_t* row_src, int64_t n, int R, double* total, double* row_cost,
+                double* basis_gh, int num_sms, cudaStream_t st);
 int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, const int32_t* sorted_funcs,
-                const uint8_t* names, const int32_t* name_off, uint64_t* out, cudaStream_t st);
+                const uint8_t* names, const int32_t* name_off, uint64_t* out, uint8_t* head, cudaStream_t st);
 int64_t select_workspace_bytes(int64_t n);
 int select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, uint64_t phase_seed, void* ws,
                 int64_t ws_bytes, int64_t* rep_idx, int64_t* n_reps, int64_t* n_rejects, int64_t* rej_idx,
@@ -60,6 +60,9 @@ struct GsPipeline {
   int rcap = 0, pcap = 0;
   int reuse = 1;
   int nwarps = 8;
+  int last_warps = 0, last_slice = 0;   // K1 launch shape (diagnostics)
+  uint8_t* hscratch = nullptr;   // K3 run-head flags (grow-only)
+  int64_t hcap = 0;
 };
 
 extern "C" {
@@ -171,7 +174,7 @@ int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
 int gs_pipeline_destroy(gs_pipeline_t p) {
   if (!p) return GS_OK;
   cudaFree(p->dev); cudaFree(p->blob); cudaFree(p->stage_of_func); cudaFree(p->algo); cudaFree(p->sorted);
-  cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err);
+  cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err); cudaFree(p->hscratch);
   for (double* b : p->wbufs) cudaFree(b);
   delete p;
   return GS_OK;
@@ -218,15 +221,16 @@ int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, doubl
                  int32_t* n_rows, uint8_t* verdict, int32_t* row_src, void* stream) {
   if (!p || S < 1 || n < 0) return fail(GS_ERR_ARG, "bad featurize arguments");
   if (n == 0) return GS_OK;
-  const int nwarps = p->nwarps;
+  // one CTA per SM, as many independent scorer warps as shared memory holds
+  const int nwarps = std::min(p->nwarps, featurize_warps(layout_for(p, S, 1), p->max_smem));
+  if (nwarps < 1)
+    return fail(GS_ERR_CAPACITY, "pipeline too large for one warp's shared-memory slice (" +
+                                     std::to_string(layout_for(p, S, 1).total) + " > " +
+                                     std::to_string(p->max_smem) + " bytes)");
   Layout L = layout_for(p, S, nwarps);
-  if (L.total > p->max_smem)
-    return fail(GS_ERR_CAPACITY, "pipeline too large for the per-CTA shared-memory workspace (" +
-                                     std::to_string(L.total) + " > " + std::to_string(p->max_smem) + " bytes)");
-  int occ = featurize_occupancy(p->host.nd, nwarps, L.total);
-  if (occ < 1) occ = 1;
-  int64_t grid = (int64_t)p->num_sms * occ;
-  if (grid > n) grid = n;
+  int64_t grid = std::min<int64_t>(p->num_sms, (n + nwarps - 1) / nwarps);
+  p->last_warps = nwarps;
+  p->last_slice = L.warp_bytes;
   int rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, nwarps,
                             (int)grid, p->err, p->reuse, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "unsupported ndim");
@@ -245,11 +249,12 @@ int gs_check(gs_pipeline_t p, void* stream) {
   return GS_OK;
 }
 
-int gs_cost(gs_pipeline_t p, const double* feats, const int32_t* row_key, const int32_t* n_rows, int64_t n,
-            double* total, double* row_cost, double* basis_gh, void* stream) {
+int gs_cost(gs_pipeline_t p, const double* feats, const int32_t* row_key, const int32_t* n_rows,
+            const int32_t* row_src, int64_t n, double* total, double* row_cost, double* basis_gh, void* stream) {
   if (!p || !p->net.sched_w) return fail(GS_ERR_ARG, "weights not set (gs_set_weights)");
-  int rc = launch_cost(p->net, p->stage_of_func, feats, row_key, n_rows, n, std::max(1, p->host.max_rows), total,
-                       row_cost, basis_gh, p->num_sms, (cudaStream_t)stream);
+  if (row_src && !row_cost) return fail(GS_ERR_ARG, "row reuse (row_src) needs the row_cost buffer");
+  int rc = launch_cost(p->net, p->stage_of_func, feats, row_key, n_rows, row_src, n, std::max(1, p->host.max_rows),
+                       total, row_cost, basis_gh, p->num_sms, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "unsupported network dims");
   CK(cudaGetLastError());
   return GS_OK;
@@ -258,7 +263,16 @@ int gs_cost(gs_pipeline_t p, const double* feats, const int32_t* row_key, const 
 int gs_struct_hash(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, int depth, uint64_t* out,
                    void* stream) {
   if (!p || depth < 0) return fail(GS_ERR_ARG, "depth must be >= 0");
-  int rc = launch_hash(dec, n, S, p->host.nf, depth, p->sorted, p->names, p->name_off, out, (cudaStream_t)stream);
+  if (n > p->hcap) {   // one-time growth of the run-head scratch
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    if (p->hscratch) CK(cudaFree(p->hscratch));
+    p->hscratch = nullptr;
+    p->hcap = 0;
+    CK(cudaMalloc(&p->hscratch, (size_t)n));
+    p->hcap = n;
+  }
+  int rc = launch_hash(dec, n, S, p->host.nf, depth, p->sorted, p->names, p->name_off, out, p->hscratch,
+                       (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "too many funcs for the hash kernel");
   CK(cudaGetLastError());
   return GS_OK;
@@ -267,8 +281,9 @@ int gs_struct_hash(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, int
 int gs_stats(gs_pipeline_t p, int64_t* out, void* stream) {
   if (!p || !out) return fail(GS_ERR_ARG, "null argument");
   CK(cudaStreamSynchronize((cudaStream_t)stream));
-  CK(cudaMemcpy(out, p->err + 2, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out, p->err + 2, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost));
   CK(cudaMemset(p->err + 2, 0, 6 * sizeof(int64_t)));
+  out[5] = (int64_t)p->last_warps << 32 | p->last_slice;
   return GS_OK;
 }
 

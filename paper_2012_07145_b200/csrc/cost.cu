@@ -169,6 +169,97 @@ __global__ void __launch_bounds__(128) cost_kernel(NetDev net, const int32_t* __
   }
 }
 
+// Exact row reuse (gs_featurize row_src): a row whose features repeat
+// candidate row_src[row]'s row bit for bit has that row's cost, so the
+// network runs once per distinct row.  Pass A compacts the computed rows of
+// a chunk in shared memory (full warps run the network), pass B gathers
+// every row's cost from its source and adds a candidate's rows in order.
+constexpr int kChunk = 1024;
+
+template <int MAXE>
+__global__ void __launch_bounds__(128) cost_rows_kernel(NetDev net, const int32_t* __restrict__ stage_of_func,
+                                                        const double* __restrict__ feats,
+                                                        const int32_t* __restrict__ row_key,
+                                                        const int32_t* __restrict__ n_rows,
+                                                        const int32_t* __restrict__ row_src, int64_t n, int R,
+                                                        double* __restrict__ row_cost) {
+  extern __shared__ __align__(16) double smd[];
+  const int E = net.E, H = net.H;
+  double* sw = smd;
+  double* whs = sw + GS_NUM_FEATURES * E;
+  double* wo = whs + E * H;
+  double* bs = wo + H * GS_NUM_COEFFS;
+  double* bo = bs + E;
+  int32_t* list = reinterpret_cast<int32_t*>(bo + GS_NUM_COEFFS);   // kChunk
+  __shared__ int cnt;
+  for (int i = threadIdx.x; i < GS_NUM_FEATURES * E; i += blockDim.x) sw[i] = net.sched_w[i];
+  for (int i = threadIdx.x; i < E * H; i += blockDim.x) whs[i] = net.head_w[E * H + i];
+  for (int i = threadIdx.x; i < H * GS_NUM_COEFFS; i += blockDim.x) wo[i] = net.out_w[i];
+  for (int i = threadIdx.x; i < E; i += blockDim.x) bs[i] = net.sched_b[i];
+  for (int i = threadIdx.x; i < GS_NUM_COEFFS; i += blockDim.x) bo[i] = net.out_b[i];
+  const int64_t total_rows = n * (int64_t)R;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t base = (int64_t)blockIdx.x * kChunk; base < total_rows; base += (int64_t)gridDim.x * kChunk) {
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    for (int i0 = 0; i0 < kChunk; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      const int64_t row = base + i;
+      bool t = false;
+      if (row < total_rows) {
+        const int64_t c = row / R;
+        const int r = (int)(row - c * R);
+        t = r < n_rows[c] && row_src[row] == (int32_t)c;
+      }
+      const unsigned b = __ballot_sync(0xffffffffu, t);
+      int pos = 0;
+      if (lane == 0 && b) pos = atomicAdd(&cnt, __popc(b));
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+      if (t) list[pos + __popc(b & ((1u << lane) - 1))] = i;
+    }
+    __syncthreads();
+    const int m = cnt;
+    (void)warp;
+    for (int q = threadIdx.x; q < m; q += blockDim.x) {
+      const int64_t row = base + list[q];
+      const int key = row_key[row];
+      const int stage = stage_of_func[key >> 8] + (key & 255);
+      row_cost[row] = stage_row_cost<MAXE>(net, sw, whs, wo, bs, bo, feats + row * GS_NUM_FEATURES, stage, nullptr);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(128) stage_sum_kernel(const int32_t* __restrict__ n_rows,
+                                                        const int32_t* __restrict__ row_src,
+                                                        const double* __restrict__ row_cost, int64_t n, int R,
+                                                        int CB, double* __restrict__ total,
+                                                        double* __restrict__ row_cost_out) {
+  extern __shared__ __align__(16) double buf[];   // CB*R
+  for (int64_t c0 = (int64_t)blockIdx.x * CB; c0 < n; c0 += (int64_t)gridDim.x * CB) {
+    const int ncb = (int)((n - c0) < CB ? (n - c0) : CB);
+    for (int idx = threadIdx.x; idx < ncb * R; idx += blockDim.x) {
+      const int cl = idx / R, r = idx % R;
+      const int64_t c = c0 + cl;
+      if (r >= n_rows[c]) continue;
+      const int64_t row = c * R + r;
+      const int64_t src = (int64_t)row_src[row] * R + r;
+      const double v = row_cost[src];
+      buf[idx] = v;
+      if (row_cost_out && src != row) row_cost_out[row] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < ncb) {
+      const int64_t c = c0 + threadIdx.x;
+      double t = 0.0;
+      const int nr = n_rows[c];
+      for (int r = 0; r < nr; ++r) t = __dadd_rn(t, buf[threadIdx.x * R + r]);
+      total[c] = t;
+    }
+    __syncthreads();
+  }
+}
+
 int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st) {
   if (n_stages == 0) return 0;
   hoist_kernel<<<n_stages, 64, 0, st>>>(net, algo, n_stages); g_launch_count++;
@@ -180,9 +271,36 @@ int cost_smem_bytes(int E, int H, int CB, int R) {
 }
 
 int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
-                const int32_t* n_rows, int64_t n, int R, double* total, double* row_cost, double* basis_gh,
-                int num_sms, cudaStream_t st) {
+                const int32_t* n_rows, const int32_t* row_src, int64_t n, int R, double* total, double* row_cost,
+                double* basis_gh, int num_sms, cudaStream_t st) {
   if (n == 0) return 0;
+  if (row_src && row_cost && !basis_gh) {
+    if (net.E > 64) return -1;
+    const int smA = (GS_NUM_FEATURES * net.E + net.E * net.H + net.H * GS_NUM_COEFFS + net.E + GS_NUM_COEFFS) * 8 +
+                    kChunk * 4;
+    const int64_t chunks = (n * (int64_t)R + kChunk - 1) / kChunk;
+    const int gridA = (int)(chunks < (int64_t)num_sms * 8 ? chunks : (int64_t)num_sms * 8);
+    if (net.E <= 32) {
+      cudaFuncSetAttribute(cost_rows_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smA);
+      cost_rows_kernel<32><<<gridA, 128, smA, st>>>(net, stage_of_func, feats, row_key, n_rows, row_src, n, R,
+                                                    row_cost);
+    } else {
+      cudaFuncSetAttribute(cost_rows_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smA);
+      cost_rows_kernel<64><<<gridA, 128, smA, st>>>(net, stage_of_func, feats, row_key, n_rows, row_src, n, R,
+                                                    row_cost);
+    }
+    g_launch_count++;
+    int CB = 1024 / (R > 0 ? R : 1);
+    if (CB < 1) CB = 1;
+    if (CB > 128) CB = 128;
+    const int smB = CB * R * 8;
+    const int64_t blocks = (n + CB - 1) / CB;
+    const int gridB = (int)(blocks < (int64_t)num_sms * 16 ? blocks : (int64_t)num_sms * 16);
+    cudaFuncSetAttribute(stage_sum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smB);
+    stage_sum_kernel<<<gridB, 128, smB, st>>>(n_rows, row_src, row_cost, n, R, CB, total, row_cost);
+    g_launch_count++;
+    return 0;
+  }
   int CB = 512 / (R > 0 ? R : 1);
   if (CB < 1) CB = 1;
   if (CB > 128) CB = 128;

@@ -55,7 +55,6 @@ struct K1 {
   GsDecision* pdec;  // previous candidate's
   int16_t* didx;
   CF<ND>* cf;        // current geometry
-  CF<ND>* pcf;       // previous candidate's geometry
   RRead* rd;
   int16_t* path;
   int32_t* rdb;      // [2*ns]: begin,end of reads per global stage
@@ -84,6 +83,7 @@ struct K1 {
   uint8_t* kdirty;   // [nf] kernel aggregates recomputed this candidate
   Misc* misc;
   int mw;            // mask words (0 = incremental resolve off)
+  bool track;        // k.cf holds the previous candidate's geometry: flag changed records
   int rcap, pcap;
   int* gerr;
 };
@@ -342,6 +342,29 @@ __device__ __forceinline__ void zero_cf(CF<ND>& c) {
   for (int i = 0; i < (int)(sizeof(CF<ND>) / 4); ++i) w[i] = 0;
 }
 
+// Store a func's geometry record (one lane).  When the buffer holds the
+// previous candidate's geometry, a record that actually changes marks the
+// func dirty: rows depending only on unchanged records are bit-identical.
+// dirty bits: 1 = any field changed, 2 = the allocation layout (tier,
+// realization region) changed — all a consumer's row reads of a producer
+// or of a fuse_at_thread child (strides, allocation bytes).
+template <int ND>
+__device__ __forceinline__ void cf_store(K1<ND>& k, int f, const CF<ND>& c) {
+  if (k.track) {
+    const CF<ND>& o = k.cf[f];
+    const int32_t* a = reinterpret_cast<const int32_t*>(&o);
+    const int32_t* b = reinterpret_cast<const int32_t*>(&c);
+    bool d = false;
+#pragma unroll
+    for (int w = 0; w < (int)(sizeof(CF<ND>) / 4); ++w) d |= a[w] != b[w];
+    bool l = o.tier != c.tier;
+#pragma unroll
+    for (int dd = 0; dd < ND; ++dd) l |= o.rlo[dd] != c.rlo[dd] || o.rhi[dd] != c.rhi[dd];
+    k.dirty[f] |= (uint8_t)(d | (l << 1));
+  }
+  k.cf[f] = c;
+}
+
 // Geometry of the non-inline decision i (resolve.py:232-333); warp-wide.
 // Kernel aggregates (threads per block = max, shared bytes = sum over the
 // kernel's members) are NOT accumulated here but by kernel_aggregates():
@@ -384,8 +407,13 @@ __device__ bool geometry_one(K1<ND>& k, int i) {
     }
     c.kind = K_ROOT; c.tier = T_GLOBAL; c.kernel = (int16_t)f; c.realizations = 1;
     c.n_threads = (int32_t)nt; c.unrolled = sp < 16; c.has_serial = 1; c.serial_prod = (int32_t)sp;
-    c.n_blocks = nb; c.k_threads = (int32_t)nt; c.k_shared = 0;
-    if (lane == 0) k.cf[f] = c;
+    c.n_blocks = nb;
+    // aggregates are kernel_aggregates()' business; keep the stored ones so
+    // the change test sees only this func's own geometry
+    c.k_threads = k.track ? k.cf[f].k_threads : (int32_t)nt;
+    c.k_shared = k.track ? k.cf[f].k_shared : 0;
+    __syncwarp();
+    if (lane == 0) cf_store(k, f, c);
     __syncwarp();
     return true;
   }
@@ -453,7 +481,7 @@ __device__ bool geometry_one(K1<ND>& k, int i) {
     c.kind = K_BLOCK; c.tier = T_SHARED; c.kernel = cg0.kernel; c.realizations = K.n_blocks;
     c.n_threads = (int32_t)nt; c.unrolled = sp < 16; c.has_serial = 1; c.serial_prod = (int32_t)sp;
     __syncwarp();
-    if (lane == 0) k.cf[f] = c;
+    if (lane == 0) cf_store(k, f, c);
   } else {
     int64_t pe = 1;
 #pragma unroll
@@ -469,7 +497,7 @@ __device__ bool geometry_one(K1<ND>& k, int i) {
     c.realizations = K.n_blocks * (int64_t)cg0.n_threads; c.n_threads = cg0.n_threads;
     c.unrolled = pe < 16; c.has_serial = 0; c.serial_prod = 1;
     __syncwarp();
-    if (lane == 0) k.cf[f] = c;
+    if (lane == 0) cf_store(k, f, c);
   }
   __syncwarp();
   return true;
@@ -503,7 +531,7 @@ __device__ void external_one(K1<ND>& k, int f) {
     c.tlo[dd] = c.rlo[dd]; c.thi[dd] = c.rhi[dd];
     c.ctx[dd] = 1; c.ext[dd] = 1;
   }
-  k.cf[f] = c;
+  cf_store(k, f, c);
 }
 
 // kernel aggregates of a root (resolve.py:325-333): one lane
@@ -518,6 +546,7 @@ __device__ void kernel_aggregates(K1<ND>& k, int kf) {
     if (c.n_threads > kt) kt = c.n_threads;
     if (c.kind == K_BLOCK) sh += alloc_of(c) * k.F[f].elem_bytes;
   }
+  if (k.track && (o.k_threads != kt || o.k_shared != sh)) k.dirty[kf] |= 1;
   o.k_threads = kt;
   o.k_shared = sh;
 }
@@ -527,7 +556,7 @@ __device__ void kernel_aggregates(K1<ND>& k, int kf) {
 // exactly as in the sequential pass over all entries.
 template <int ND>
 __device__ void inline_one(K1<ND>& k, int f) {
-  CF<ND>& ic = k.cf[f];
+  CF<ND> ic;
   zero_cf(ic);
   ic.kind = K_INLINE; ic.consumer = -1;
   for (int q = k.icb[f]; q < k.icb[f + 1]; ++q) {
@@ -548,6 +577,7 @@ __device__ void inline_one(K1<ND>& k, int f) {
     for (int dd = 0; dd < ND; ++dd) ic.ctx[dd] = 1;
   }
   for (int dd = 0; dd < ND; ++dd) { ic.rhi[dd] = -1; ic.thi[dd] = -1; ic.ext[dd] = 1; }
+  cf_store(k, f, ic);
 }
 
 // warp 0: decision validation + structure (if changed) + geometry.
@@ -597,10 +627,9 @@ __device__ void resolve(K1<ND>& k) {
   } else {
     for (int f = lane; f < nf; f += 32) { k.gdirty[f] = 1; k.kdirty[f] = 1; }
   }
+  for (int f = lane; f < nf; f += 32) k.dirty[f] = diff ? 0 : 3;
+  k.track = diff;
   __syncwarp();
-  if (diff)   // keep the records about to be rewritten, for the change test
-    for (int f = lane; f < nf; f += 32)
-      if (k.gdirty[f] || k.kdirty[f]) k.pcf[f] = k.cf[f];
   // decisions to re-resolve, in decision order
   int cnt = 0;
   for (int i0 = 0; i0 < m.ndec; i0 += 32) {
@@ -623,19 +652,6 @@ __device__ void resolve(K1<ND>& k) {
   for (int f = lane; f < nf; f += 32)
     if (k.gdirty[f] && k.didx[f] >= 0 && k.dec[k.didx[f]].kind == GS_INLINE) inline_one(k, f);
   __syncwarp();
-  constexpr int WPF = (int)(sizeof(CF<ND>) / 4);
-  for (int f = lane; f < nf; f += 32) {
-    bool d = true;
-    if (diff) {
-      d = false;
-      if (k.gdirty[f] || k.kdirty[f]) {
-        const int32_t* a = reinterpret_cast<const int32_t*>(&k.cf[f]);
-        const int32_t* b = reinterpret_cast<const int32_t*>(&k.pcf[f]);
-        for (int w = 0; w < WPF; ++w) d |= a[w] != b[w];
-      }
-    }
-    k.dirty[f] = d;
-  }
   __syncwarp();
 }
 
@@ -863,21 +879,49 @@ struct ModM {
   }
 };
 
-// lane origins (byte address of the instruction constant 0) of emulated warp w
+// Lane origins (byte address of instruction constant 0) of the emulated
+// warps of block 0, warp after warp: thread t's coordinates are the
+// mixed-radix digits of t over the thread extents (dim 0 fastest); moving
+// to the next warp adds the digits of 32 with carries — no division in the
+// loop.
 template <int ND>
-__device__ __forceinline__ int64_t warp_origin(const CF<ND>& h, const int64_t* ts, const int64_t* bs, int64_t cst,
-                                               int w, int lane, bool& active) {
-  int t = w * 32 + lane;
-  active = t < h.n_threads;
-  int64_t org = cst;
+struct WarpWalk {
+  int cd[ND], inc[ND], ext[ND];
+  int64_t mul[ND], org0;
+  int t, n;
+  __device__ WarpWalk(const CF<ND>& h, const int64_t* ts, const int64_t* bs, int64_t cst, int lane) {
+    int a = lane, b = 32;
 #pragma unroll
-  for (int d = 0; d < ND; ++d) {
-    const int cd = t % h.ctx[d];
-    t /= h.ctx[d];
-    org += (int64_t)cd * h.coeff[d] * ts[d] * bs[d];
+    for (int d = 0; d < ND; ++d) {
+      ext[d] = h.ctx[d];
+      cd[d] = a % ext[d]; a /= ext[d];
+      inc[d] = b % ext[d]; b /= ext[d];
+      mul[d] = (int64_t)h.coeff[d] * ts[d] * bs[d];
+    }
+    cd[ND - 1] += a * ext[ND - 1];   // top digit is unbounded
+    inc[ND - 1] += b * ext[ND - 1];
+    org0 = cst;
+    t = lane;
+    n = h.n_threads;
   }
-  return org;
-}
+  __device__ __forceinline__ int64_t origin(bool& active) const {
+    active = t < n;
+    int64_t o = org0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) o += (int64_t)cd[d] * mul[d];
+    return o;
+  }
+  __device__ __forceinline__ void next() {
+    int carry = 0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      cd[d] += inc[d] + carry;
+      carry = 0;
+      if (d < ND - 1 && cd[d] >= ext[d]) { cd[d] -= ext[d]; carry = 1; }
+    }
+    t += 32;
+  }
+};
 
 // transactions of one emulated warp for ONE instruction constant r
 // (featurize.py:173-196): global = distinct segments; shared = max over
@@ -1058,9 +1102,10 @@ __device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, in
   int64_t rel0 = 0, rel1 = 0, o00 = 0, o01 = 0;
   unsigned am0 = 0u, am1 = 0u;
   unsigned long long total = 0;
-  for (int w = 0; w < nwarps; ++w) {
+  WarpWalk<ND> walk(h, ts, bs, cst, lane);
+  for (int w = 0; w < nwarps; ++w, walk.next()) {
     bool active;
-    const int64_t org = warp_origin(h, ts, bs, cst, w, lane, active);
+    const int64_t org = walk.origin(active);
     const unsigned amask = __ballot_sync(0xffffffffu, active);
     const int64_t ow = __shfl_sync(0xffffffffu, org, 0);
     const int64_t rw = org - ow;
@@ -1356,68 +1401,75 @@ __device__ __forceinline__ void bulk_wait(uint64_t* bar) {
   }
 }
 
+// Every warp is an independent scorer: it walks its own contiguous range of
+// candidates (consecutive candidates of a beam step are siblings), keeping
+// its decision structure, geometry and scratch in its own slice of shared
+// memory; the candidate-independent pipeline descriptor is shared by the
+// CTA.  There is no CTA-wide barrier after the descriptor is staged, so the
+// serial parts of one candidate (resolve, prune) overlap other warps' rows.
 template <int ND>
-__global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob,
-                                                        const GsDecision* __restrict__ dec, int64_t n, int S,
-                                                        double* __restrict__ feats, int32_t* __restrict__ row_key,
-                                                        int32_t* __restrict__ n_rows, uint8_t* __restrict__ verdict,
-                                                        int32_t* __restrict__ row_src, Layout L, int* gerr, int reuse) {
+__global__ void __launch_bounds__(kK1MaxWarps * 32, 1)
+featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob, const GsDecision* __restrict__ dec,
+                 int64_t n, int S, double* __restrict__ feats, int32_t* __restrict__ row_key,
+                 int32_t* __restrict__ n_rows, uint8_t* __restrict__ verdict, int32_t* __restrict__ row_src,
+                 Layout L, int* gerr, int reuse) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar;
   const int warp = threadIdx.x >> 5, lane = lane_id(), nw = blockDim.x >> 5;
   if (threadIdx.x == 0) bulk_stage(sm + L.blob, blob, P->blob_bytes, &bar);
+  uint8_t* ws = sm + L.warps + (size_t)warp * L.warp_bytes;   // this warp's slice
   K1<ND> k;
   k.P = P;
   k.F = reinterpret_cast<const GsFunc*>(sm + L.blob);
   k.ST = reinterpret_cast<const GsStage*>(sm + L.blob + P->off_stages);
   k.A = reinterpret_cast<const GsAccess*>(sm + L.blob + P->off_access);
-  k.dec = reinterpret_cast<GsDecision*>(sm + L.dec);
-  k.pdec = reinterpret_cast<GsDecision*>(sm + L.pdec);
-  k.didx = reinterpret_cast<int16_t*>(sm + L.didx);
-  k.cf = reinterpret_cast<CF<ND>*>(sm + L.cf);
-  k.pcf = reinterpret_cast<CF<ND>*>(sm + L.pcf);
-  k.rd = reinterpret_cast<RRead*>(sm + L.reads);
-  k.path = reinterpret_cast<int16_t*>(sm + L.paths);
-  k.rdb = reinterpret_cast<int32_t*>(sm + L.rdb);
-  k.frd = reinterpret_cast<int32_t*>(sm + L.frd);
-  k.rows = reinterpret_cast<int32_t*>(sm + L.rows);
-  k.stack = reinterpret_cast<Frame*>(sm + L.stack);
-  k.volacc = reinterpret_cast<int64_t*>(sm + L.volacc);
-  k.touched = reinterpret_cast<int16_t*>(sm + L.touched);
-  k.icall = reinterpret_cast<ICall*>(sm + L.icall);
-  k.srcb = reinterpret_cast<int32_t*>(sm + L.srcb);
-  k.srcl = reinterpret_cast<int16_t*>(sm + L.srcl);
-  k.rdepb = reinterpret_cast<int32_t*>(sm + L.rdepb);
-  k.rdep = reinterpret_cast<int16_t*>(sm + L.rdep);
-  k.dirty = reinterpret_cast<uint8_t*>(sm + L.dirty);
-  k.rowlist = reinterpret_cast<int16_t*>(sm + L.rowlist);
-  k.kern = reinterpret_cast<int16_t*>(sm + L.kern);
-  k.dm = reinterpret_cast<uint32_t*>(sm + L.dm);
-  k.cmask = reinterpret_cast<uint32_t*>(sm + L.cmask);
-  k.kmb = reinterpret_cast<int32_t*>(sm + L.kmb);
-  k.kml = reinterpret_cast<int16_t*>(sm + L.kml);
-  k.icb = reinterpret_cast<int32_t*>(sm + L.icb);
-  k.icl = reinterpret_cast<int16_t*>(sm + L.icl);
-  k.dlist = reinterpret_cast<int16_t*>(sm + L.dlist);
-  k.gdirty = reinterpret_cast<uint8_t*>(sm + L.gdirty);
-  k.kdirty = reinterpret_cast<uint8_t*>(sm + L.kdirty);
-  k.misc = reinterpret_cast<Misc*>(sm + L.misc);
-  k.rcap = L.rcap; k.pcap = L.pcap; k.gerr = gerr; k.mw = L.mw;
-  WarpScr& W = *reinterpret_cast<WarpScr*>(sm + L.warps + warp * L.warp_bytes);
-  uint8_t* rflag = reinterpret_cast<uint8_t*>(sm + L.rflag);
-  int32_t* rsrc = reinterpret_cast<int32_t*>(sm + L.rsrc);
-  // contiguous candidate range per CTA: consecutive candidates of a beam
-  // step are siblings, which is what the incremental resolve and the row
-  // reuse below exploit
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t c0 = (int64_t)blockIdx.x * per;
+  k.dec = reinterpret_cast<GsDecision*>(ws + L.dec);
+  k.pdec = reinterpret_cast<GsDecision*>(ws + L.pdec);
+  k.didx = reinterpret_cast<int16_t*>(ws + L.didx);
+  k.cf = reinterpret_cast<CF<ND>*>(ws + L.cf);
+  k.rd = reinterpret_cast<RRead*>(ws + L.reads);
+  k.path = reinterpret_cast<int16_t*>(ws + L.paths);
+  k.rdb = reinterpret_cast<int32_t*>(ws + L.rdb);
+  k.frd = reinterpret_cast<int32_t*>(ws + L.frd);
+  k.rows = reinterpret_cast<int32_t*>(ws + L.rows);
+  k.stack = reinterpret_cast<Frame*>(ws + L.stack);
+  k.volacc = reinterpret_cast<int64_t*>(ws + L.volacc);
+  k.touched = reinterpret_cast<int16_t*>(ws + L.touched);
+  k.icall = reinterpret_cast<ICall*>(ws + L.icall);
+  k.srcb = reinterpret_cast<int32_t*>(ws + L.srcb);
+  k.srcl = reinterpret_cast<int16_t*>(ws + L.srcl);
+  k.rdepb = reinterpret_cast<int32_t*>(ws + L.rdepb);
+  k.rdep = reinterpret_cast<int16_t*>(ws + L.rdep);
+  k.dirty = reinterpret_cast<uint8_t*>(ws + L.dirty);
+  k.rowlist = reinterpret_cast<int16_t*>(ws + L.rowlist);
+  k.kern = reinterpret_cast<int16_t*>(ws + L.kern);
+  k.dm = reinterpret_cast<uint32_t*>(ws + L.dm);
+  k.cmask = reinterpret_cast<uint32_t*>(ws + L.cmask);
+  k.kmb = reinterpret_cast<int32_t*>(ws + L.kmb);
+  k.kml = reinterpret_cast<int16_t*>(ws + L.kml);
+  k.icb = reinterpret_cast<int32_t*>(ws + L.icb);
+  k.icl = reinterpret_cast<int16_t*>(ws + L.icl);
+  k.dlist = reinterpret_cast<int16_t*>(ws + L.dlist);
+  k.gdirty = reinterpret_cast<uint8_t*>(ws + L.gdirty);
+  k.kdirty = reinterpret_cast<uint8_t*>(ws + L.kdirty);
+  k.misc = reinterpret_cast<Misc*>(ws + L.misc);
+  k.rcap = L.rcap; k.pcap = L.pcap; k.gerr = gerr; k.mw = L.mw; k.track = false;
+  WarpScr& W = *reinterpret_cast<WarpScr*>(ws + L.scr);
+  uint8_t* rflag = ws + L.rflag;
+  int32_t* rsrc = reinterpret_cast<int32_t*>(ws + L.rsrc);
+  // contiguous candidate range per warp
+  const int64_t nwt = (int64_t)gridDim.x * nw;
+  const int64_t gw = (int64_t)blockIdx.x * nw + warp;
+  const int64_t per = (n + nwt - 1) / nwt;
+  const int64_t c0 = gw * per < n ? gw * per : n;
   const int64_t c1 = c0 + per < n ? c0 + per : n;
-  if (threadIdx.x == 0) { k.misc->prev_valid = 0; k.misc->same_struct = 0; k.misc->ndec = 0; }
-  unsigned long long st_inc = 0, st_rows = 0, st_emit = 0, st_geo = 0;   // work counters (thread 0)
+  Misc& m = *k.misc;
+  if (lane == 0) { m.prev_valid = 0; m.same_struct = 0; m.ndec = 0; }
+  unsigned long long st_inc = 0, st_rows = 0, st_emit = 0, st_geo = 0;   // work counters (lane 0)
   bulk_wait(&bar);
-  __syncthreads();
+  __syncthreads();   // the only CTA barrier: descriptor staged
   for (int64_t c = c0; c < c1; ++c) {
-    if (warp == 0) {
+    {
       const uint4* src = reinterpret_cast<const uint4*>(dec + c * S);
       uint4* dst = reinterpret_cast<uint4*>(k.dec);
       for (int i = lane; i < S; i += 32) dst[i] = __ldg(src + i);   // 128-bit loads
@@ -1442,79 +1494,76 @@ __global__ void __launch_bounds__(256) featurize_kernel(const PipeDev* __restric
         }
         diff |= __ballot_sync(0xffffffffu, d);
       }
+      __syncwarp();
       if (lane == 0) {
-        Misc& m = *k.misc;
         m.same_struct = reuse && m.prev_valid && diff == 0 && (int)cnt == m.ndec;
-        m.ndec = (int)cnt; m.err = 0;
+        m.ndec = (int)cnt; m.err = 0; m.ngeo = 0;
         if (!m.same_struct) m.nrows = 0;
       }
       __syncwarp();
       resolve<ND>(k);
-      const int v = k.misc->err ? 255 : prune_verdict<ND>(k);
+      const int v = m.err ? 255 : prune_verdict<ND>(k);
       if (lane == 0) {
-        Misc& m = *k.misc;
         if (m.err) { atomicOr(gerr, m.err); m.nrows = 0; }
         verdict[c] = (uint8_t)v;
         n_rows[c] = m.nrows;
       }
+      __syncwarp();
     }
-    __syncthreads();
-    const Misc& m = *k.misc;
     const int nr = feats ? m.nrows : 0;   // feats == NULL: prune verdict only
     const bool diffable = m.same_struct && !m.err;
     // rows to recompute: own func, host, host kernel, read producers and
     // fuse_at_thread children unchanged => features are bit-identical
-    for (int r = threadIdx.x; r < nr; r += blockDim.x) {
-      bool d = true;
-      if (diffable) {
-        const int f = k.rows[r] >> 8;
-        const CF<ND>& g = k.cf[f];
-        const int host = g.kind == K_INLINE ? g.consumer : f;
-        d = k.dirty[f];
-        if (host >= 0) { d |= k.dirty[host]; if (k.cf[host].kernel >= 0) d |= k.dirty[k.cf[host].kernel]; }
-        for (int q = k.rdepb[r]; q < k.rdepb[r + 1] && !d; ++q) d |= k.dirty[k.rdep[q]];
+    int nd = 0;
+    for (int r0 = 0; r0 < nr; r0 += 32) {
+      const int r = r0 + lane;
+      bool d = false;
+      if (r < nr) {
+        d = true;
+        if (diffable) {
+          const int f = k.rows[r] >> 8;
+          const CF<ND>& g = k.cf[f];
+          const int host = g.kind == K_INLINE ? g.consumer : f;
+          d = k.dirty[f] & 1;
+          if (host >= 0) { d |= k.dirty[host] & 1; if (k.cf[host].kernel >= 0) d |= k.dirty[k.cf[host].kernel] & 1; }
+          // read producers / thread children: only their layout matters
+          for (int q = k.rdepb[r]; q < k.rdepb[r + 1] && !d; ++q) d |= (k.dirty[k.rdep[q]] >> 1) & 1;
+        }
+        rflag[r] = d;
+        if (d) rsrc[r] = (int32_t)c;
       }
-      rflag[r] = d;
-      if (d) rsrc[r] = (int32_t)c;
+      const unsigned b = __ballot_sync(0xffffffffu, d);
+      if (d) k.rowlist[nd + __popc(b & ((1u << lane) - 1))] = (int16_t)r;
+      nd += __popc(b);
     }
-    __syncthreads();
-    if (warp == 0) {   // compact the dirty rows
-      int cntd = 0;
-      for (int r0 = 0; r0 < nr; r0 += 32) {
-        const int r = r0 + lane;
-        const bool d = r < nr && rflag[r];
-        const unsigned b = __ballot_sync(0xffffffffu, d);
-        if (d) k.rowlist[cntd + __popc(b & ((1u << lane) - 1))] = (int16_t)r;
-        cntd += __popc(b);
-      }
-      if (lane == 0) k.misc->ndirty = cntd;
-    }
-    __syncthreads();
-    const int nd = k.misc->ndirty;
-    if (threadIdx.x == 0) { st_inc += m.same_struct; st_rows += nd; st_emit += nr; st_geo += m.ngeo; }
-    for (int q = warp; q < nd; q += nw) {
+    __syncwarp();
+    if (lane == 0) { st_inc += m.same_struct; st_rows += nd; st_emit += nr; st_geo += m.ngeo; }
+    for (int q = 0; q < nd; ++q) {
       const int r = k.rowlist[q];
       const int key = k.rows[r];
       const int f = key >> 8, si = key & 255;
       row_features<ND>(k, W, f, si, k.cf[f].kind == K_INLINE, feats + ((int64_t)c * L.R + r) * GS_NUM_FEATURES);
     }
-    // clean rows: copy the previous candidate's (same CTA, already visible)
-    for (int r = warp; r < nr; r += nw) {
-      if (lane == 0) {
-        row_key[c * L.R + r] = k.rows[r];
-        if (row_src) row_src[c * L.R + r] = rsrc[r];
-      }
-      if (rflag[r]) continue;
-      const double* src = feats + ((int64_t)(c - 1) * L.R + r) * GS_NUM_FEATURES;
-      double* dst = feats + ((int64_t)c * L.R + r) * GS_NUM_FEATURES;
-      for (int i = lane; i < GS_NUM_FEATURES; i += 32) dst[i] = src[i];
+    // row keys / sources, and clean rows copied from the previous candidate
+    // (written by this warp: visible after __syncwarp)
+    for (int r = lane; r < nr; r += 32) {
+      row_key[c * L.R + r] = k.rows[r];
+      if (row_src) row_src[c * L.R + r] = rsrc[r];
     }
-    __syncthreads();
+    if (diffable && nd < nr) {
+      const double* src = feats + (int64_t)(c - 1) * L.R * GS_NUM_FEATURES;
+      double* dst = feats + (int64_t)c * L.R * GS_NUM_FEATURES;
+      for (int i = lane; i < nr * GS_NUM_FEATURES; i += 32) {
+        const int r = i / GS_NUM_FEATURES;
+        if (!rflag[r]) dst[i] = src[i];
+      }
+    }
+    __syncwarp();
     { GsDecision* t = k.dec; k.dec = k.pdec; k.pdec = t; }
-    if (threadIdx.x == 0) k.misc->prev_valid = (k.misc->err == 0) && feats != nullptr;
-    __syncthreads();
+    if (lane == 0) m.prev_valid = (m.err == 0) && feats != nullptr;
+    __syncwarp();
   }
-  if (threadIdx.x == 0 && c1 > c0) {
+  if (lane == 0 && c1 > c0) {
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(gerr + 2);
     atomicAdd(ctr + 0, (unsigned long long)(c1 - c0));
     atomicAdd(ctr + 1, st_inc); atomicAdd(ctr + 2, st_rows); atomicAdd(ctr + 3, st_emit); atomicAdd(ctr + 4, st_geo);
@@ -1531,25 +1580,27 @@ namespace gs {
 template <int ND>
 static int cf_size() { return (int)sizeof(CF<ND>); }
 
+// Shared memory: [pipeline descriptor | warp 0 slice | warp 1 slice | ...];
+// offsets inside a slice are relative to the slice.  The structure-build
+// scratch (DFS stack, volume accumulators, touched list) aliases the row
+// scratch: they are never live at the same time.
 Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rcap, int pcap, int nwarps) {
   auto al = [](int x) { return (x + 15) & ~15; };
   Layout L{};
+  L.blob = 0;
+  L.warps = al(blob_bytes);
   int o = 0;
-  L.blob = o; o += al(blob_bytes);
   L.dec = o; o += al(S * 16);
   L.pdec = o; o += al(S * 16);
   L.didx = o; o += al(nf * 2);
   int cfs = nd == 1 ? cf_size<1>() : nd == 2 ? cf_size<2>() : nd == 3 ? cf_size<3>() : cf_size<4>();
   L.cf = o; o += al(nf * cfs);
-  L.pcf = o; o += al(nf * cfs);
+  L.pcf = 0;
   L.reads = o; o += al(rcap * (int)sizeof(RRead));
   L.paths = o; o += al(pcap * 2);
   L.rdb = o; o += al(2 * ns * 4);
   L.frd = o; o += al(nf * 4);
   L.rows = o; o += al(R * 4);
-  L.stack = o; o += al((nf + 2) * (int)sizeof(Frame));
-  L.volacc = o; o += al(nf * 8);
-  L.touched = o; o += al(2 * nf * 2 + 4);
   L.icall = o; o += al(pcap * (int)sizeof(ICall));
   L.srcb = o; o += al((nf + 1) * 4);
   L.srcl = o; o += al(rcap * 2);
@@ -1571,11 +1622,24 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   L.gdirty = o; o += al(nf);
   L.kdirty = o; o += al(nf);
   L.misc = o; o += al((int)sizeof(Misc));
-  L.warp_bytes = al((int)sizeof(WarpScr));
-  L.warps = o; o += nwarps * L.warp_bytes;
-  L.total = o;
+  // aliased: row scratch | structure-build scratch
+  L.scr = o;
+  int sa = 0;
+  L.stack = o + sa; sa += al((nf + 2) * (int)sizeof(Frame));
+  L.volacc = o + sa; sa += al(nf * 8);
+  L.touched = o + sa; sa += al(2 * nf * 2 + 4);
+  const int scr = al((int)sizeof(WarpScr)) > sa ? al((int)sizeof(WarpScr)) : sa;
+  o += scr;
+  L.warp_bytes = al(o);
+  L.total = L.warps + nwarps * L.warp_bytes;
   L.rcap = rcap; L.pcap = pcap; L.S = S; L.R = R;
   return L;
+}
+
+// warps per CTA that fit the shared memory budget (one CTA per SM)
+int featurize_warps(const Layout& L1, int max_smem) {
+  int w = (max_smem - L1.warps) / L1.warp_bytes;
+  return w < 1 ? 0 : (w > kK1MaxWarps ? kK1MaxWarps : w);
 }
 
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
@@ -1597,15 +1661,5 @@ int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDeci
   return 0;
 }
 
-int featurize_occupancy(int nd, int nwarps, int smem) {
-  int nb = 0;
-  switch (nd) {
-    case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, featurize_kernel<1>, nwarps * 32, smem); break;
-    case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, featurize_kernel<2>, nwarps * 32, smem); break;
-    case 3: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, featurize_kernel<3>, nwarps * 32, smem); break;
-    default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, featurize_kernel<4>, nwarps * 32, smem); break;
-  }
-  return nb;
-}
 
 }  // namespace gs

@@ -15,6 +15,7 @@ constexpr int kMaxM = 128;          // largest residue modulus (transaction / ba
 constexpr int kRowReads = 64;       // reads attributed to one row
 constexpr int kGroupReads = 16;     // reads in one (tier, producer) group
 constexpr int kLaneIv = 96;         // per-lane interval capacity for unions
+constexpr int kK1MaxWarps = 8;      // K1 warps per CTA (one CTA per SM)
 constexpr int64_t kAddrBias = int64_t(1) << 40;  // featurize.py:256
 
 enum Tier : int8_t { T_GLOBAL = 0, T_SHARED = 1, T_REGISTER = 2, T_NONE = 3 };
@@ -69,7 +70,7 @@ struct RRead {                // one expanded read (resolve.py:56-79 ResolvedRea
 struct Layout {                 // byte offsets inside dynamic shared memory (K1)
   int blob, dec, pdec, didx, cf, pcf, reads, paths, rdb, frd, rows, stack, volacc, touched, icall, srcb,
       srcl, rdepb, rdep, dirty, rflag, rowlist, rsrc, kern, dm, cmask, kmb, kml, icb, icl, dlist, gdirty,
-      kdirty, misc, warps;
+      kdirty, misc, warps, scr;
   int mw;                       // dependency-mask words per func (0 = incremental resolve off)
   int warp_bytes, total;
   int rcap, pcap, S, R;

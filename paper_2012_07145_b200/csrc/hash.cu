@@ -91,12 +91,33 @@ __device__ const char* kind_repr(int k) {
   }
 }
 
+// Does candidate c hash like candidate c-1?  The canonical tuple reads only
+// (func, kind, consumer, serial is not None, thread is not None) of every
+// decision (loopnest.py:151-165), so equal fields => equal bytes => equal
+// hash at every depth.  Beam-step siblings differ only in tilings.
+__device__ __forceinline__ bool same_structure(const GsDecision* a, const GsDecision* b, int S) {
+  for (int i = 0; i < S; ++i) {
+    const uint2 x = *reinterpret_cast<const uint2*>(a + i);
+    const uint2 y = *reinterpret_cast<const uint2*>(b + i);
+    // bytes 0-3 func/consumer, byte 4 kind, byte 5 flags (low two bits)
+    if (x.x != y.x || ((x.y ^ y.y) & 0x0003FFu) != 0u) return false;
+    if ((x.x & 0xFFFFu) == 0xFFFFu) return true;   // both logs ended here
+  }
+  return true;
+}
+
 __global__ void hash_kernel(const GsDecision* __restrict__ dec, int64_t n, int S, int nf, int depth,
                             const int32_t* __restrict__ sorted_funcs, const uint8_t* __restrict__ names,
-                            const int32_t* __restrict__ name_off, uint64_t* __restrict__ out) {
+                            const int32_t* __restrict__ name_off, uint64_t* __restrict__ out,
+                            uint8_t* __restrict__ head) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   const GsDecision* d = dec + c * S;
+  if (head) {
+    const bool h = c == 0 || !same_structure(d, d - S, S);
+    head[c] = h;
+    if (!h) return;
+  }
   int16_t didx[kHashMaxFuncs];
   for (int f = 0; f < nf; ++f) didx[f] = -1;
   int nd = 0;
@@ -158,13 +179,27 @@ __global__ void hash_kernel(const GsDecision* __restrict__ dec, int64_t n, int S
   out[c] = b.final();
 }
 
+// non-head candidates copy the hash of the head of their run
+__global__ void hash_fill_kernel(const uint8_t* __restrict__ head, int64_t n, uint64_t* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n || head[c]) return;
+  int64_t j = c - 1;
+  while (!head[j]) --j;
+  out[c] = out[j];
+}
+
 int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, const int32_t* sorted_funcs,
-                const uint8_t* names, const int32_t* name_off, uint64_t* out, cudaStream_t st) {
+                const uint8_t* names, const int32_t* name_off, uint64_t* out, uint8_t* head, cudaStream_t st) {
   if (n == 0) return 0;
   if (nf > kHashMaxFuncs) return -1;
   if (depth > 3) depth = 3;
   int64_t blocks = (n + 127) / 128;
-  hash_kernel<<<(unsigned)blocks, 128, 0, st>>>(dec, n, S, nf, depth, sorted_funcs, names, name_off, out); g_launch_count++;
+  hash_kernel<<<(unsigned)blocks, 128, 0, st>>>(dec, n, S, nf, depth, sorted_funcs, names, name_off, out, head);
+  g_launch_count++;
+  if (head) {
+    hash_fill_kernel<<<(unsigned)blocks, 128, 0, st>>>(head, n, out);
+    g_launch_count++;
+  }
   return 0;
 }
 

@@ -119,23 +119,37 @@ class Scorer:
         """K1 work counters since the last call (see gs_stats)."""
         out = np.zeros(6, dtype=np.int64)
         _lib.check(self.lib.gs_stats(self.handle, C.c_void_p(out.ctypes.data), _stream()))
-        return dict(zip(("candidates", "incremental", "rows_computed", "rows", "geometries", "reserved"),
-                        out.tolist()))
+        d = dict(zip(("candidates", "incremental", "rows_computed", "rows", "geometries"), out[:5].tolist()))
+        d["k1_warps"], d["k1_slice_bytes"] = int(out[5]) >> 32, int(out[5]) & 0xFFFFFFFF
+        return d
 
     def check(self):
         """Synchronize and raise on any device-side capacity / schedule error."""
         _lib.check(self.lib.gs_check(self.handle, _stream()))
 
     # -- K2 -------------------------------------------------------------------
-    def cost(self, f, rows=False, basis=False, total=None):
+    def cost(self, f, rows=False, basis=False, total=None, reuse=None, scratch=None):
+        """Totals (and optionally per-row costs / basis) of a featurized batch.
+
+        reuse (default: when `f` carries K1's row_src and no basis is asked
+        for) evaluates the network once per distinct row; `scratch` is an
+        optional preallocated [N, R] fp64 row-cost buffer for that mode."""
         n = f["feats"].shape[0]
         if total is None:
             total = torch.empty((n,), dtype=torch.float64, device=self.device)
-        rc = torch.empty((n, self.R), dtype=torch.float64, device=self.device) if rows else None
+        src = f.get("row_src")
+        if reuse is None:
+            reuse = src is not None and not basis
+        if not reuse:
+            src = None
+        rc = None
+        if rows or src is not None:
+            rc = scratch if scratch is not None else torch.empty((n, self.R), dtype=torch.float64,
+                                                                 device=self.device)
         gh = torch.empty((n, self.R, 31), dtype=torch.float64, device=self.device) if basis else None
-        _lib.check(self.lib.gs_cost(self.handle, _ptr(f["feats"]), _ptr(f["row_key"]),
-                                    _ptr(f["n_rows"]), n, _ptr(total), _ptr(rc), _ptr(gh), _stream()))
-        return total, rc, gh
+        _lib.check(self.lib.gs_cost(self.handle, _ptr(f["feats"]), _ptr(f["row_key"]), _ptr(f["n_rows"]),
+                                    _ptr(src), n, _ptr(total), _ptr(rc), _ptr(gh), _stream()))
+        return total, (rc if rows else None), gh
 
     # -- K3 -------------------------------------------------------------------
     def struct_hash(self, dec: torch.Tensor, depth: int, out=None):

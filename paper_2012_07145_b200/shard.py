@@ -28,14 +28,16 @@ class StepPlan:
         self.pass_index, self.phase_seed, self.beam = pass_index, phase_seed, beam
         self.penalty, self.num_passes, self.tie_band = penalty, num_passes, tie_band
         self.fbuf = None
+        self.rcbuf = None
         self.local_count = n
 
     def _features(self, d):
         m = d.shape[0]
         if self.fbuf is None or self.fbuf["feats"].shape[0] != m:
-            self.fbuf = None
+            self.fbuf = self.rcbuf = None
             torch.cuda.empty_cache()
             self.fbuf = self.sc.featurize(d)
+            self.rcbuf = torch.empty((m, self.sc.R), dtype=torch.float64, device=self.sc.device)
         else:
             self.sc.featurize(d, out=self.fbuf)
         return self.fbuf
@@ -56,7 +58,7 @@ class StepPlan:
         f = self._features(d)
         if k1_times is not None:
             b.record()
-        total, _, _ = sc.cost(f)
+        total, _, _ = sc.cost(f, scratch=self.rcbuf)
         rep, _, cnt = sc.select(hl, f["verdict"], self.phase_seed, rejects=False)
         nrep = int(cnt[0].item())
         rep = rep[:nrep]

@@ -43,7 +43,9 @@ def _run(sc, recs, reuse):
     dec = sc.to_device(recs)
     f = sc.featurize(dec)
     total, _, _ = sc.cost(f)
+    full, _, _ = sc.cost(f, reuse=False)
     sc.check()
+    assert torch.equal(total, full), "row-reuse K2 differs from the full network pass"
     return {k: v.cpu().numpy() for k, v in f.items()}, total.cpu().numpy()
 
 
@@ -75,6 +77,18 @@ def test_reuse_is_bit_exact(src, dev):
         assert np.array_equal(on["feats"][i, :r], off["feats"][i, :r]), (src, i)
         assert np.array_equal(on["row_key"][i, :r], off["row_key"][i, :r])
     assert np.array_equal(t_on, t_off)
+    # K3 run-head reuse: every sibling hashes like a per-candidate hash
+    sc.set_reuse(True)
+    d = sc.to_device(recs)
+    from oracle import structure
+    info0 = gen.GraphInfo(graph)
+    for depth in (0, 1, 2, 3):
+        hs = sc.struct_hash(d, depth).cpu().numpy().view(np.uint64)
+        for i in range(0, len(recs), max(1, len(recs) // 7)):
+            assert int(hs[i]) == structure.structural_hash(_decisions(info0, recs[i]), depth), (src, depth, i)
+        one = np.array([sc.struct_hash(d[i:i + 1], depth).cpu().numpy().view(np.uint64)[0]
+                        for i in range(0, len(recs), max(1, len(recs) // 7))])
+        assert np.array_equal(one, hs[::max(1, len(recs) // 7)])
     # oracle on a strided subsample (siblings of different parents)
     from oracle import features
     info = gen.GraphInfo(graph)

@@ -29,6 +29,6 @@ for name, fn in (("K1", lambda: sc.featurize(dec, out=f)), ("K2", lambda: sc.cos
     torch.cuda.synchronize()
     print(f"{name}: {a.elapsed_time(b) / 3:.2f} ms for {recs.shape[0]} candidates")
 st = sc.stats()
-print({k: v / 3 for k, v in st.items()})
+print({k: (v / 3 if k.startswith(("cand", "incr", "rows", "geo")) else v) for k, v in st.items()})
 print("rows computed per candidate:", st["rows_computed"] / max(1, st["candidates"]),
       "geometries per candidate:", st["geometries"] / max(1, st["candidates"]))
