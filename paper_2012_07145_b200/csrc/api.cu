@@ -7,10 +7,12 @@
 #include <algorithm>
 
 namespace gs {
-Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rcap, int pcap, int nwarps);
+Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rcap, int pcap, int nwarps,
+                   bool spill);
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
-                     const Layout& L, int nwarps, int grid, int* gerr, int reuse, cudaStream_t st);
+                     const Layout& L, int nwarps, int grid, int* gerr, int reuse, uint8_t* gscratch,
+                     cudaStream_t st);
 int featurize_warps(const Layout& L1, int max_smem);
 int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st);
 int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
@@ -62,6 +64,8 @@ struct GsPipeline {
   int nwarps = 8;
   int last_warps = 0, last_slice = 0;   // K1 launch shape (diagnostics)
   uint8_t* hscratch = nullptr;   // K3 run-head flags (grow-only)
+  uint8_t* gscratch = nullptr;   // K1 spilled structure arrays (grow-only)
+  int64_t gcap = 0;
   int64_t hcap = 0;
 };
 
@@ -133,7 +137,7 @@ int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
     }
     long long bound = 0;
     for (int a = 0; a < h.na; ++a) bound += Q[d->access[a].consumer];
-    p->rcap = (int)std::min<long long>(4096, bound + 32);
+    p->rcap = (int)std::min<long long>(32767, bound + 32);   // int16 read indices
     p->pcap = (int)std::min<long long>(65535, bound + 32);
   }
   cudaDeviceProp prop;
@@ -174,7 +178,7 @@ int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
 int gs_pipeline_destroy(gs_pipeline_t p) {
   if (!p) return GS_OK;
   cudaFree(p->dev); cudaFree(p->blob); cudaFree(p->stage_of_func); cudaFree(p->algo); cudaFree(p->sorted);
-  cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err); cudaFree(p->hscratch);
+  cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err); cudaFree(p->hscratch); cudaFree(p->gscratch);
   for (double* b : p->wbufs) cudaFree(b);
   delete p;
   return GS_OK;
@@ -206,9 +210,9 @@ int gs_set_weights(gs_pipeline_t p, int E, int H, const double* aw, const double
   return GS_OK;
 }
 
-static Layout layout_for(gs_pipeline_t p, int S, int nwarps) {
+static Layout layout_for(gs_pipeline_t p, int S, int nwarps, bool spill) {
   return make_layout(p->host.nd, p->host.nf, p->host.ns, p->host.blob_bytes, S, std::max(1, p->host.max_rows),
-                     p->rcap, p->pcap, nwarps);
+                     p->rcap, p->pcap, nwarps, spill);
 }
 
 int gs_set_reuse(gs_pipeline_t p, int enable) {
@@ -221,18 +225,36 @@ int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, doubl
                  int32_t* n_rows, uint8_t* verdict, int32_t* row_src, void* stream) {
   if (!p || S < 1 || n < 0) return fail(GS_ERR_ARG, "bad featurize arguments");
   if (n == 0) return GS_OK;
-  // one CTA per SM, as many independent scorer warps as shared memory holds
-  const int nwarps = std::min(p->nwarps, featurize_warps(layout_for(p, S, 1), p->max_smem));
+  // one CTA per SM, as many independent scorer warps as shared memory
+  // holds; pipelines whose worst-case inline expansion would leave fewer
+  // than 4 warps keep the capacity-sized arrays in global scratch instead
+  bool spill = false;
+  int nwarps = std::min(p->nwarps, featurize_warps(layout_for(p, S, 1, false), p->max_smem));
+  if (nwarps < 4) {
+    spill = true;
+    nwarps = std::min(p->nwarps, featurize_warps(layout_for(p, S, 1, true), p->max_smem));
+  }
   if (nwarps < 1)
     return fail(GS_ERR_CAPACITY, "pipeline too large for one warp's shared-memory slice (" +
-                                     std::to_string(layout_for(p, S, 1).total) + " > " +
+                                     std::to_string(layout_for(p, S, 1, true).total) + " > " +
                                      std::to_string(p->max_smem) + " bytes)");
-  Layout L = layout_for(p, S, nwarps);
+  Layout L = layout_for(p, S, nwarps, spill);
   int64_t grid = std::min<int64_t>(p->num_sms, (n + nwarps - 1) / nwarps);
+  if (spill) {
+    const int64_t need = grid * nwarps * (int64_t)L.gl_bytes;
+    if (need > p->gcap) {   // grow-only global scratch
+      CK(cudaStreamSynchronize((cudaStream_t)stream));
+      if (p->gscratch) CK(cudaFree(p->gscratch));
+      p->gscratch = nullptr;
+      p->gcap = 0;
+      CK(cudaMalloc(&p->gscratch, (size_t)need));
+      p->gcap = need;
+    }
+  }
   p->last_warps = nwarps;
   p->last_slice = L.warp_bytes;
   int rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, nwarps,
-                            (int)grid, p->err, p->reuse, (cudaStream_t)stream);
+                            (int)grid, p->err, p->reuse, spill ? p->gscratch : nullptr, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "unsupported ndim");
   CK(cudaGetLastError());
   return GS_OK;

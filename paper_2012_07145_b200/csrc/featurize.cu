@@ -739,11 +739,65 @@ __device__ int footprint(const GsAccess* A, const int16_t* p, int plen, int d, i
   return n;
 }
 
+// Closed-form footprint of [a,b] through the links of dim d as an
+// arithmetic progression of disjoint, non-adjacent intervals
+// {start + i*step + [0, len-1] : i < cnt} (cnt == 1: one interval): a
+// link x -> [x*s + lo, x*s + hi] maps an interval to an interval when s is
+// at most the window width, else to a progression; a progression of
+// intervals maps to a progression (merging into one interval when the
+// images touch) unless both levels spread (returns false: expand).
+// points = cnt*len, dim-0 runs = cnt (boxes.py:92-138 for one product).
+__device__ bool footprint_ap(const GsAccess* A, const int16_t* p, int plen, int d, int64_t a, int64_t b,
+                             int64_t& pts, int64_t& runs) {
+  int64_t st = a, step = 1, len = b - a + 1, cnt = 1;
+  if (len <= 0) { pts = runs = 0; return true; }
+  for (int k = 0; k < plen; ++k) {
+    const GsAccess& x = A[p[k]];
+    const int64_t s = x.s[d], wl = x.lo[d], w = (int64_t)x.hi[d] - x.lo[d] + 1;
+    if (cnt == 1) {
+      if (s <= w) { st = st * s + wl; len = (len - 1) * s + w; }
+      else { cnt = len; st = st * s + wl; step = s; len = w; }
+    } else if (s <= w) {
+      const int64_t nl = (len - 1) * s + w, ns = step * s, n0 = st * s + wl;
+      if (ns <= nl) { st = n0; len = (cnt - 1) * ns + nl; cnt = 1; step = 1; }
+      else { st = n0; step = ns; len = nl; }
+    } else if (len == 1) {
+      const int64_t ns = step * s, n0 = st * s + wl;
+      if (ns <= w) { st = n0; len = (cnt - 1) * ns + w; cnt = 1; step = 1; }
+      else { st = n0; step = ns; len = w; }
+    } else {
+      return false;
+    }
+  }
+  pts = cnt * len;
+  runs = cnt;
+  return true;
+}
+
 template <int ND>
 __device__ void union_count(const GsAccess* A, const RRead* rd, const int16_t* paths,
                             const int16_t* rl, const int8_t* grp, int nr, int g,
                             const int32_t* blo, const int32_t* bhi,
                             int64_t& vol, int64_t& lines, int& err) {
+  {   // a group of one read: closed form per dim, no interval lists
+    int K1 = 0, only = -1;
+    for (int q = 0; q < nr; ++q) if (grp[q] == g) { ++K1; only = q; }
+    if (K1 == 1) {
+      const RRead& r = rd[rl[only]];
+      int64_t pv[ND], rv[ND];
+      bool ok = true;
+#pragma unroll
+      for (int d = 0; d < ND; ++d) ok = ok && footprint_ap(A, paths + r.pbeg, r.plen, d, blo[d], bhi[d], pv[d], rv[d]);
+      if (ok) {
+        int64_t outer = 1;
+#pragma unroll
+        for (int d = 1; d < ND; ++d) outer *= pv[d];
+        vol = pv[0] * outer;
+        lines = rv[0] * outer;
+        return;
+      }
+    }
+  }
   Iv buf[kLaneIv];
   int16_t off[kGroupReads][ND], cnt[kGroupReads][ND];
   int K = 0, used = 0;
@@ -1412,12 +1466,16 @@ __global__ void __launch_bounds__(kK1MaxWarps * 32, 1)
 featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob, const GsDecision* __restrict__ dec,
                  int64_t n, int S, double* __restrict__ feats, int32_t* __restrict__ row_key,
                  int32_t* __restrict__ n_rows, uint8_t* __restrict__ verdict, int32_t* __restrict__ row_src,
-                 Layout L, int* gerr, int reuse) {
+                 Layout L, int* gerr, int reuse, uint8_t* __restrict__ gscratch) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar;
   const int warp = threadIdx.x >> 5, lane = lane_id(), nw = blockDim.x >> 5;
   if (threadIdx.x == 0) bulk_stage(sm + L.blob, blob, P->blob_bytes, &bar);
   uint8_t* ws = sm + L.warps + (size_t)warp * L.warp_bytes;   // this warp's slice
+  // capacity-sized structure arrays live in the slice, or — for pipelines
+  // whose worst-case inline expansion does not fit shared memory — in this
+  // warp's slice of a global scratch (generic pointers: same code)
+  uint8_t* wg = L.gl_bytes ? gscratch + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * L.gl_bytes : ws;
   K1<ND> k;
   k.P = P;
   k.F = reinterpret_cast<const GsFunc*>(sm + L.blob);
@@ -1427,19 +1485,19 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   k.pdec = reinterpret_cast<GsDecision*>(ws + L.pdec);
   k.didx = reinterpret_cast<int16_t*>(ws + L.didx);
   k.cf = reinterpret_cast<CF<ND>*>(ws + L.cf);
-  k.rd = reinterpret_cast<RRead*>(ws + L.reads);
-  k.path = reinterpret_cast<int16_t*>(ws + L.paths);
+  k.rd = reinterpret_cast<RRead*>(wg + L.reads);
+  k.path = reinterpret_cast<int16_t*>(wg + L.paths);
   k.rdb = reinterpret_cast<int32_t*>(ws + L.rdb);
   k.frd = reinterpret_cast<int32_t*>(ws + L.frd);
   k.rows = reinterpret_cast<int32_t*>(ws + L.rows);
   k.stack = reinterpret_cast<Frame*>(ws + L.stack);
   k.volacc = reinterpret_cast<int64_t*>(ws + L.volacc);
   k.touched = reinterpret_cast<int16_t*>(ws + L.touched);
-  k.icall = reinterpret_cast<ICall*>(ws + L.icall);
+  k.icall = reinterpret_cast<ICall*>(wg + L.icall);
   k.srcb = reinterpret_cast<int32_t*>(ws + L.srcb);
-  k.srcl = reinterpret_cast<int16_t*>(ws + L.srcl);
+  k.srcl = reinterpret_cast<int16_t*>(wg + L.srcl);
   k.rdepb = reinterpret_cast<int32_t*>(ws + L.rdepb);
-  k.rdep = reinterpret_cast<int16_t*>(ws + L.rdep);
+  k.rdep = reinterpret_cast<int16_t*>(wg + L.rdep);
   k.dirty = reinterpret_cast<uint8_t*>(ws + L.dirty);
   k.rowlist = reinterpret_cast<int16_t*>(ws + L.rowlist);
   k.kern = reinterpret_cast<int16_t*>(ws + L.kern);
@@ -1448,7 +1506,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   k.kmb = reinterpret_cast<int32_t*>(ws + L.kmb);
   k.kml = reinterpret_cast<int16_t*>(ws + L.kml);
   k.icb = reinterpret_cast<int32_t*>(ws + L.icb);
-  k.icl = reinterpret_cast<int16_t*>(ws + L.icl);
+  k.icl = reinterpret_cast<int16_t*>(wg + L.icl);
   k.dlist = reinterpret_cast<int16_t*>(ws + L.dlist);
   k.gdirty = reinterpret_cast<uint8_t*>(ws + L.gdirty);
   k.kdirty = reinterpret_cast<uint8_t*>(ws + L.kdirty);
@@ -1584,28 +1642,32 @@ static int cf_size() { return (int)sizeof(CF<ND>); }
 // offsets inside a slice are relative to the slice.  The structure-build
 // scratch (DFS stack, volume accumulators, touched list) aliases the row
 // scratch: they are never live at the same time.
-Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rcap, int pcap, int nwarps) {
+Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rcap, int pcap, int nwarps,
+                   bool spill) {
   auto al = [](int x) { return (x + 15) & ~15; };
   Layout L{};
   L.blob = 0;
   L.warps = al(blob_bytes);
   int o = 0;
+  int g = 0;   // global scratch bytes per warp (spill)
+  // capacity-sized arrays: in the smem slice, or in global scratch
+  auto place = [&](int bytes) { int r; if (spill) { r = g; g += al(bytes); } else { r = o; o += al(bytes); } return r; };
   L.dec = o; o += al(S * 16);
   L.pdec = o; o += al(S * 16);
   L.didx = o; o += al(nf * 2);
   int cfs = nd == 1 ? cf_size<1>() : nd == 2 ? cf_size<2>() : nd == 3 ? cf_size<3>() : cf_size<4>();
   L.cf = o; o += al(nf * cfs);
   L.pcf = 0;
-  L.reads = o; o += al(rcap * (int)sizeof(RRead));
-  L.paths = o; o += al(pcap * 2);
+  L.reads = place(rcap * (int)sizeof(RRead));
+  L.paths = place(pcap * 2);
   L.rdb = o; o += al(2 * ns * 4);
   L.frd = o; o += al(nf * 4);
   L.rows = o; o += al(R * 4);
-  L.icall = o; o += al(pcap * (int)sizeof(ICall));
+  L.icall = place(pcap * (int)sizeof(ICall));
   L.srcb = o; o += al((nf + 1) * 4);
-  L.srcl = o; o += al(rcap * 2);
+  L.srcl = place(rcap * 2);
   L.rdepb = o; o += al((R + 1) * 4);
-  L.rdep = o; o += al((rcap + nf) * 2);
+  L.rdep = place((rcap + nf) * 2);
   L.dirty = o; o += al(nf);
   L.rflag = o; o += al(R);
   L.rowlist = o; o += al(R * 2);
@@ -1617,7 +1679,7 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   L.kmb = o; o += al((nf + 1) * 4);
   L.kml = o; o += al(nf * 2);
   L.icb = o; o += al((nf + 1) * 4);
-  L.icl = o; o += al(pcap * 2);
+  L.icl = place(pcap * 2);
   L.dlist = o; o += al(nf * 2);
   L.gdirty = o; o += al(nf);
   L.kdirty = o; o += al(nf);
@@ -1631,6 +1693,7 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   const int scr = al((int)sizeof(WarpScr)) > sa ? al((int)sizeof(WarpScr)) : sa;
   o += scr;
   L.warp_bytes = al(o);
+  L.gl_bytes = g;
   L.total = L.warps + nwarps * L.warp_bytes;
   L.rcap = rcap; L.pcap = pcap; L.S = S; L.R = R;
   return L;
@@ -1644,14 +1707,14 @@ int featurize_warps(const Layout& L1, int max_smem) {
 
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
-                     const Layout& L,
-                     int nwarps, int grid, int* gerr, int reuse, cudaStream_t st) {
+                     const Layout& L, int nwarps, int grid, int* gerr, int reuse, uint8_t* gscratch,
+                     cudaStream_t st) {
   dim3 b(nwarps * 32);
   switch (nd) {
 #define GS_CASE(D)                                                                                  \
   case D:                                                                                           \
     cudaFuncSetAttribute(featurize_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total); \
-    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, gerr, reuse); \
+    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, gerr, reuse, gscratch); \
     g_launch_count++;                                                                               \
     break;
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4)

@@ -72,6 +72,7 @@ struct Layout {                 // byte offsets inside dynamic shared memory (K1
       srcl, rdepb, rdep, dirty, rflag, rowlist, rsrc, kern, dm, cmask, kmb, kml, icb, icl, dlist, gdirty,
       kdirty, misc, warps, scr;
   int mw;                       // dependency-mask words per func (0 = incremental resolve off)
+  int gl_bytes;                 // per-warp global scratch (capacity-sized arrays spilled), 0 = none
   int warp_bytes, total;
   int rcap, pcap, S, R;
 };

@@ -73,9 +73,9 @@ def graphs():
         "chain20": (parse_pipeline(make_chain_src(20, extent=512), "chain20"), 12, DEFAULT_THRESHOLDS),
         "chain100": (parse_pipeline(make_chain_src(100, extent=1024), "chain100"), 6, DEFAULT_THRESHOLDS),
     }
-    for name in ("unsharp", "harris", "resnet_block", "camera_pipe", "local_laplacian"):
+    for name in ("unsharp", "harris", "resnet_small", "camera_pipe", "local_laplacian"):
         if os.path.exists(os.path.join(PIPE_DIR, f"{name}.txt")):
-            n = 16 if name in ("unsharp", "harris", "resnet_block") else 4
+            n = 16 if name in ("unsharp", "harris", "resnet_small") else 4
             out[name] = (authored(name), n, DEFAULT_THRESHOLDS)
     return out
 
@@ -182,8 +182,19 @@ def main():
     save_weights(w0, os.path.join(HERE, "weights_seed0.txt"))
     w1 = init_weights(seed=3, embed_dim=16, hidden_dim=48)
     save_weights(w1, os.path.join(HERE, "weights_small.txt"))
+    if "--c3" in sys.argv:   # C3: full search with the freeze pre-pass on a ~100-func pipeline
+        for tag in [a for a in sys.argv[1:] if not a.startswith("-")] or ["camera_pipe"]:
+            print("s", tag, record_search(f"{tag}_freeze", authored(tag),
+                                          SearchConfig(beam_size=2, num_passes=1, seed=0, freeze_enabled=True),
+                                          params, w0, freeze=True), flush=True)
+        return
+    only = [a for a in sys.argv[1:] if not a.startswith("-")]
     for name, (graph, n, th) in graphs().items():
+        if only and name not in only:
+            continue
         print(name, record_candidates(name, graph, n, th, params, w0), flush=True)
+    if only:
+        return
     small = TilingConfig(serial_powers=(1, 2), odd_serial=(), innermost_thread=(16, 32),
                          outer_thread=(1, 4), unroll_budget=64)
     print("s chain2", record_search("chain2", parse_pipeline(CHAIN2_SRC, "chain2"),

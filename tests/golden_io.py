@@ -17,7 +17,7 @@ from paper_2012_07145_b200.schedule import parse_dump
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 CANDIDATE_SETS = ("chain2", "chain3", "diamond", "self_read", "strided", "tiny_fork",
                   "blur", "conv", "stencil_chain", "chain20", "chain100")
-AUTHORED = ("unsharp", "harris", "resnet_block", "camera_pipe", "local_laplacian")
+AUTHORED = ("unsharp", "harris", "resnet_small", "camera_pipe", "local_laplacian")
 SEARCHES = ("chain2", "diamond", "diamond_T", "stencil_chain", "chain16_freeze")
 
 
@@ -80,3 +80,29 @@ def weights(which="seed0"):
 
 
 PARAMS = MachineParams()
+
+
+def decisions_from_records(info, rec):
+    """Packed GsDecision records of one candidate -> reference-style
+    ((func, Decision), ...) tuple (for the oracle)."""
+    from paper_2012_07145_b200.descriptor import KIND_NAME
+    from paper_2012_07145_b200.schedule import Decision
+    out = []
+    for r in rec:
+        if r["func"] == 0xFFFF:
+            break
+        nd = len(info.extents[int(r["func"])])
+        out.append((info.names[int(r["func"])], Decision(
+            KIND_NAME[int(r["kind"])],
+            None if r["consumer"] == 0xFFFF else info.names[int(r["consumer"])],
+            tuple(int(x) for x in r["serial"][:nd]) if r["flags"] & 1 else None,
+            tuple(int(x) for x in r["thread"][:nd]) if r["flags"] & 2 else None)))
+    return tuple(out)
+
+
+def search_tags():
+    """Traced searches present under tests/golden (SEARCHES + C3 freeze traces)."""
+    import glob
+    tags = [os.path.basename(p)[len("search_"):-len(".json.gz")]
+            for p in glob.glob(os.path.join(GOLDEN, "search_*.json.gz"))]
+    return sorted(tags)

@@ -10,7 +10,7 @@ import pytest
 
 torch = pytest.importorskip("torch")
 
-from golden_io import PARAMS, SEARCHES, search_trace, weights  # noqa: E402
+from golden_io import PARAMS, search_tags, search_trace, weights  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -24,7 +24,7 @@ def dev():
     return torch.device("cuda")
 
 
-@pytest.mark.parametrize("tag", SEARCHES)
+@pytest.mark.parametrize("tag", search_tags())
 def test_cut_replay_bit_exact(tag, dev):
     from paper_2012_07145_b200.cut import beam_cut
     from paper_2012_07145_b200.engine import Scorer
