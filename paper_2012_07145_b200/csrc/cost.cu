@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(128) cost_kernel(NetDev net, const int32_t* __
 // network runs once per distinct row.  Pass A compacts the computed rows of
 // a chunk in shared memory (full warps run the network), pass B gathers
 // every row's cost from its source and adds a candidate's rows in order.
-constexpr int kChunk = 1024;
+constexpr int kChunk = 8192;
 
 template <int MAXE>
 __global__ void __launch_bounds__(128) cost_rows_kernel(NetDev net, const int32_t* __restrict__ stage_of_func,

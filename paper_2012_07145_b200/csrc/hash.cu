@@ -12,52 +12,66 @@ constexpr int kHashMaxFuncs = 1024;
 __constant__ uint64_t kIV[8] = {0x6a09e667f3bcc908ULL, 0xbb67ae8584caa73bULL, 0x3c6ef372fe94f82bULL,
                                 0xa54ff53a5f1d36f1ULL, 0x510e527fade682d1ULL, 0x9b05688c2b3e6c1fULL,
                                 0x1f83d9abfb41bd6bULL, 0x5be0cd19137e2179ULL};
-__constant__ uint8_t kSigma[12][16] = {
-    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
-    {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4}, {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
-    {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13}, {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
-    {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11}, {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
-    {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5}, {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
-    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
 
 __device__ __forceinline__ uint64_t rotr(uint64_t x, int n) { return (x >> n) | (x << (64 - n)); }
 
+// blake2b-64, unkeyed.  The current 128-byte block is staged in this
+// thread's shared-memory slot (byte appends are plain st.shared.u8); the
+// 12 rounds are fully unrolled with compile-time message schedules, so the
+// message words and the state stay in registers.
+template <int R>
+__device__ __forceinline__ void blake_round(uint64_t* v, const uint64_t* m) {
+  constexpr uint8_t S[12][16] = {
+      {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+      {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4}, {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+      {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13}, {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+      {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11}, {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+      {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5}, {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
+      {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
+#define G(a, b, c, d, x, y)                     \
+  v[a] = v[a] + v[b] + m[S[R][x]];              \
+  v[d] = rotr(v[d] ^ v[a], 32);                 \
+  v[c] = v[c] + v[d];                           \
+  v[b] = rotr(v[b] ^ v[c], 24);                 \
+  v[a] = v[a] + v[b] + m[S[R][y]];              \
+  v[d] = rotr(v[d] ^ v[a], 16);                 \
+  v[c] = v[c] + v[d];                           \
+  v[b] = rotr(v[b] ^ v[c], 63);
+  G(0, 4, 8, 12, 0, 1) G(1, 5, 9, 13, 2, 3) G(2, 6, 10, 14, 4, 5) G(3, 7, 11, 15, 6, 7)
+  G(0, 5, 10, 15, 8, 9) G(1, 6, 11, 12, 10, 11) G(2, 7, 8, 13, 12, 13) G(3, 4, 9, 14, 14, 15)
+#undef G
+}
+
 struct Blake {
   uint64_t h[8];
-  uint64_t m[16];   // current block (little-endian words)
+  uint8_t* blk;     // this thread's 128-byte block in shared memory
   uint64_t t;       // bytes compressed so far
   int fill;         // bytes in the current block
 
-  __device__ void init() {
+  __device__ void init(uint8_t* block) {
+    blk = block;
 #pragma unroll
     for (int i = 0; i < 8; ++i) h[i] = kIV[i];
     h[0] ^= 0x01010000ULL ^ 8ULL;   // digest 8 bytes, no key
     t = 0; fill = 0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) m[i] = 0;
   }
   __device__ void compress(bool last) {
-    uint64_t v[16];
+    uint64_t m[16], v[16];
+    for (int i = fill; i < 128; ++i) blk[i] = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      uint64_t w = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) w |= (uint64_t)blk[8 * i + b] << (8 * b);
+      m[i] = w;
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) { v[i] = h[i]; v[i + 8] = kIV[i]; }
     v[12] ^= t;
     if (last) v[14] = ~v[14];
-#pragma unroll
-    for (int r = 0; r < 12; ++r) {
-      const uint8_t* s = kSigma[r];
-#define G(a, b, c, d, x, y)                      \
-  v[a] = v[a] + v[b] + m[s[x]];                  \
-  v[d] = rotr(v[d] ^ v[a], 32);                  \
-  v[c] = v[c] + v[d];                            \
-  v[b] = rotr(v[b] ^ v[c], 24);                  \
-  v[a] = v[a] + v[b] + m[s[y]];                  \
-  v[d] = rotr(v[d] ^ v[a], 16);                  \
-  v[c] = v[c] + v[d];                            \
-  v[b] = rotr(v[b] ^ v[c], 63);
-      G(0, 4, 8, 12, 0, 1) G(1, 5, 9, 13, 2, 3) G(2, 6, 10, 14, 4, 5) G(3, 7, 11, 15, 6, 7)
-      G(0, 5, 10, 15, 8, 9) G(1, 6, 11, 12, 10, 11) G(2, 7, 8, 13, 12, 13) G(3, 4, 9, 14, 14, 15)
-#undef G
-    }
+    blake_round<0>(v, m); blake_round<1>(v, m); blake_round<2>(v, m); blake_round<3>(v, m);
+    blake_round<4>(v, m); blake_round<5>(v, m); blake_round<6>(v, m); blake_round<7>(v, m);
+    blake_round<8>(v, m); blake_round<9>(v, m); blake_round<10>(v, m); blake_round<11>(v, m);
 #pragma unroll
     for (int i = 0; i < 8; ++i) h[i] ^= v[i] ^ v[i + 8];
   }
@@ -65,13 +79,9 @@ struct Blake {
     if (fill == 128) {
       t += 128;
       compress(false);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) m[i] = 0;
       fill = 0;
     }
-    // dynamic index into m: keep it in local memory-friendly form
-    m[fill >> 3] |= (uint64_t)b << ((fill & 7) * 8);
-    ++fill;
+    blk[fill++] = b;
   }
   __device__ void str(const char* s) { while (*s) byte((uint8_t)*s++); }
   __device__ void bytes(const uint8_t* p, int n) { for (int i = 0; i < n; ++i) byte(p[i]); }
@@ -95,35 +105,40 @@ __device__ const char* kind_repr(int k) {
 // (func, kind, consumer, serial is not None, thread is not None) of every
 // decision (loopnest.py:151-165), so equal fields => equal bytes => equal
 // hash at every depth.  Beam-step siblings differ only in tilings.
-__device__ __forceinline__ bool same_structure(const GsDecision* a, const GsDecision* b, int S) {
-  for (int i = 0; i < S; ++i) {
-    const uint2 x = *reinterpret_cast<const uint2*>(a + i);
-    const uint2 y = *reinterpret_cast<const uint2*>(b + i);
-    // bytes 0-3 func/consumer, byte 4 kind, byte 5 flags (low two bits)
-    if (x.x != y.x || ((x.y ^ y.y) & 0x0003FFu) != 0u) return false;
-    if ((x.x & 0xFFFFu) == 0xFFFFu) return true;   // both logs ended here
+// run heads, one warp per candidate: coalesced 8-byte loads of the two
+// logs, one ballot per 32 records
+__global__ void hash_head_kernel(const GsDecision* __restrict__ dec, int64_t n, int S,
+                                 uint8_t* __restrict__ head) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= n) return;
+  if (c == 0) { if (lane == 0) head[0] = 1; return; }
+  const uint2* a = reinterpret_cast<const uint2*>(dec + c * S);
+  const uint2* b = reinterpret_cast<const uint2*>(dec + (c - 1) * S);
+  bool diff = false;
+  for (int i = lane; i < S; i += 32) {
+    const uint2 x = __ldg(a + 2 * i), y = __ldg(b + 2 * i);   // first 8 bytes of record i
+    diff |= x.x != y.x || ((x.y ^ y.y) & 0x0003FFu) != 0u;
   }
-  return true;
+  diff = __any_sync(0xffffffffu, diff);
+  if (lane == 0) head[c] = diff;
 }
 
 __global__ void hash_kernel(const GsDecision* __restrict__ dec, int64_t n, int S, int nf, int depth,
                             const int32_t* __restrict__ sorted_funcs, const uint8_t* __restrict__ names,
                             const int32_t* __restrict__ name_off, uint64_t* __restrict__ out,
-                            uint8_t* __restrict__ head) {
+                            const uint8_t* __restrict__ head) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
+  if (head && !head[c]) return;
+  __shared__ uint8_t blocks[128 * 128];
   const GsDecision* d = dec + c * S;
-  if (head) {
-    const bool h = c == 0 || !same_structure(d, d - S, S);
-    head[c] = h;
-    if (!h) return;
-  }
   int16_t didx[kHashMaxFuncs];
   for (int f = 0; f < nf; ++f) didx[f] = -1;
   int nd = 0;
   for (int i = 0; i < S && d[i].func != 0xFFFF; ++i) { didx[d[i].func] = (int16_t)i; ++nd; }
   Blake b;
-  b.init();
+  b.init(blocks + 128 * threadIdx.x);
   auto name = [&](int f) { b.bytes(names + name_off[f], name_off[f + 1] - name_off[f]); };
   if (depth == 0) {
     b.str("('kernels', (");
@@ -194,6 +209,10 @@ int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, cons
   if (nf > kHashMaxFuncs) return -1;
   if (depth > 3) depth = 3;
   int64_t blocks = (n + 127) / 128;
+  if (head) {
+    hash_head_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(dec, n, S, head);
+    g_launch_count++;
+  }
   hash_kernel<<<(unsigned)blocks, 128, 0, st>>>(dec, n, S, nf, depth, sorted_funcs, names, name_off, out, head);
   g_launch_count++;
   if (head) {

@@ -67,9 +67,8 @@ def beam_cut(scorer, dec: torch.Tensor, pass_index: int, phase_seed: int, flagge
     if nrep > 1:
         bsel = torch.nonzero(bot[:nrep]).flatten()
         bdec = dec.index_select(0, rep.index_select(0, bsel))
-        for depth in range(1, num_passes + 1):
-            hs = as_u64(scorer.struct_hash(bdec, depth))
-            memo_new |= {(depth, int(x)) for x in hs}
+        for depth, hs in enumerate(scorer.memo_hashes(bdec, num_passes), start=1):
+            memo_new |= {(depth, int(x)) for x in as_u64(hs)}
     return CutResult(beam=[int(rep_cpu[p]) for p in pos_cpu],
                      costs=[float(tot_cpu[p]) for p in pos_cpu],
                      rejects=rejects, memo_new=memo_new,

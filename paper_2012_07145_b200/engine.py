@@ -162,6 +162,19 @@ class Scorer:
                                            _ptr(out), _stream()))
         return out
 
+    def memo_hashes(self, dec: torch.Tensor, num_passes: int):
+        """Hashes at depths 1..num_passes (the bad-hash memo, search.py:196-200).
+        The canonical key caps the depth at 3 (loopnest.py:137), so deeper
+        depths reuse the depth-3 hashes."""
+        out, h3 = [], None
+        for depth in range(1, num_passes + 1):
+            if depth >= 3:
+                h3 = self.struct_hash(dec, 3) if h3 is None else h3
+                out.append(h3)
+            else:
+                out.append(self.struct_hash(dec, depth))
+        return out
+
     # -- K4 -------------------------------------------------------------------
     def select(self, hashes: torch.Tensor, verdict: torch.Tensor, phase_seed: int, rejects=True):
         n = hashes.shape[0]

@@ -76,7 +76,7 @@ class StepPlan:
         # bad-hash memo: hashes of the bottom half at every pass depth
         if costs.shape[0] > 1:
             bdec = dec.index_select(0, cand.index_select(0, torch.nonzero(bot).flatten()))
-            memo = [sc.struct_hash(bdec, dpt) for dpt in range(1, self.num_passes + 1)]
+            memo = sc.memo_hashes(bdec, self.num_passes)
         else:
             memo = []
         return {"beam": beam.cpu().tolist(), "total": total, "verdict": f["verdict"], "memo": memo,

@@ -1,14 +1,16 @@
 #!/bin/bash
-# One gpurun call: GPU parity tests, bench line, ncu launch list, ncu full capture of K1.
+# Round measurement: GPU parity tests, full bench line (with the CPU
+# reference timed beside it), ncu launch list, ncu full captures of K1/K2.
 set -x
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/nvsmi.txt 2>&1
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-   --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --parents 1000 > gpurun_out/ncu_launch.log 2>&1
+timeout 1200 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 900 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+   --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:featurize_kernel -s 1 -c 1 \
    -o gpurun_out/prof_k1 -f python tools/prof_k1.py 200 > gpurun_out/ncu_full.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:cost_kernel -s 1 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:cost_rows_kernel -s 1 -c 1 \
    -o gpurun_out/prof_k2 -f python tools/prof_k1.py 200 > gpurun_out/ncu_full_k2.log 2>&1
 exit 0
