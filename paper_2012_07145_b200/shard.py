@@ -108,6 +108,9 @@ def exchange_reps(costs, ph, cand, world, group=None):
     torch.distributed backend (NCCL on the GPU path, gloo in the CPU tests).
     Returns (costs f64, pass hashes i64, candidate indices i64)."""
     import torch.distributed as dist
+    if dist.get_backend(group) == "gloo" and costs.is_cuda:   # gloo gathers host tensors
+        c, p, i = exchange_reps(costs.cpu(), ph.cpu(), cand.cpu(), world, group)
+        return c.to(costs.device), p.to(costs.device), i.to(costs.device)
     nrep = int(costs.shape[0])
     dev = costs.device
     rec = torch.stack([ph, costs.view(torch.int64), cand,

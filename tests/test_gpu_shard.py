@@ -1,0 +1,73 @@
+"""The sharded beam step (shard.StepPlan) on the GPU: two
+ranks on the one device of a gpurun box (gloo carries the representative
+records; on a multi-GPU node the same code runs one rank per GPU over
+NCCL) must cut exactly the beam a single rank cuts, with every rank
+featurizing only its own buckets."""
+
+import os
+import socket
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.multiprocessing as tmp  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+PARENTS = 40
+
+
+def _plan(world, rank):
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2012_07145_b200 import shard
+    from paper_2012_07145_b200.engine import TIE_BAND, Scorer
+    from paper_2012_07145_b200.params import DEFAULT_THRESHOLDS, MachineParams, init_weights
+    graph, recs, _ = bench._workload(PARENTS)
+    sc = Scorer(graph, MachineParams(), DEFAULT_THRESHOLDS, init_weights(0))
+    dec = sc.to_device(recs)
+    plan = shard.StepPlan(sc, len(recs), world, rank, bench.PASS_INDEX, bench.PHASE_SEED, bench.BEAM, 2.0,
+                          bench.NUM_PASSES, TIE_BAND)
+    return plan, dec
+
+
+def _rank(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan, dec = _plan(world, rank)
+        out = plan.run(dec)
+        memo = [sorted(int(x) for x in m.cpu().tolist()) for m in out["memo"]]
+        q.put((rank, out["beam"], plan.local_count, out["n_reps"], memo))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_step_cuts_the_single_rank_beam():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    plan, dec = _plan(1, 0)
+    want = plan.run(dec)
+    want_memo = [sorted(int(x) for x in m.cpu().tolist()) for m in want["memo"]]
+    n = dec.shape[0]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert sum(g[2] for g in got) == n                 # buckets partition the step
+    assert all(0 < g[2] < n for g in got)
+    for rank, beam, _, n_reps, memo in got:
+        assert beam == want["beam"], rank
+        assert n_reps == want["n_reps"]
+        assert memo == want_memo, rank     # bottom half of the merged global reps
