@@ -240,7 +240,7 @@ int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, doubl
                                      std::to_string(p->max_smem) + " bytes)");
   Layout L = layout_for(p, S, nwarps, spill);
   int64_t grid = std::min<int64_t>(p->num_sms, (n + nwarps - 1) / nwarps);
-  if (spill) {
+  {
     const int64_t need = grid * nwarps * (int64_t)L.gl_bytes;
     if (need > p->gcap) {   // grow-only global scratch
       CK(cudaStreamSynchronize((cudaStream_t)stream));
@@ -254,7 +254,7 @@ int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, doubl
   p->last_warps = nwarps;
   p->last_slice = L.warp_bytes;
   int rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, nwarps,
-                            (int)grid, p->err, p->reuse, spill ? p->gscratch : nullptr, (cudaStream_t)stream);
+                            (int)grid, p->err, p->reuse, p->gscratch, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "unsupported ndim");
   CK(cudaGetLastError());
   return GS_OK;

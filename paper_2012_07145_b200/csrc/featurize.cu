@@ -52,13 +52,11 @@ struct K1 {
   const GsAccess* A;
   const PipeDev* P;
   GsDecision* dec;   // current decision records
-  GsDecision* pdec;  // previous candidate's
   int16_t* didx;
   CF<ND>* cf;        // current geometry
   RRead* rd;
   int16_t* path;
   int32_t* rdb;      // [2*ns]: begin,end of reads per global stage
-  int32_t* frd;      // [nf]: first read index of each non-inline func
   int32_t* rows;
   Frame* stack;
   int64_t* volacc;
@@ -122,7 +120,7 @@ __device__ __forceinline__ void block_box(const CF<ND>& c, int32_t* lo, int32_t*
   // resolve.py:112-122
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
-    if (c.kind == K_ROOT) { lo[d] = 0; hi[d] = c.bbx[d] - 1; }
+    if (c.kind == K_ROOT) { lo[d] = 0; hi[d] = c.ctx[d] * c.coeff[d] - 1; }   // thread*serial
     else if (c.kind == K_BLOCK) { lo[d] = c.rlo[d]; hi[d] = c.rhi[d]; }
     else { lo[d] = c.base[d]; hi[d] = c.base[d] + (c.ctx[d] - 1) * c.coeff[d] + c.ext[d] - 1; }
   }
@@ -206,7 +204,6 @@ __device__ void resolve_structure(K1<ND>& k) {
     const GsDecision& d = k.dec[i];
     if (d.kind == GS_INLINE) continue;
     const GsFunc& fn = k.F[d.func];
-    k.frd[d.func] = m.nreads;
     for (int s = 0; s < fn.n_stages && !m.err; ++s) {
       int gsid = fn.stage_begin + s;
       int nt = 0;
@@ -403,7 +400,6 @@ __device__ bool geometry_one(K1<ND>& k, int i) {
       c.rlo[dd] = 0; c.rhi[dd] = (int32_t)(b * st - 1);
       c.tlo[dd] = c.rlo[dd]; c.thi[dd] = c.rhi[dd];
       c.ctx[dd] = thr[dd]; c.base[dd] = 0; c.coeff[dd] = ser[dd]; c.ext[dd] = ser[dd];
-      c.bbx[dd] = (int32_t)st;
     }
     c.kind = K_ROOT; c.tier = T_GLOBAL; c.kernel = (int16_t)f; c.realizations = 1;
     c.n_threads = (int32_t)nt; c.unrolled = sp < 16; c.has_serial = 1; c.serial_prod = (int32_t)sp;
@@ -1015,12 +1011,14 @@ __device__ __forceinline__ unsigned warp_count(unsigned long long a, bool active
 //    For shared memory the count depends on the residue only mod the bank
 //    width (adding whole words rotates the banks), so at most bank-width
 //    evaluations are needed per class.
-template <int ND>
+// MC / BW / NB: compile-time period, bank width and bank count for the
+// common machines (0 = read them from Mc at run time).
+template <int ND, int MC, int BW, int NB>
 __device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, int plen, bool identity,
                                       const CF<ND>& h, const CF<ND>& prod, int eb, int tier,
                                       const GsMachine& Mc, WarpScr& W, int& err) {
   const int lane = lane_id();
-  const int M = tier == T_GLOBAL ? Mc.global_transaction_bytes : Mc.shared_banks * Mc.bank_width_bytes;
+  const int M = MC ? MC : tier == T_GLOBAL ? Mc.global_transaction_bytes : Mc.shared_banks * Mc.bank_width_bytes;
   const ModM mm(M);
   const int per = (M + 31) / 32;
   int64_t bs[ND], ts[ND];
@@ -1130,8 +1128,8 @@ __device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, in
   int64_t cst = kAddrBias;
 #pragma unroll
   for (int d = 0; d < ND; ++d) cst += ((int64_t)h.base[d] * ts[d] - prod.rlo[d]) * bs[d];
-  const int bw = Mc.bank_width_bytes, banks = Mc.shared_banks;
-  const int bw_lg = (bw & (bw - 1)) == 0 ? __ffs(bw) - 1 : -1;
+  const int bw = BW ? BW : Mc.bank_width_bytes, banks = NB ? NB : Mc.shared_banks;
+  const int bw_lg = BW ? (BW == 4 ? 2 : BW == 8 ? 3 : __ffs(BW) - 1) : (bw & (bw - 1)) == 0 ? __ffs(bw) - 1 : -1;
   // residues that matter per class: all M (global), M mod bank width (shared)
   const bool fold = tier != T_GLOBAL && bw_lg >= 0 && bw <= 32 && (M % bw) == 0;
   const int P = fold ? bw : M;                 // class weight vector length
@@ -1346,16 +1344,25 @@ __device__ void row_features(K1<ND>& k, WarpScr& W, int func, int si, bool inl, 
   }
   __syncwarp();
   // ---- loads (block 0 of the host's kernel)
+  // the default machine (32 B transactions, 32 banks x 4 B) gets the
+  // compile-time-specialised counter
+  const bool vdef = M.global_transaction_bytes == 32 && M.shared_banks == 32 && M.bank_width_bytes == 4;
+  auto tx = [&](const int16_t* path, int plen, bool identity, const CF<ND>& host, const CF<ND>& prod, int eb,
+                int tier) -> unsigned long long {
+    if (vdef) {
+      if (tier == T_GLOBAL) return warp_tx<ND, 32, 4, 32>(k.A, path, plen, identity, host, prod, eb, tier, M, W, err);
+      return warp_tx<ND, 128, 4, 32>(k.A, path, plen, identity, host, prod, eb, tier, M, W, err);
+    }
+    return warp_tx<ND, 0, 0, 0>(k.A, path, plen, identity, host, prod, eb, tier, M, W, err);
+  };
   unsigned long long ld[2] = {0, 0};
   for (int q = 0; q < nr; ++q) {
     const RRead& r = k.rd[W.rl[q]];
     if (r.tier != T_GLOBAL && r.tier != T_SHARED) continue;
-    ld[r.tier] += warp_tx<ND>(k.A, k.path + r.pbeg, r.plen, false, h, k.cf[r.producer],
-                              k.F[r.producer].elem_bytes, r.tier, M, W, err);
+    ld[r.tier] += tx(k.path + r.pbeg, r.plen, false, h, k.cf[r.producer], k.F[r.producer].elem_bytes, r.tier);
   }
   unsigned long long st = 0;
-  if (!inl && (g.tier == T_GLOBAL || g.tier == T_SHARED))
-    st = warp_tx<ND>(k.A, nullptr, 0, true, g, g, fn.elem_bytes, g.tier, M, W, err);
+  if (!inl && (g.tier == T_GLOBAL || g.tier == T_SHARED)) st = tx(nullptr, 0, true, g, g, fn.elem_bytes, g.tier);
   // ---- working set at thread: fuse_at_thread children (featurize.py:482-492)
   int64_t wsc = 0;
   if (!inl) {
@@ -1475,25 +1482,24 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   // capacity-sized structure arrays live in the slice, or — for pipelines
   // whose worst-case inline expansion does not fit shared memory — in this
   // warp's slice of a global scratch (generic pointers: same code)
-  uint8_t* wg = L.gl_bytes ? gscratch + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * L.gl_bytes : ws;
+  uint8_t* wgs = gscratch + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * L.gl_bytes;
+  uint8_t* wg = L.spill ? wgs : ws;
   K1<ND> k;
   k.P = P;
   k.F = reinterpret_cast<const GsFunc*>(sm + L.blob);
   k.ST = reinterpret_cast<const GsStage*>(sm + L.blob + P->off_stages);
   k.A = reinterpret_cast<const GsAccess*>(sm + L.blob + P->off_access);
   k.dec = reinterpret_cast<GsDecision*>(ws + L.dec);
-  k.pdec = reinterpret_cast<GsDecision*>(ws + L.pdec);
   k.didx = reinterpret_cast<int16_t*>(ws + L.didx);
   k.cf = reinterpret_cast<CF<ND>*>(ws + L.cf);
   k.rd = reinterpret_cast<RRead*>(wg + L.reads);
   k.path = reinterpret_cast<int16_t*>(wg + L.paths);
   k.rdb = reinterpret_cast<int32_t*>(ws + L.rdb);
-  k.frd = reinterpret_cast<int32_t*>(ws + L.frd);
   k.rows = reinterpret_cast<int32_t*>(ws + L.rows);
   k.stack = reinterpret_cast<Frame*>(ws + L.stack);
   k.volacc = reinterpret_cast<int64_t*>(ws + L.volacc);
   k.touched = reinterpret_cast<int16_t*>(ws + L.touched);
-  k.icall = reinterpret_cast<ICall*>(wg + L.icall);
+  k.icall = reinterpret_cast<ICall*>(wgs + L.icall);
   k.srcb = reinterpret_cast<int32_t*>(ws + L.srcb);
   k.srcl = reinterpret_cast<int16_t*>(wg + L.srcl);
   k.rdepb = reinterpret_cast<int32_t*>(ws + L.rdepb);
@@ -1506,7 +1512,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   k.kmb = reinterpret_cast<int32_t*>(ws + L.kmb);
   k.kml = reinterpret_cast<int16_t*>(ws + L.kml);
   k.icb = reinterpret_cast<int32_t*>(ws + L.icb);
-  k.icl = reinterpret_cast<int16_t*>(wg + L.icl);
+  k.icl = reinterpret_cast<int16_t*>(wgs + L.icl);
   k.dlist = reinterpret_cast<int16_t*>(ws + L.dlist);
   k.gdirty = reinterpret_cast<uint8_t*>(ws + L.gdirty);
   k.kdirty = reinterpret_cast<uint8_t*>(ws + L.kdirty);
@@ -1534,21 +1540,20 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
       if (lane < k.mw) k.cmask[lane] = 0u;
       __syncwarp();
       unsigned cnt = 0, diff = 0;
+      // the previous candidate's records: still in L2 (this warp just read them)
+      const uint4* prv = reinterpret_cast<const uint4*>(dec + (c > c0 ? c - 1 : c) * S);
       for (int i0 = 0; i0 < S; i0 += 32) {
         const int i = i0 + lane;
         const bool live = i < S && k.dec[i].func != 0xFFFF;
         cnt += __popc(__ballot_sync(0xffffffffu, live));
         bool d = false;
         if (i < S) {
-          const GsDecision& a = k.dec[i];
-          const GsDecision& b = k.pdec[i];
-          d = a.func != b.func || a.consumer != b.consumer || a.kind != b.kind;
-          if (live && k.mw > 0 && !d) {   // same structure here: did the tiling change?
-            const uint4 x = reinterpret_cast<const uint4*>(k.dec)[i];
-            const uint4 y = reinterpret_cast<const uint4*>(k.pdec)[i];
-            if (x.x != y.x || x.y != y.y || x.z != y.z || x.w != y.w)
-              atomicOr(&k.cmask[a.func >> 5], 1u << (a.func & 31));
-          }
+          const uint4 x = reinterpret_cast<const uint4*>(k.dec)[i];
+          const uint4 y = __ldg(prv + i);
+          // func | consumer << 16 in .x, kind in the low byte of .y
+          d = x.x != y.x || ((x.y ^ y.y) & 0xFFu) != 0u;
+          if (live && k.mw > 0 && !d && (x.y != y.y || x.z != y.z || x.w != y.w))
+            atomicOr(&k.cmask[k.dec[i].func >> 5], 1u << (k.dec[i].func & 31));
         }
         diff |= __ballot_sync(0xffffffffu, d);
       }
@@ -1617,7 +1622,6 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
       }
     }
     __syncwarp();
-    { GsDecision* t = k.dec; k.dec = k.pdec; k.pdec = t; }
     if (lane == 0) m.prev_valid = (m.err == 0) && feats != nullptr;
     __syncwarp();
   }
@@ -1652,8 +1656,8 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   int g = 0;   // global scratch bytes per warp (spill)
   // capacity-sized arrays: in the smem slice, or in global scratch
   auto place = [&](int bytes) { int r; if (spill) { r = g; g += al(bytes); } else { r = o; o += al(bytes); } return r; };
+  auto gplace = [&](int bytes) { int r = g; g += al(bytes); return r; };   // always global
   L.dec = o; o += al(S * 16);
-  L.pdec = o; o += al(S * 16);
   L.didx = o; o += al(nf * 2);
   int cfs = nd == 1 ? cf_size<1>() : nd == 2 ? cf_size<2>() : nd == 3 ? cf_size<3>() : cf_size<4>();
   L.cf = o; o += al(nf * cfs);
@@ -1661,9 +1665,8 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   L.reads = place(rcap * (int)sizeof(RRead));
   L.paths = place(pcap * 2);
   L.rdb = o; o += al(2 * ns * 4);
-  L.frd = o; o += al(nf * 4);
   L.rows = o; o += al(R * 4);
-  L.icall = place(pcap * (int)sizeof(ICall));
+  L.icall = gplace(pcap * (int)sizeof(ICall));
   L.srcb = o; o += al((nf + 1) * 4);
   L.srcl = place(rcap * 2);
   L.rdepb = o; o += al((R + 1) * 4);
@@ -1679,7 +1682,7 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   L.kmb = o; o += al((nf + 1) * 4);
   L.kml = o; o += al(nf * 2);
   L.icb = o; o += al((nf + 1) * 4);
-  L.icl = place(pcap * 2);
+  L.icl = gplace(pcap * 2);
   L.dlist = o; o += al(nf * 2);
   L.gdirty = o; o += al(nf);
   L.kdirty = o; o += al(nf);
@@ -1694,6 +1697,7 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   o += scr;
   L.warp_bytes = al(o);
   L.gl_bytes = g;
+  L.spill = spill;
   L.total = L.warps + nwarps * L.warp_bytes;
   L.rcap = rcap; L.pcap = pcap; L.S = S; L.R = R;
   return L;

@@ -47,15 +47,12 @@ struct CF {
   int32_t rlo[ND], rhi[ND];       // padded realization region
   int32_t tlo[ND], thi[ND];       // union of realizations over the run
   int32_t ctx[ND], base[ND], coeff[ND], ext[ND];
-  int32_t bbx[ND];                // root: thread*serial (block box extent)
   int32_t serial_prod;
   int32_t k_threads;              // kernel owner only: max threads per block
   int32_t spare[(ND & 1) ? 2 : 1];  // explicit: no padding bytes (records are memcmp'd)
   int64_t realizations;
-  int64_t calls;                  // inline: total calls
-  int64_t best;                   // inline: best per-consumer calls
-  int64_t n_blocks;               // kernel owner only
-  int64_t k_shared;               // kernel owner only: shared bytes
+  union { int64_t n_blocks; int64_t calls; };   // kernel owner: blocks; inline: total calls
+  union { int64_t k_shared; int64_t best; };    // kernel owner: shared bytes; inline: best per-consumer calls
 };
 
 struct RRead {                // one expanded read (resolve.py:56-79 ResolvedRead)
@@ -68,11 +65,12 @@ struct RRead {                // one expanded read (resolve.py:56-79 ResolvedRea
 };
 
 struct Layout {                 // byte offsets inside dynamic shared memory (K1)
-  int blob, dec, pdec, didx, cf, pcf, reads, paths, rdb, frd, rows, stack, volacc, touched, icall, srcb,
+  int blob, dec, didx, cf, pcf, reads, paths, rdb, rows, stack, volacc, touched, icall, srcb,
       srcl, rdepb, rdep, dirty, rflag, rowlist, rsrc, kern, dm, cmask, kmb, kml, icb, icl, dlist, gdirty,
       kdirty, misc, warps, scr;
   int mw;                       // dependency-mask words per func (0 = incremental resolve off)
-  int gl_bytes;                 // per-warp global scratch (capacity-sized arrays spilled), 0 = none
+  int gl_bytes;                 // per-warp global scratch bytes (inline-call lists, spilled arrays)
+  int spill;                    // capacity-sized structure arrays in global scratch
   int warp_bytes, total;
   int rcap, pcap, S, R;
 };
