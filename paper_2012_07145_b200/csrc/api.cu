@@ -12,7 +12,7 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
                      const Layout& L, int nwarps, int grid, int* gerr, int reuse, uint8_t* gscratch,
-                     cudaStream_t st);
+                     uint8_t* heads, cudaStream_t st);
 int featurize_warps(const Layout& L1, int max_smem);
 int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st);
 int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
@@ -61,10 +61,12 @@ struct GsPipeline {
   int max_smem = 0;
   int rcap = 0, pcap = 0;
   int reuse = 1;
-  int nwarps = 8;
+  int nwarps = kK1MaxWarps;
   int last_warps = 0, last_slice = 0;   // K1 launch shape (diagnostics)
   uint8_t* hscratch = nullptr;   // K3 run-head flags (grow-only)
   uint8_t* gscratch = nullptr;   // K1 spilled structure arrays (grow-only)
+  uint8_t* k1heads = nullptr;    // K1 run-head flags (grow-only)
+  int64_t k1cap = 0;
   int64_t gcap = 0;
   int64_t hcap = 0;
 };
@@ -178,7 +180,7 @@ int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
 int gs_pipeline_destroy(gs_pipeline_t p) {
   if (!p) return GS_OK;
   cudaFree(p->dev); cudaFree(p->blob); cudaFree(p->stage_of_func); cudaFree(p->algo); cudaFree(p->sorted);
-  cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err); cudaFree(p->hscratch); cudaFree(p->gscratch);
+  cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err); cudaFree(p->hscratch); cudaFree(p->gscratch); cudaFree(p->k1heads);
   for (double* b : p->wbufs) cudaFree(b);
   delete p;
   return GS_OK;
@@ -251,10 +253,18 @@ int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, doubl
       p->gcap = need;
     }
   }
+  if (n > p->k1cap) {   // grow-only run-head flags for the K1 work units
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    if (p->k1heads) CK(cudaFree(p->k1heads));
+    p->k1heads = nullptr;
+    p->k1cap = 0;
+    CK(cudaMalloc(&p->k1heads, (size_t)n));
+    p->k1cap = n;
+  }
   p->last_warps = nwarps;
   p->last_slice = L.warp_bytes;
   int rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, nwarps,
-                            (int)grid, p->err, p->reuse, p->gscratch, (cudaStream_t)stream);
+                            (int)grid, p->err, p->reuse, p->gscratch, p->k1heads, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "unsupported ndim");
   CK(cudaGetLastError());
   return GS_OK;

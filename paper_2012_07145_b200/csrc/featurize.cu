@@ -129,6 +129,7 @@ __device__ __forceinline__ void block_box(const CF<ND>& c, int32_t* lo, int32_t*
 // chain box of [lo,hi] through a path of accesses, dimension d
 __device__ __forceinline__ void chain_iv(const GsAccess* A, const int16_t* p, int plen, int d,
                                          int64_t& a, int64_t& b) {
+  #pragma unroll 1
   for (int k = 0; k < plen; ++k) {
     const GsAccess& x = A[p[k]];
     a = a * x.s[d] + x.lo[d];
@@ -195,7 +196,7 @@ __device__ void expand_stage(K1<ND>& k, int root, int gstage, int& ntouched) {
 
 // lane 0
 template <int ND>
-__device__ void resolve_structure(K1<ND>& k) {
+__device__ __noinline__ void resolve_structure(K1<ND>& k) {
   Misc& m = *k.misc;
   const int nf = k.P->nf;
   m.nreads = 0; m.npath = 0; m.nicall = 0;
@@ -368,7 +369,7 @@ __device__ __forceinline__ void cf_store(K1<ND>& k, int f, const CF<ND>& c) {
 // no member's geometry reads them, so the result is the same and a
 // sibling that changes one member recomputes only its kernel's sums.
 template <int ND>
-__device__ bool geometry_one(K1<ND>& k, int i) {
+__device__ __noinline__ bool geometry_one(K1<ND>& k, int i) {
   const int lane = lane_id();
   Misc& m = *k.misc;
   const GsDecision d = k.dec[i];
@@ -425,6 +426,7 @@ __device__ bool geometry_one(K1<ND>& k, int i) {
   for (int dd = 0; dd < ND; ++dd) { lo[dd] = tlo[dd] = INT64_MAX; hi[dd] = thi[dd] = INT64_MIN; ts0[dd] = 1; }
   {
     const RRead& r0 = k.rd[first];
+    #pragma unroll 1
     for (int q = 0; q < r0.plen; ++q)
 #pragma unroll
       for (int dd = 0; dd < ND; ++dd) ts0[dd] *= k.A[k.path[r0.pbeg + q]].s[dd];
@@ -710,11 +712,13 @@ __device__ int footprint(const GsAccess* A, const int16_t* p, int plen, int d, i
   if (cap < 1) { err |= E_LANEIV; return 0; }
   buf[0] = Iv{a, b};
   int n = 1;
+  #pragma unroll 1
   for (int k = 0; k < plen; ++k) {
     const GsAccess& x = A[p[k]];
     const int64_t s = x.s[d], wl = x.lo[d], wh = x.hi[d];
     if (s <= wh - wl + 1) {       // every interval maps to one interval; merge in place
       int w = 0;
+      #pragma unroll 1
       for (int i = 0; i < n; ++i) {
         Iv v{buf[i].lo * s + wl, buf[i].hi * s + wh};
         if (w && v.lo <= buf[w - 1].hi + 1) { if (v.hi > buf[w - 1].hi) buf[w - 1].hi = v.hi; }
@@ -723,10 +727,12 @@ __device__ int footprint(const GsAccess* A, const int16_t* p, int plen, int d, i
       n = w;
     } else {                      // one interval per point, already disjoint & sorted
       int64_t tot = 0;
+      #pragma unroll 1
       for (int i = 0; i < n; ++i) tot += buf[i].hi - buf[i].lo + 1;
       if (tot > cap) { err |= E_LANEIV; return 0; }
       // expand from the back so the source is not overwritten
       int w = (int)tot;
+      #pragma unroll 1
       for (int i = n - 1; i >= 0; --i)
         for (int64_t xx = buf[i].hi; xx >= buf[i].lo; --xx) buf[--w] = Iv{xx * s + wl, xx * s + wh};
       n = (int)tot;
@@ -747,6 +753,7 @@ __device__ bool footprint_ap(const GsAccess* A, const int16_t* p, int plen, int 
                              int64_t& pts, int64_t& runs) {
   int64_t st = a, step = 1, len = b - a + 1, cnt = 1;
   if (len <= 0) { pts = runs = 0; return true; }
+  #pragma unroll 1
   for (int k = 0; k < plen; ++k) {
     const GsAccess& x = A[p[k]];
     const int64_t s = x.s[d], wl = x.lo[d], w = (int64_t)x.hi[d] - x.lo[d] + 1;
@@ -771,7 +778,7 @@ __device__ bool footprint_ap(const GsAccess* A, const int16_t* p, int plen, int 
 }
 
 template <int ND>
-__device__ void union_count(const GsAccess* A, const RRead* rd, const int16_t* paths,
+__device__ __noinline__ void union_count(const GsAccess* A, const RRead* rd, const int16_t* paths,
                             const int16_t* rl, const int8_t* grp, int nr, int g,
                             const int32_t* blo, const int32_t* bhi,
                             int64_t& vol, int64_t& lines, int& err) {
@@ -814,10 +821,12 @@ __device__ void union_count(const GsAccess* A, const RRead* rd, const int16_t* p
     int64_t outer = 1;
     for (int d = 1; d < ND; ++d) {
       int64_t t = 0;
+      #pragma unroll 1
       for (int i = 0; i < cnt[0][d]; ++i) t += buf[off[0][d] + i].hi - buf[off[0][d] + i].lo + 1;
       outer *= t;
     }
     int64_t t0 = 0;
+    #pragma unroll 1
     for (int i = 0; i < cnt[0][0]; ++i) t0 += buf[off[0][0] + i].hi - buf[off[0][0] + i].lo + 1;
     vol = t0 * outer;
     lines = (int64_t)cnt[0][0] * outer;
@@ -829,13 +838,16 @@ __device__ void union_count(const GsAccess* A, const RRead* rd, const int16_t* p
   int ncut[ND > 1 ? ND - 1 : 1];
   for (int d = 1; d < ND; ++d) {
     int n = 0;
+    #pragma unroll 1
     for (int q = 0; q < K; ++q)
+      #pragma unroll 1
       for (int i = 0; i < cnt[q][d]; ++i) {
         int64_t v2[2] = {buf[off[q][d] + i].lo, buf[off[q][d] + i].hi + 1};
         for (int e = 0; e < 2; ++e) {
           int64_t v = v2[e];
           int pos = n;
           bool dup = false;
+          #pragma unroll 1
           for (int t = 0; t < n; ++t) { if (cuts[d - 1][t] == v) { dup = true; break; } }
           if (dup) continue;
           if (n >= kCuts) { err |= E_LANEIV; return; }
@@ -855,11 +867,13 @@ __device__ void union_count(const GsAccess* A, const RRead* rd, const int16_t* p
     // cell = pieces idx[d]
     int64_t cellv = 1;
     unsigned act = 0;
+    #pragma unroll 1
     for (int q = 0; q < K; ++q) {
       bool in = true;
       for (int d = 1; d < ND && in; ++d) {
         int64_t p0 = cuts[d - 1][idx[d - 1]];
         bool hit = false;
+        #pragma unroll 1
         for (int i = 0; i < cnt[q][d]; ++i) {
           const Iv& v = buf[off[q][d] + i];
           if (v.lo <= p0 && p0 <= v.hi) { hit = true; break; }
@@ -872,12 +886,14 @@ __device__ void union_count(const GsAccess* A, const RRead* rd, const int16_t* p
     if (act) {
       // k-way merge of the active dim-0 lists
       int head[kGroupReads];
+      #pragma unroll 1
       for (int q = 0; q < K; ++q) head[q] = 0;
       int64_t runs = 0, len = 0, cl = 0, ch = 0;
       bool open = false;
       while (true) {
         int best = -1;
         int64_t bl = 0;
+        #pragma unroll 1
         for (int q = 0; q < K; ++q) {
           if (!((act >> q) & 1) || head[q] >= cnt[q][0]) continue;
           int64_t l = buf[off[q][0] + head[q]].lo;
@@ -913,14 +929,25 @@ __device__ void union_count(const GsAccess* A, const RRead* rd, const int16_t* p
 // ---------------------------------------------------------------------------
 // Residue arithmetic modulo the transaction / bank period M: shifts and
 // masks when M is a power of two (every real machine), divisions otherwise.
+// out-of-line slow paths (non-power-of-two periods): keep 64-bit division
+// code out of the hot loops' instruction footprint
+__device__ __noinline__ int64_t floordiv_slow(int64_t a, int64_t b) { return floordiv(a, b); }
+__device__ __noinline__ int64_t posmod_slow(int64_t a, int64_t m) { return posmod(a, m); }
+
+template <int MC>
 struct ModM {
   int M, lg;
-  __device__ explicit ModM(int m) : M(m), lg(-1) {
-    if (m > 0 && (m & (m - 1)) == 0) { lg = 0; while ((1 << lg) < m) ++lg; }
+  __device__ explicit ModM(int m) : M(MC ? MC : m), lg(-1) {
+    if (MC) { lg = 0; while ((1 << lg) < MC) ++lg; }   // constant-folded
+    else if (m > 0 && (m & (m - 1)) == 0) { lg = 0; while ((1 << lg) < m) ++lg; }
   }
-  __device__ __forceinline__ int64_t fdiv(int64_t a) const { return lg >= 0 ? (a >> lg) : floordiv(a, M); }
+  __device__ __forceinline__ int64_t fdiv(int64_t a) const {
+    if (MC) return a >> lg;
+    return lg >= 0 ? (a >> lg) : floordiv_slow(a, M);
+  }
   __device__ __forceinline__ int pmod(int64_t a) const {
-    return lg >= 0 ? (int)(a & (int64_t)(M - 1)) : (int)posmod(a, M);
+    if (MC) return (int)(a & (int64_t)(MC - 1));
+    return lg >= 0 ? (int)(a & (int64_t)(M - 1)) : (int)posmod_slow(a, M);
   }
   // #{x in [a,b] : x = r (mod M)}
   __device__ __forceinline__ unsigned long long count_in(int64_t a, int64_t b, int r) const {
@@ -976,7 +1003,8 @@ struct WarpWalk {
 // transactions of one emulated warp for ONE instruction constant r
 // (featurize.py:173-196): global = distinct segments; shared = max over
 // banks of distinct words; warp-collective, lanes agree on the result
-__device__ __forceinline__ unsigned warp_count(unsigned long long a, bool active, int tier, const ModM& mg, int bw_lg,
+template <int MC>
+__device__ __forceinline__ unsigned warp_count(unsigned long long a, bool active, int tier, const ModM<MC>& mg, int bw_lg,
                                                int bw, int banks) {
   const int lane = lane_id();
   if (tier == T_GLOBAL) {
@@ -1014,12 +1042,12 @@ __device__ __forceinline__ unsigned warp_count(unsigned long long a, bool active
 // MC / BW / NB: compile-time period, bank width and bank count for the
 // common machines (0 = read them from Mc at run time).
 template <int ND, int MC, int BW, int NB>
-__device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, int plen, bool identity,
+__device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, int plen, bool identity,
                                       const CF<ND>& h, const CF<ND>& prod, int eb, int tier,
                                       const GsMachine& Mc, WarpScr& W, int& err) {
   const int lane = lane_id();
   const int M = MC ? MC : tier == T_GLOBAL ? Mc.global_transaction_bytes : Mc.shared_banks * Mc.bank_width_bytes;
-  const ModM mm(M);
+  const ModM<MC> mm(M);
   const int per = (M + 31) / 32;
   int64_t bs[ND], ts[ND];
   {
@@ -1030,6 +1058,7 @@ __device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, in
       acc *= (int64_t)prod.rhi[d] - prod.rlo[d] + 1;
       ts[d] = 1;
       if (!identity)
+        #pragma unroll 1
         for (int q = 0; q < plen; ++q) ts[d] *= A[path[q]].s[d];
     }
   }
@@ -1055,6 +1084,7 @@ __device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, in
               const unsigned long long hv = W.H[r];
               if (!hv) continue;
               const int64_t base = (int64_t)r * s;
+              #pragma unroll 1
               for (int64_t w = wl; w <= wh; ++w) atomicAdd(&W.S[mm.pmod(base + w)], hv);
             }
           } else {
@@ -1085,6 +1115,7 @@ __device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, in
         int r = lane + 32 * j;
         if (r >= M) continue;
         unsigned long long c = 0;
+        #pragma unroll 1
         for (int i = 0; i < n; ++i) c += mm.count_in(buf[i].lo, buf[i].hi, r);
         W.H[r] = c;
       }
@@ -1112,6 +1143,7 @@ __device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, in
       const int k = lane + 32 * j;
       if (k >= M) continue;
       unsigned long long acc = 0;
+      #pragma unroll 1
       for (int i = 0; i < nnz; ++i) {
         const int r = W.nz[i];
         acc += W.T[r] * W.S[mm.pmod(k - r)];
@@ -1197,6 +1229,28 @@ __device__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, in
     const bool active = ((j ? am1 : am0) >> lane) & 1u;
     const int64_t org = j ? o01 + rel1 : o00 + rel0;
     const unsigned long long* wv = j ? W.S : W.H;
+    if (MC == 32 && tier == T_GLOBAL) {
+      // lanes = residues.  When the representative's lane addresses are
+      // non-decreasing (row-major thread tiles), the segments of one
+      // instruction are too, so its count is 1 + the segment changes
+      // between consecutive active lanes: every residue at once, no match.
+      const int64_t up = __shfl_up_sync(0xffffffffu, org, 1);
+      if (__all_sync(0xffffffffu, lane == 0 || !active || org >= up)) {
+        const int na = __popc(j ? am1 : am0);   // active lanes are a prefix
+        int64_t prev = __shfl_sync(0xffffffffu, org, 0) + lane;
+        unsigned cnt = na > 0 ? 1u : 0u;
+#pragma unroll 4
+        for (int i = 1; i < na; ++i) {
+          const int64_t cur = __shfl_sync(0xffffffffu, org, i) + lane;
+          cnt += (unsigned)((cur >> 5) != (prev >> 5));
+          prev = cur;
+        }
+        unsigned long long part = wv[lane] * cnt;
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        total += part;
+        continue;
+      }
+    }
     for (int c = 0; c < pp; ++c) {
       unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < P && wv[c * 32 + lane] != 0);
       while (nz) {
@@ -1265,7 +1319,7 @@ __device__ void parallel_feats(double* v, const GsMachine& M, int n, const CF<ND
 }
 
 template <int ND>
-__device__ void row_features(K1<ND>& k, WarpScr& W, int func, int si, bool inl, double* out) {
+__device__ __noinline__ void row_features(K1<ND>& k, WarpScr& W, int func, int si, bool inl, double* out) {
   const int lane = lane_id();
   const GsMachine& M = k.P->m;
   Misc& m = *k.misc;
@@ -1473,7 +1527,7 @@ __global__ void __launch_bounds__(kK1MaxWarps * 32, 1)
 featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob, const GsDecision* __restrict__ dec,
                  int64_t n, int S, double* __restrict__ feats, int32_t* __restrict__ row_key,
                  int32_t* __restrict__ n_rows, uint8_t* __restrict__ verdict, int32_t* __restrict__ row_src,
-                 Layout L, int* gerr, int reuse, uint8_t* __restrict__ gscratch) {
+                 Layout L, int* gerr, int reuse, uint8_t* __restrict__ gscratch, const uint8_t* __restrict__ heads) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar;
   const int warp = threadIdx.x >> 5, lane = lane_id(), nw = blockDim.x >> 5;
@@ -1492,16 +1546,16 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   k.dec = reinterpret_cast<GsDecision*>(ws + L.dec);
   k.didx = reinterpret_cast<int16_t*>(ws + L.didx);
   k.cf = reinterpret_cast<CF<ND>*>(ws + L.cf);
-  k.rd = reinterpret_cast<RRead*>(wg + L.reads);
-  k.path = reinterpret_cast<int16_t*>(wg + L.paths);
-  k.rdb = reinterpret_cast<int32_t*>(ws + L.rdb);
+  k.rd = reinterpret_cast<RRead*>(wgs + L.reads);
+  k.path = reinterpret_cast<int16_t*>(wgs + L.paths);
+  k.rdb = reinterpret_cast<int32_t*>(wgs + L.rdb);
   k.rows = reinterpret_cast<int32_t*>(ws + L.rows);
   k.stack = reinterpret_cast<Frame*>(ws + L.stack);
   k.volacc = reinterpret_cast<int64_t*>(ws + L.volacc);
   k.touched = reinterpret_cast<int16_t*>(ws + L.touched);
   k.icall = reinterpret_cast<ICall*>(wgs + L.icall);
-  k.srcb = reinterpret_cast<int32_t*>(ws + L.srcb);
-  k.srcl = reinterpret_cast<int16_t*>(wg + L.srcl);
+  k.srcb = reinterpret_cast<int32_t*>(wgs + L.srcb);
+  k.srcl = reinterpret_cast<int16_t*>(wgs + L.srcl);
   k.rdepb = reinterpret_cast<int32_t*>(ws + L.rdepb);
   k.rdep = reinterpret_cast<int16_t*>(wg + L.rdep);
   k.dirty = reinterpret_cast<uint8_t*>(ws + L.dirty);
@@ -1509,8 +1563,8 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   k.kern = reinterpret_cast<int16_t*>(ws + L.kern);
   k.dm = reinterpret_cast<uint32_t*>(ws + L.dm);
   k.cmask = reinterpret_cast<uint32_t*>(ws + L.cmask);
-  k.kmb = reinterpret_cast<int32_t*>(ws + L.kmb);
-  k.kml = reinterpret_cast<int16_t*>(ws + L.kml);
+  k.kmb = reinterpret_cast<int32_t*>(wgs + L.kmb);
+  k.kml = reinterpret_cast<int16_t*>(wgs + L.kml);
   k.icb = reinterpret_cast<int32_t*>(ws + L.icb);
   k.icl = reinterpret_cast<int16_t*>(wgs + L.icl);
   k.dlist = reinterpret_cast<int16_t*>(ws + L.dlist);
@@ -1521,17 +1575,35 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   WarpScr& W = *reinterpret_cast<WarpScr*>(ws + L.scr);
   uint8_t* rflag = ws + L.rflag;
   int32_t* rsrc = reinterpret_cast<int32_t*>(ws + L.rsrc);
-  // contiguous candidate range per warp
-  const int64_t nwt = (int64_t)gridDim.x * nw;
-  const int64_t gw = (int64_t)blockIdx.x * nw + warp;
-  const int64_t per = (n + nwt - 1) / nwt;
-  const int64_t c0 = gw * per < n ? gw * per : n;
-  const int64_t c1 = c0 + per < n ? c0 + per : n;
+  // Work units: kUnit-candidate slices of the batch, each extended to start
+  // and end at a decision-structure run head, handed out dynamically; a unit
+  // therefore never splits a run of siblings (whose first member needs the
+  // full resolve anyway), and warps that drew cheap runs take more of them.
   Misc& m = *k.misc;
-  if (lane == 0) { m.prev_valid = 0; m.same_struct = 0; m.ndec = 0; }
-  unsigned long long st_inc = 0, st_rows = 0, st_emit = 0, st_geo = 0;   // work counters (lane 0)
+  unsigned long long st_cand = 0, st_inc = 0, st_rows = 0, st_emit = 0, st_geo = 0;   // (lane 0)
+  unsigned* work = reinterpret_cast<unsigned*>(gerr + 14);
+  const int64_t nunits = (n + kUnit - 1) / kUnit;
+  auto snap = [&](int64_t x) -> int64_t {
+    if (x >= n) return n;
+    if (!heads) return x;
+    for (int64_t i = x; i < n; i += 32) {
+      const bool h = i + lane < n && heads[i + lane];
+      const unsigned b = __ballot_sync(0xffffffffu, h);
+      if (b) return i + __ffs(b) - 1;
+    }
+    return n;
+  };
   bulk_wait(&bar);
   __syncthreads();   // the only CTA barrier: descriptor staged
+  for (;;) {
+  unsigned uj = 0;
+  if (lane == 0) uj = atomicAdd(work, 1u);
+  const int64_t j = __shfl_sync(0xffffffffu, uj, 0);
+  if (j >= nunits) break;
+  const int64_t c0 = snap(j * kUnit), c1 = snap((j + 1) * kUnit);
+  if (c0 >= c1) continue;
+  if (lane == 0) { m.prev_valid = 0; m.same_struct = 0; m.ndec = 0; st_cand += c1 - c0; }
+  __syncwarp();
   for (int64_t c = c0; c < c1; ++c) {
     {
       const uint4* src = reinterpret_cast<const uint4*>(dec + c * S);
@@ -1601,35 +1673,61 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     }
     __syncwarp();
     if (lane == 0) { st_inc += m.same_struct; st_rows += nd; st_emit += nr; st_geo += m.ngeo; }
+    // a sibling starts from the previous candidate's feature block (this
+    // warp wrote it: visible after __syncwarp), copied as one contiguous run
+    // of 16-byte vectors with four loads in flight per lane; the dirty rows
+    // are then recomputed over it
+    if (diffable && nd < nr) {
+      const int4* src = reinterpret_cast<const int4*>(feats + (int64_t)(c - 1) * L.R * GS_NUM_FEATURES);
+      int4* dst = reinterpret_cast<int4*>(feats + (int64_t)c * L.R * GS_NUM_FEATURES);
+      const int nv = nr * (GS_NUM_FEATURES * 8 / 16);
+      int i = lane;
+      for (; i + 96 < nv; i += 128) {
+        const int4 a0 = src[i], a1 = src[i + 32], a2 = src[i + 64], a3 = src[i + 96];
+        dst[i] = a0; dst[i + 32] = a1; dst[i + 64] = a2; dst[i + 96] = a3;
+      }
+      for (; i < nv; i += 32) dst[i] = src[i];
+      __syncwarp();
+    }
     for (int q = 0; q < nd; ++q) {
       const int r = k.rowlist[q];
       const int key = k.rows[r];
       const int f = key >> 8, si = key & 255;
       row_features<ND>(k, W, f, si, k.cf[f].kind == K_INLINE, feats + ((int64_t)c * L.R + r) * GS_NUM_FEATURES);
     }
-    // row keys / sources, and clean rows copied from the previous candidate
-    // (written by this warp: visible after __syncwarp)
     for (int r = lane; r < nr; r += 32) {
       row_key[c * L.R + r] = k.rows[r];
       if (row_src) row_src[c * L.R + r] = rsrc[r];
-    }
-    if (diffable && nd < nr) {
-      const double* src = feats + (int64_t)(c - 1) * L.R * GS_NUM_FEATURES;
-      double* dst = feats + (int64_t)c * L.R * GS_NUM_FEATURES;
-      for (int i = lane; i < nr * GS_NUM_FEATURES; i += 32) {
-        const int r = i / GS_NUM_FEATURES;
-        if (!rflag[r]) dst[i] = src[i];
-      }
     }
     __syncwarp();
     if (lane == 0) m.prev_valid = (m.err == 0) && feats != nullptr;
     __syncwarp();
   }
-  if (lane == 0 && c1 > c0) {
+  }
+  if (lane == 0 && st_cand) {
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(gerr + 2);
-    atomicAdd(ctr + 0, (unsigned long long)(c1 - c0));
+    atomicAdd(ctr + 0, st_cand);
     atomicAdd(ctr + 1, st_inc); atomicAdd(ctr + 2, st_rows); atomicAdd(ctr + 3, st_emit); atomicAdd(ctr + 4, st_geo);
   }
+}
+
+// Decision-structure run heads for the K1 work units: candidate c starts a
+// run when any record's (func, consumer, kind) differs from candidate c-1's
+// (the K1 sibling test); one warp per candidate, coalesced record loads.
+__global__ void k1_heads_kernel(const GsDecision* __restrict__ dec, int64_t n, int S, uint8_t* __restrict__ head) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= n) return;
+  if (c == 0) { if (lane == 0) head[0] = 1; return; }
+  const uint2* a = reinterpret_cast<const uint2*>(dec + c * S);
+  const uint2* b = reinterpret_cast<const uint2*>(dec + (c - 1) * S);
+  bool diff = false;
+  for (int i = lane; i < S; i += 32) {
+    const uint2 x = __ldg(a + 2 * i), y = __ldg(b + 2 * i);
+    diff |= x.x != y.x || ((x.y ^ y.y) & 0xFFu) != 0u;
+  }
+  diff = __any_sync(0xffffffffu, diff);
+  if (lane == 0) head[c] = diff;
 }
 
 }  // namespace gs
@@ -1662,13 +1760,13 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   int cfs = nd == 1 ? cf_size<1>() : nd == 2 ? cf_size<2>() : nd == 3 ? cf_size<3>() : cf_size<4>();
   L.cf = o; o += al(nf * cfs);
   L.pcf = 0;
-  L.reads = place(rcap * (int)sizeof(RRead));
-  L.paths = place(pcap * 2);
-  L.rdb = o; o += al(2 * ns * 4);
+  L.reads = gplace(rcap * (int)sizeof(RRead));
+  L.paths = gplace(pcap * 2);
+  L.rdb = gplace(2 * ns * 4);
   L.rows = o; o += al(R * 4);
   L.icall = gplace(pcap * (int)sizeof(ICall));
-  L.srcb = o; o += al((nf + 1) * 4);
-  L.srcl = place(rcap * 2);
+  L.srcb = gplace((nf + 1) * 4);
+  L.srcl = gplace(rcap * 2);
   L.rdepb = o; o += al((R + 1) * 4);
   L.rdep = place((rcap + nf) * 2);
   L.dirty = o; o += al(nf);
@@ -1679,8 +1777,8 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   L.kern = o; o += al(nf * 2);
   L.dm = o; o += al(nf * L.mw * 4);
   L.cmask = o; o += al(kMaxMaskWords * 4);
-  L.kmb = o; o += al((nf + 1) * 4);
-  L.kml = o; o += al(nf * 2);
+  L.kmb = gplace((nf + 1) * 4);
+  L.kml = gplace(nf * 2);
   L.icb = o; o += al((nf + 1) * 4);
   L.icl = gplace(pcap * 2);
   L.dlist = o; o += al(nf * 2);
@@ -1712,13 +1810,18 @@ int featurize_warps(const Layout& L1, int max_smem) {
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
                      const Layout& L, int nwarps, int grid, int* gerr, int reuse, uint8_t* gscratch,
-                     cudaStream_t st) {
+                     uint8_t* heads, cudaStream_t st) {
   dim3 b(nwarps * 32);
+  if (heads && reuse) {
+    k1_heads_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(dec, n, S, heads);
+    g_launch_count++;
+  }
+  cudaMemsetAsync(gerr + 14, 0, sizeof(unsigned), st);   // work-unit counter
   switch (nd) {
 #define GS_CASE(D)                                                                                  \
   case D:                                                                                           \
     cudaFuncSetAttribute(featurize_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total); \
-    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, gerr, reuse, gscratch); \
+    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, gerr, reuse, gscratch, reuse ? heads : nullptr); \
     g_launch_count++;                                                                               \
     break;
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4)
