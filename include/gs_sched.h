@@ -209,6 +209,14 @@ int gs_beam_topk(const double* costs, const uint64_t* pass_hash, int64_t n,
  * the last K1 launch: scorer warps per CTA << 32 | shared bytes per warp. */
 int gs_stats(gs_pipeline_t p, int64_t* out, void* stream);
 
+/* Diagnostics: K1 per-phase warp cycles summed over scorer warps since the
+ * last call (16 slots; all zero unless the library was built with
+ * -DGS_PHASES): [0..6] record diff, resolve, prune, row flags, sibling
+ * copy, row features, key/source writes; [8..13] inside a row: setup,
+ * unions, load transactions, working set + store transactions, assembly,
+ * (13 = loads end).  Synchronizes the device. */
+int gs_debug_phases(int64_t* out);
+
 /* Device-side error word of the last K1 launch (capacity overflow etc.);
  * synchronizes `stream`. */
 int gs_check(gs_pipeline_t p, void* stream);

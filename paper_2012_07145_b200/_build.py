@@ -13,6 +13,7 @@ SOURCES = ("featurize.cu", "cost.cu", "hash.cu", "select.cu", "api.cu")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+FLAGS += [f for f in os.environ.get("GS_NVCC_EXTRA", "").split() if f]   # e.g. -DGS_PHASES
 
 
 def _stale():

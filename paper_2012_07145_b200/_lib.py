@@ -13,12 +13,12 @@ import os
 from .descriptor import GsPipelineDesc
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgs_sched.so")
+LIB_PATH = os.environ.get("GS_LIB_PATH") or os.path.join(HERE, "libgs_sched.so")   # override: diagnostics builds
 
 EXPORTS = ("gs_last_error", "gs_version", "gs_launch_count", "gs_pipeline_create", "gs_pipeline_destroy",
            "gs_pipeline_max_rows", "gs_set_weights", "gs_set_reuse", "gs_featurize", "gs_cost",
            "gs_struct_hash", "gs_select_workspace_bytes", "gs_select_reps",
-           "gs_topk_workspace_bytes", "gs_beam_topk", "gs_check", "gs_stats")
+           "gs_topk_workspace_bytes", "gs_beam_topk", "gs_check", "gs_stats", "gs_debug_phases")
 
 
 class GsError(RuntimeError):
@@ -55,6 +55,7 @@ def load(path: str = LIB_PATH):
         "gs_beam_topk": (i32, [V, V, i64, V, i64, dbl, dbl, u64, i64, dbl, V, i64, V, V, V, V]),
         "gs_check": (i32, [P, V]),
         "gs_stats": (i32, [P, V, V]),
+        "gs_debug_phases": (i32, [V]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

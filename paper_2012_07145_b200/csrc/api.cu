@@ -14,6 +14,7 @@ int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDeci
                      const Layout& L, int nwarps, int grid, int* gerr, int reuse, uint8_t* gscratch,
                      uint8_t* heads, cudaStream_t st);
 int featurize_warps(const Layout& L1, int max_smem);
+int read_phases(long long* out);
 int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st);
 int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
                 const int32_t* n_rows, const int32_t* row_src, int64_t n, int R, double* total, double* row_cost,
@@ -316,6 +317,13 @@ int gs_stats(gs_pipeline_t p, int64_t* out, void* stream) {
   CK(cudaMemcpy(out, p->err + 2, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost));
   CK(cudaMemset(p->err + 2, 0, 6 * sizeof(int64_t)));
   out[5] = (int64_t)p->last_warps << 32 | p->last_slice;
+  return GS_OK;
+}
+
+int gs_debug_phases(int64_t* out) {
+  if (!out) return fail(GS_ERR_ARG, "null argument");
+  CK(cudaDeviceSynchronize());
+  if (read_phases(reinterpret_cast<long long*>(out))) return fail(GS_ERR_CUDA, "phase counters unavailable");
   return GS_OK;
 }
 

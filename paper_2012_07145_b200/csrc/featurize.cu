@@ -929,6 +929,18 @@ __device__ __noinline__ void union_count(const GsAccess* A, const RRead* rd, con
 // ---------------------------------------------------------------------------
 // Residue arithmetic modulo the transaction / bank period M: shifts and
 // masks when M is a power of two (every real machine), divisions otherwise.
+// Per-phase cycle accounting of the scorer warps (diagnostics; build with
+// -DGS_PHASES): 0 record load + diff, 1 resolve, 2 prune, 3 row flags,
+// 4 sibling block copy, 5 row features, 6 key/source writes.
+__device__ unsigned long long g_phase[16];
+#ifdef GS_PHASES
+#define GS_SUB(i) do { if (lane_id() == 0) { long long t_ = clock64(); atomicAdd(&g_phase[i], (unsigned long long)(t_ - tsub)); tsub = t_; } } while (0)
+#define GS_MARK(i) do { if (lane == 0) { long long t_ = clock64(); ph[i] += t_ - tph; tph = t_; } } while (0)
+#else
+#define GS_SUB(i) do { } while (0)
+#define GS_MARK(i) do { } while (0)
+#endif
+
 // out-of-line slow paths (non-power-of-two periods): keep 64-bit division
 // code out of the hot loops' instruction footprint
 __device__ __noinline__ int64_t floordiv_slow(int64_t a, int64_t b) { return floordiv(a, b); }
@@ -1046,6 +1058,9 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
                                       const CF<ND>& h, const CF<ND>& prod, int eb, int tier,
                                       const GsMachine& Mc, WarpScr& W, int& err) {
   const int lane = lane_id();
+#ifdef GS_PHASES
+  long long tsub = clock64();
+#endif
   const int M = MC ? MC : tier == T_GLOBAL ? Mc.global_transaction_bytes : Mc.shared_banks * Mc.bank_width_bytes;
   const ModM<MC> mm(M);
   const int per = (M + 31) / 32;
@@ -1155,6 +1170,7 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
     __syncwarp();
   }
 
+  GS_SUB(7);
   // ---- count: warp-pattern classes ---------------------------------------
   const int nwarps = (h.n_threads + 31) / 32;
   int64_t cst = kAddrBias;
@@ -1187,7 +1203,52 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
   unsigned am0 = 0u, am1 = 0u;
   unsigned long long total = 0;
   WarpWalk<ND> walk(h, ts, bs, cst, lane);
-  for (int w = 0; w < nwarps; ++w, walk.next()) {
+  // Regular thread tiles — dim-0 rows of a multiple of 32 threads, or whole
+  // rows whose length divides 32 stacked without wrapping — give every warp
+  // warp 0's lane pattern: one class whose member shifts are the origins of
+  // the warps' first threads (a scalar mixed-radix walk), folded into a
+  // histogram of shifts mod P and one cyclic convolution with T.
+  bool regular = false;
+  if ((MC == 32 || MC == 128) && P <= 32 && (h.n_threads & 31) == 0) {
+    const int cx = h.ctx[0];
+    regular = (cx % 32 == 0) || (ND >= 2 && 32 % cx == 0 && h.ctx[ND >= 2 ? 1 : 0] % (32 / cx) == 0);
+  }
+  if (regular) {
+    bool active;
+    const int64_t org = walk.origin(active);
+    o00 = __shfl_sync(0xffffffffu, org, 0);
+    rel0 = org - o00;
+    am0 = __ballot_sync(0xffffffffu, active);
+    ncls = 1;
+    int dg[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) dg[d] = 0;
+    unsigned long long cnt = 0;   // lane d: members whose shift = d (mod P)
+    for (int w = 0; w < nwarps; ++w) {
+      int64_t dlt = 0;
+#pragma unroll
+      for (int d = 0; d < ND; ++d) dlt += (int64_t)dg[d] * walk.mul[d];
+      cnt += (unsigned long long)(lane == (int)(dlt & (int64_t)(P - 1)));
+      int carry = 0;
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        dg[d] += walk.inc[d] + carry;
+        carry = 0;
+        if (d < ND - 1 && dg[d] >= walk.ext[d]) { dg[d] -= walk.ext[d]; carry = 1; }
+      }
+    }
+    unsigned long long acc = 0;
+    unsigned nzd = __ballot_sync(0xffffffffu, lane < P && cnt != 0);
+    while (nzd) {
+      const int d = __ffs(nzd) - 1; nzd &= nzd - 1;
+      const unsigned long long cd = __shfl_sync(0xffffffffu, cnt, d);
+      if (fold) acc += cd * __shfl_sync(0xffffffffu, tb, (lane - d) & (P - 1));
+      else acc += cd * W.T[(lane - d) & (P - 1)];
+    }
+    if (lane < P) W.H[lane] = acc;
+    __syncwarp();
+  }
+  for (int w = 0; w < nwarps && !regular; ++w, walk.next()) {
     bool active;
     const int64_t org = walk.origin(active);
     const unsigned amask = __ballot_sync(0xffffffffu, active);
@@ -1215,6 +1276,31 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
       continue;
     }
     // a third lane pattern: evaluate this warp directly
+    if (fold) {                      // shared: the count depends on r mod bw only
+      for (int e = 0; e < bw; ++e) {
+        const unsigned long long we = __shfl_sync(0xffffffffu, tb, e);
+        if (we) total += we * warp_count((unsigned long long)(org + e), active, tier, mm, bw_lg, bw, banks);
+      }
+      continue;
+    }
+    if (MC == 32 && tier == T_GLOBAL) {   // lanes = residues (see the class evaluation below)
+      const int64_t up = __shfl_up_sync(0xffffffffu, org, 1);
+      if (__all_sync(0xffffffffu, lane == 0 || !active || org >= up)) {
+        const int na = __popc(amask);
+        int64_t prev = ow + lane;
+        unsigned cnt = na > 0 ? 1u : 0u;
+#pragma unroll 4
+        for (int i = 1; i < na; ++i) {
+          const int64_t cur = __shfl_sync(0xffffffffu, org, i) + lane;
+          cnt += (unsigned)((cur >> 5) != (prev >> 5));
+          prev = cur;
+        }
+        unsigned long long part = W.T[lane] * cnt;
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        total += part;
+        continue;
+      }
+    }
     for (int c = 0; c < per; ++c) {
       unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < M && W.T[c * 32 + lane] != 0);
       while (nz) {
@@ -1225,6 +1311,7 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
     }
   }
   __syncwarp();
+  GS_SUB(14);
   for (int j = 0; j < ncls; ++j) {
     const bool active = ((j ? am1 : am0) >> lane) & 1u;
     const int64_t org = j ? o01 + rel1 : o00 + rel0;
@@ -1261,6 +1348,7 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
     }
   }
   __syncwarp();
+  GS_SUB(15);
   return total;
 }
 
@@ -1318,9 +1406,13 @@ __device__ void parallel_feats(double* v, const GsMachine& M, int n, const CF<ND
   v[F_TASKS_PER_CORE] = (double)kern.n_blocks / (double)M.num_sms;
 }
 
+
 template <int ND>
 __device__ __noinline__ void row_features(K1<ND>& k, WarpScr& W, int func, int si, bool inl, double* out) {
   const int lane = lane_id();
+#ifdef GS_PHASES
+  long long tsub = clock64();
+#endif
   const GsMachine& M = k.P->m;
   Misc& m = *k.misc;
   const CF<ND>& g = k.cf[func];
@@ -1380,6 +1472,7 @@ __device__ __noinline__ void row_features(K1<ND>& k, WarpScr& W, int func, int s
   }
   __syncwarp();
   const int ng = W.ngroups;
+  GS_SUB(8);
   // ---- unions: tasks (box, group); boxes 0 region, 1 lane, 2 point, 3 block
   const int nbox_tasks = 4 * ng;
   for (int t = lane; t < nbox_tasks; t += 32) {
@@ -1397,6 +1490,7 @@ __device__ __noinline__ void row_features(K1<ND>& k, WarpScr& W, int func, int s
     atomicAdd(&W.acc[box][W.gtier[gi]][1], (unsigned long long)lines);
   }
   __syncwarp();
+  GS_SUB(9);
   // ---- loads (block 0 of the host's kernel)
   // the default machine (32 B transactions, 32 banks x 4 B) gets the
   // compile-time-specialised counter
@@ -1415,8 +1509,10 @@ __device__ __noinline__ void row_features(K1<ND>& k, WarpScr& W, int func, int s
     if (r.tier != T_GLOBAL && r.tier != T_SHARED) continue;
     ld[r.tier] += tx(k.path + r.pbeg, r.plen, false, h, k.cf[r.producer], k.F[r.producer].elem_bytes, r.tier);
   }
+  GS_SUB(13);
   unsigned long long st = 0;
   if (!inl && (g.tier == T_GLOBAL || g.tier == T_SHARED)) st = tx(nullptr, 0, true, g, g, fn.elem_bytes, g.tier);
+  GS_SUB(10);
   // ---- working set at thread: fuse_at_thread children (featurize.py:482-492)
   int64_t wsc = 0;
   if (!inl) {
@@ -1426,6 +1522,7 @@ __device__ __noinline__ void row_features(K1<ND>& k, WarpScr& W, int func, int s
     }
     for (int o = 16; o; o >>= 1) wsc += __shfl_xor_sync(0xffffffffu, wsc, o);
   }
+  GS_SUB(11);
   int lerr = err;
   for (int o = 16; o; o >>= 1) lerr |= __shfl_xor_sync(0xffffffffu, lerr, o);
   if (lane == 0) {
@@ -1492,6 +1589,7 @@ __device__ __noinline__ void row_features(K1<ND>& k, WarpScr& W, int func, int s
   }
   __syncwarp();
   for (int i = lane; i < GS_NUM_FEATURES; i += 32) out[i] = W.feat[i];
+  GS_SUB(12);
 }
 
 // ---------------------------------------------------------------------------
@@ -1522,6 +1620,7 @@ __device__ __forceinline__ void bulk_wait(uint64_t* bar) {
 // memory; the candidate-independent pipeline descriptor is shared by the
 // CTA.  There is no CTA-wide barrier after the descriptor is staged, so the
 // serial parts of one candidate (resolve, prune) overlap other warps' rows.
+
 template <int ND>
 __global__ void __launch_bounds__(kK1MaxWarps * 32, 1)
 featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob, const GsDecision* __restrict__ dec,
@@ -1581,6 +1680,9 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   // full resolve anyway), and warps that drew cheap runs take more of them.
   Misc& m = *k.misc;
   unsigned long long st_cand = 0, st_inc = 0, st_rows = 0, st_emit = 0, st_geo = 0;   // (lane 0)
+#ifdef GS_PHASES
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tph = 0;
+#endif
   unsigned* work = reinterpret_cast<unsigned*>(gerr + 14);
   const int64_t nunits = (n + kUnit - 1) / kUnit;
   auto snap = [&](int64_t x) -> int64_t {
@@ -1605,6 +1707,9 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   if (lane == 0) { m.prev_valid = 0; m.same_struct = 0; m.ndec = 0; st_cand += c1 - c0; }
   __syncwarp();
   for (int64_t c = c0; c < c1; ++c) {
+#ifdef GS_PHASES
+    tph = clock64();
+#endif
     {
       const uint4* src = reinterpret_cast<const uint4*>(dec + c * S);
       uint4* dst = reinterpret_cast<uint4*>(k.dec);
@@ -1636,8 +1741,11 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
         if (!m.same_struct) m.nrows = 0;
       }
       __syncwarp();
+      GS_MARK(0);
       resolve<ND>(k);
+      GS_MARK(1);
       const int v = m.err ? 255 : prune_verdict<ND>(k);
+      GS_MARK(2);
       if (lane == 0) {
         if (m.err) { atomicOr(gerr, m.err); m.nrows = 0; }
         verdict[c] = (uint8_t)v;
@@ -1677,6 +1785,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     // warp wrote it: visible after __syncwarp), copied as one contiguous run
     // of 16-byte vectors with four loads in flight per lane; the dirty rows
     // are then recomputed over it
+    GS_MARK(3);
     if (diffable && nd < nr) {
       const int4* src = reinterpret_cast<const int4*>(feats + (int64_t)(c - 1) * L.R * GS_NUM_FEATURES);
       int4* dst = reinterpret_cast<int4*>(feats + (int64_t)c * L.R * GS_NUM_FEATURES);
@@ -1689,21 +1798,28 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
       for (; i < nv; i += 32) dst[i] = src[i];
       __syncwarp();
     }
+    GS_MARK(4);
     for (int q = 0; q < nd; ++q) {
       const int r = k.rowlist[q];
       const int key = k.rows[r];
       const int f = key >> 8, si = key & 255;
       row_features<ND>(k, W, f, si, k.cf[f].kind == K_INLINE, feats + ((int64_t)c * L.R + r) * GS_NUM_FEATURES);
     }
+    GS_MARK(5);
     for (int r = lane; r < nr; r += 32) {
       row_key[c * L.R + r] = k.rows[r];
       if (row_src) row_src[c * L.R + r] = rsrc[r];
     }
     __syncwarp();
+    GS_MARK(6);
     if (lane == 0) m.prev_valid = (m.err == 0) && feats != nullptr;
     __syncwarp();
   }
   }
+#ifdef GS_PHASES
+  if (lane == 0)
+    for (int i = 0; i < 7; ++i) atomicAdd(&g_phase[i], (unsigned long long)ph[i]);
+#endif
   if (lane == 0 && st_cand) {
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(gerr + 2);
     atomicAdd(ctr + 0, st_cand);
@@ -1802,6 +1918,15 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
 }
 
 // warps per CTA that fit the shared memory budget (one CTA per SM)
+int read_phases(long long* out) {
+  unsigned long long h[16];
+  if (cudaMemcpyFromSymbol(h, g_phase, sizeof(h)) != cudaSuccess) return -1;
+  for (int i = 0; i < 16; ++i) out[i] = (long long)h[i];
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+  return 0;
+}
+
 int featurize_warps(const Layout& L1, int max_smem) {
   int w = (max_smem - L1.warps) / L1.warp_bytes;
   return w < 1 ? 0 : (w > kK1MaxWarps ? kK1MaxWarps : w);

@@ -32,3 +32,16 @@ st = sc.stats()
 print({k: (v / 3 if k.startswith(("cand", "incr", "rows", "geo")) else v) for k, v in st.items()})
 print("rows computed per candidate:", st["rows_computed"] / max(1, st["candidates"]),
       "geometries per candidate:", st["geometries"] / max(1, st["candidates"]))
+ph = __import__("numpy").zeros(16, dtype="int64")
+sc.lib.gs_debug_phases(__import__("ctypes").c_void_p(ph.ctypes.data))
+if ph.sum():
+    names = ["diff", "resolve", "prune", "row flags", "copy", "rows", "writes"]
+    tot = ph[:7].sum()
+    print("phases:", {n: f"{100 * v / tot:.1f}%" for n, v in zip(names, ph[:7])})
+    sub = {"setup": ph[8], "unions": ph[9], "loads": ph[13], "store": ph[10], "ws": ph[11], "assembly": ph[12]}
+    st = sum(sub.values())
+    if st:
+        print("row phases:", {n: f"{100 * v / st:.1f}%" for n, v in sub.items()})
+    tx = {"T build": ph[7], "classes": ph[14], "evaluate": ph[15]}
+    if sum(tx.values()):
+        print("warp_tx phases:", {n: f"{100 * v / sum(tx.values()):.1f}%" for n, v in tx.items()})
