@@ -100,6 +100,13 @@ __device__ __forceinline__ int64_t wmax64(int64_t v) {
   return v;
 }
 
+__device__ __noinline__ int64_t div64_slow(int64_t a, int64_t b) { return a / b; }
+// a / b for a >= 0, b > 0: 32-bit division when both fit (all real extents)
+__device__ __forceinline__ int64_t udiv(int64_t a, int64_t b) {
+  if (((uint64_t)a | (uint64_t)b) <= 0x7FFFFFFFull) return (int64_t)((uint32_t)a / (uint32_t)b);
+  return div64_slow(a, b);
+}
+
 template <int ND>
 __device__ __forceinline__ int64_t prod_ext(const CF<ND>& c) {
   int64_t p = 1;
@@ -395,7 +402,7 @@ __device__ __noinline__ bool geometry_one(K1<ND>& k, int i) {
       ser[dd] = tiled ? d.serial[dd] : 1;
       thr[dd] = tiled ? d.thread[dd] : (dd == inner ? (e < 32 ? e : 32) : 1);
       int64_t st = (int64_t)ser[dd] * thr[dd];
-      int64_t b = (e + st - 1) / st;
+      int64_t b = udiv(e + st - 1, st);
       if (b < 1) b = 1;
       nb *= b; nt *= thr[dd]; sp *= ser[dd];
       c.rlo[dd] = 0; c.rhi[dd] = (int32_t)(b * st - 1);
@@ -466,7 +473,7 @@ __device__ __noinline__ bool geometry_one(K1<ND>& k, int i) {
 #pragma unroll
     for (int dd = 0; dd < ND; ++dd) {
       int s = (d.flags & 1) ? d.serial[dd] : 1;
-      int64_t t = (hi[dd] - lo[dd] + 1 + s - 1) / s;
+      int64_t t = hi[dd] - lo[dd] + 1 + s - 1 >= 0 ? udiv(hi[dd] - lo[dd] + 1 + s - 1, s) : (hi[dd] - lo[dd] + s) / s;
       if (t < 1) t = 1;
       c.rlo[dd] = (int32_t)lo[dd];
       c.rhi[dd] = (int32_t)(lo[dd] + t * s - 1);
@@ -676,7 +683,7 @@ __device__ int prune_verdict(const K1<ND>& k) {
       if (d.kind == GS_INLINE) ci += c.calls;
       else {
         ci += prod_ext(c) * c.n_threads * k.cf[c.kernel].n_blocks;
-        const int64_t w = (c.n_threads + M.warp_size - 1) / M.warp_size;
+        const int w = (c.n_threads + M.warp_size - 1) / M.warp_size;
         const double util = (double)c.n_threads / (double)(w * M.warp_size);
         if (util < th.warp_utilization_floor) code = GS_PRUNE_WARP_UTIL;
         else if (c.has_serial && (int64_t)c.serial_prod > th.unroll_budget) code = GS_PRUNE_SERIAL;
@@ -1051,6 +1058,98 @@ __device__ __forceinline__ unsigned warp_count(unsigned long long a, bool active
 //    For shared memory the count depends on the residue only mod the bank
 //    width (adding whole words rotates the banks), so at most bank-width
 //    evaluations are needed per class.
+// Histogram of the emitted instructions' address constants modulo Q (a
+// power of two <= 32), lane = residue, all in registers: per-dim coordinate
+// counts, window taps and the byte-stride map are shuffles (odd multipliers
+// permute Z/Q; a factor 2^a folds the top a bits), and the convolution into
+// the running histogram runs over its nonzero residues.  Q = 32: global
+// 32-byte segments.  Q = bank width: shared banks, whose count depends on
+// the constant only modulo the bank width.  Lanes >= Q return 0.
+template <int ND, int Q>
+__device__ unsigned long long residue_hist(const GsAccess* A, const int16_t* path, int plen, bool identity,
+                                           const CF<ND>& h, const int64_t* bs, WarpScr& W, int& err) {
+  constexpr int QL = Q == 32 ? 5 : Q == 16 ? 4 : Q == 8 ? 3 : Q == 4 ? 2 : Q == 2 ? 1 : 0;
+  const int lane = lane_id();
+  const bool mine = lane < Q;
+  const ModM<Q> mq(Q);
+  unsigned long long T = lane == 0;
+  for (int d = 0; d < ND; ++d) {
+    const int e = h.ext[d];
+    unsigned long long H = 0;
+    if (identity || !h.unrolled) {
+      if (mine) H = mq.count_in(0, e - 1, lane);
+      if (!identity) {
+#pragma unroll 1
+        for (int q = 0; q < plen; ++q) {
+          const GsAccess& x = A[path[q]];
+          const int64_t s = x.s[d], wl = x.lo[d], wh = x.hi[d];
+          unsigned long long S = 0;
+          if (wh - wl + 1 >= Q) {
+            unsigned nz = __ballot_sync(0xffffffffu, mine && H != 0);
+            while (nz) {
+              const int r = __ffs(nz) - 1; nz &= nz - 1;
+              const unsigned long long hv = __shfl_sync(0xffffffffu, H, r);
+              S += hv * mq.count_in(wl, wh, (int)((lane - (int64_t)r * s) & (Q - 1)));
+            }
+          } else if (s & 1) {
+            int inv = (int)s;
+            inv *= 2 - (int)s * inv;
+            inv *= 2 - (int)s * inv;
+#pragma unroll 1
+            for (int64_t w = wl; w <= wh; ++w)
+              S += __shfl_sync(0xffffffffu, H, (int)(((lane - w) * inv) & (Q - 1)));
+          } else {   // even stride: scatter through shared memory
+            if (mine) { W.H[lane] = H; W.S[lane] = 0; }
+            __syncwarp();
+            if (mine && H) {
+              const int64_t base = (int64_t)lane * s;
+#pragma unroll 1
+              for (int64_t w = wl; w <= wh; ++w) atomicAdd(&W.S[(int)((base + w) & (Q - 1))], H);
+            }
+            __syncwarp();
+            if (mine) S = W.S[lane];
+            __syncwarp();
+          }
+          H = mine ? S : 0;
+        }
+      }
+    } else {
+      Iv buf[kLaneIv];
+      const int n = footprint(A, path, plen, d, 0, e - 1, buf, kLaneIv, err);
+#pragma unroll 1
+      for (int i = 0; i < n; ++i) if (mine) H += mq.count_in(buf[i].lo, buf[i].hi, lane);
+    }
+    // scale by the byte stride of dim d: S2[(r * bm) mod Q] += H[r]
+    const int bm = (int)(bs[d] & (Q - 1));
+    unsigned long long S2;
+    if (bm == 0) {
+      unsigned long long u = H;
+      for (int o = 16; o; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+      S2 = lane == 0 ? u : 0;
+    } else {
+      const int a = __ffs(bm) - 1, odd = bm >> a, lo = QL - a;
+      int inv = odd;
+      inv *= 2 - odd * inv;
+      inv *= 2 - odd * inv;
+      unsigned long long u = H;
+      for (int o = 1 << lo; o < Q; o <<= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+      const int src = ((lane >> a) * inv) & ((1 << lo) - 1);
+      const unsigned long long g = __shfl_sync(0xffffffffu, u, src);
+      S2 = mine && (lane & ((1 << a) - 1)) == 0 ? g : 0;
+    }
+    // T <- T (*) S2 (cyclic)
+    unsigned long long Tn = 0;
+    unsigned nz = __ballot_sync(0xffffffffu, mine && T != 0);
+    while (nz) {
+      const int r = __ffs(nz) - 1; nz &= nz - 1;
+      const unsigned long long tr = __shfl_sync(0xffffffffu, T, r);
+      Tn += tr * __shfl_sync(0xffffffffu, S2, (lane - r) & (Q - 1));
+    }
+    T = mine ? Tn : 0;
+  }
+  return T;
+}
+
 // MC / BW / NB: compile-time period, bank width and bank count for the
 // common machines (0 = read them from Mc at run time).
 template <int ND, int MC, int BW, int NB>
@@ -1077,99 +1176,109 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
         for (int q = 0; q < plen; ++q) ts[d] *= A[path[q]].s[d];
     }
   }
-  for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.T[r] = (r == 0); }
-  __syncwarp();
-  for (int d = 0; d < ND; ++d) {
-    const int e = h.ext[d];
-    // per-dim histogram of relative coordinates (mod M) into H
-    if (identity || !h.unrolled) {
-      for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.H[r] = mm.count_in(0, e - 1, r); }
-      __syncwarp();
-      if (!identity) {
-        for (int q = 0; q < plen; ++q) {
-          const GsAccess& x = A[path[q]];
-          const int64_t s = x.s[d], wl = x.lo[d], wh = x.hi[d];
-          // S[k] = sum_r H[r] * #{w in [wl,wh] : r*s + w = k (mod M)}
-          for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.S[r] = 0; }
-          __syncwarp();
-          if (wh - wl + 1 < M) {       // short window: scatter each residue's taps
-            for (int j = 0; j < per; ++j) {
-              const int r = lane + 32 * j;
-              if (r >= M) continue;
-              const unsigned long long hv = W.H[r];
-              if (!hv) continue;
-              const int64_t base = (int64_t)r * s;
-              #pragma unroll 1
-              for (int64_t w = wl; w <= wh; ++w) atomicAdd(&W.S[mm.pmod(base + w)], hv);
-            }
-          } else {
-            for (int c = 0; c < per; ++c) {
-              unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < M && W.H[c * 32 + lane] != 0);
-              while (nz) {
-                const int b = __ffs(nz) - 1; nz &= nz - 1;
-                const int r = c * 32 + b;
+  // shared banks on the default machine: only the constants mod the 4-byte
+  // bank width matter (see the class counting below)
+  constexpr bool kFold4 = MC == 128 && BW == 4;
+  unsigned long long tb4 = 0;
+  if (MC == 32) {
+    W.T[lane] = residue_hist<ND, 32>(A, path, plen, identity, h, bs, W, err);
+    __syncwarp();
+  } else if (kFold4 && tier != T_GLOBAL) {
+    tb4 = residue_hist<ND, 4>(A, path, plen, identity, h, bs, W, err);
+  } else {
+    for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.T[r] = (r == 0); }
+    __syncwarp();
+    for (int d = 0; d < ND; ++d) {
+      const int e = h.ext[d];
+      // per-dim histogram of relative coordinates (mod M) into H
+      if (identity || !h.unrolled) {
+        for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.H[r] = mm.count_in(0, e - 1, r); }
+        __syncwarp();
+        if (!identity) {
+          for (int q = 0; q < plen; ++q) {
+            const GsAccess& x = A[path[q]];
+            const int64_t s = x.s[d], wl = x.lo[d], wh = x.hi[d];
+            // S[k] = sum_r H[r] * #{w in [wl,wh] : r*s + w = k (mod M)}
+            for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.S[r] = 0; }
+            __syncwarp();
+            if (wh - wl + 1 < M) {       // short window: scatter each residue's taps
+              for (int j = 0; j < per; ++j) {
+                const int r = lane + 32 * j;
+                if (r >= M) continue;
                 const unsigned long long hv = W.H[r];
-                const int64_t sh = mm.pmod((int64_t)r * s);
-                for (int j = 0; j < per; ++j) {
-                  const int k = lane + 32 * j;
-                  if (k < M) W.S[k] += hv * mm.count_in(wl, wh, mm.pmod(k - sh));
+                if (!hv) continue;
+                const int64_t base = (int64_t)r * s;
+                #pragma unroll 1
+                for (int64_t w = wl; w <= wh; ++w) atomicAdd(&W.S[mm.pmod(base + w)], hv);
+              }
+            } else {
+              for (int c = 0; c < per; ++c) {
+                unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < M && W.H[c * 32 + lane] != 0);
+                while (nz) {
+                  const int b = __ffs(nz) - 1; nz &= nz - 1;
+                  const int r = c * 32 + b;
+                  const unsigned long long hv = W.H[r];
+                  const int64_t sh = mm.pmod((int64_t)r * s);
+                  for (int j = 0; j < per; ++j) {
+                    const int k = lane + 32 * j;
+                    if (k < M) W.S[k] += hv * mm.count_in(wl, wh, mm.pmod(k - sh));
+                  }
                 }
               }
             }
+            __syncwarp();
+            for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.H[r] = W.S[r]; }
+            __syncwarp();
           }
-          __syncwarp();
-          for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.H[r] = W.S[r]; }
-          __syncwarp();
         }
+      } else {
+        // unrolled: unique points of the chain footprint of [0, e-1]
+        Iv buf[kLaneIv];
+        int n = footprint(A, path, plen, d, 0, e - 1, buf, kLaneIv, err);
+        for (int j = 0; j < per; ++j) {
+          int r = lane + 32 * j;
+          if (r >= M) continue;
+          unsigned long long c = 0;
+          #pragma unroll 1
+          for (int i = 0; i < n; ++i) c += mm.count_in(buf[i].lo, buf[i].hi, r);
+          W.H[r] = c;
+        }
+        __syncwarp();
       }
-    } else {
-      // unrolled: unique points of the chain footprint of [0, e-1]
-      Iv buf[kLaneIv];
-      int n = footprint(A, path, plen, d, 0, e - 1, buf, kLaneIv, err);
+      // scale by the byte stride of dim d, then convolve into T
+      const int64_t bm = mm.pmod(bs[d]);
+      for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.S[r] = 0; }
+      __syncwarp();
       for (int j = 0; j < per; ++j) {
         int r = lane + 32 * j;
-        if (r >= M) continue;
-        unsigned long long c = 0;
-        #pragma unroll 1
-        for (int i = 0; i < n; ++i) c += mm.count_in(buf[i].lo, buf[i].hi, r);
-        W.H[r] = c;
+        if (r < M && W.H[r]) atomicAdd(&W.S[mm.pmod((int64_t)r * bm)], W.H[r]);
+      }
+      // nonzero residues of T, then H[k] = sum_r T[r] S[k - r] (lane per k)
+      int nnz = 0;
+      for (int c = 0; c < per; ++c) {
+        const int r = c * 32 + lane;
+        const bool t = r < M && W.T[r] != 0;
+        const unsigned b = __ballot_sync(0xffffffffu, t);
+        if (t) W.nz[nnz + __popc(b & ((1u << lane) - 1))] = (int16_t)r;
+        nnz += __popc(b);
       }
       __syncwarp();
-    }
-    // scale by the byte stride of dim d, then convolve into T
-    const int64_t bm = mm.pmod(bs[d]);
-    for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.S[r] = 0; }
-    __syncwarp();
-    for (int j = 0; j < per; ++j) {
-      int r = lane + 32 * j;
-      if (r < M && W.H[r]) atomicAdd(&W.S[mm.pmod((int64_t)r * bm)], W.H[r]);
-    }
-    // nonzero residues of T, then H[k] = sum_r T[r] S[k - r] (lane per k)
-    int nnz = 0;
-    for (int c = 0; c < per; ++c) {
-      const int r = c * 32 + lane;
-      const bool t = r < M && W.T[r] != 0;
-      const unsigned b = __ballot_sync(0xffffffffu, t);
-      if (t) W.nz[nnz + __popc(b & ((1u << lane) - 1))] = (int16_t)r;
-      nnz += __popc(b);
-    }
-    __syncwarp();
-    for (int j = 0; j < per; ++j) {
-      const int k = lane + 32 * j;
-      if (k >= M) continue;
-      unsigned long long acc = 0;
-      #pragma unroll 1
-      for (int i = 0; i < nnz; ++i) {
-        const int r = W.nz[i];
-        acc += W.T[r] * W.S[mm.pmod(k - r)];
+      for (int j = 0; j < per; ++j) {
+        const int k = lane + 32 * j;
+        if (k >= M) continue;
+        unsigned long long acc = 0;
+        #pragma unroll 1
+        for (int i = 0; i < nnz; ++i) {
+          const int r = W.nz[i];
+          acc += W.T[r] * W.S[mm.pmod(k - r)];
+        }
+        W.H[k] = acc;
       }
-      W.H[k] = acc;
+      __syncwarp();
+      for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.T[r] = W.H[r]; }
+      __syncwarp();
     }
-    __syncwarp();
-    for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.T[r] = W.H[r]; }
-    __syncwarp();
   }
-
   GS_SUB(7);
   // ---- count: warp-pattern classes ---------------------------------------
   const int nwarps = (h.n_threads + 31) / 32;
@@ -1184,7 +1293,9 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
   const int pp = (P + 31) / 32;
   // TB[e] = sum of T[r] over r = e (mod P): lane e (fold) holds it
   unsigned long long tb = 0;
-  if (fold) {
+  if (kFold4 && fold) {
+    tb = tb4;                      // lane e < 4 holds TB[e]
+  } else if (fold) {
     for (int j = 0; j < per; ++j) {
       const int r = lane + 32 * j;
       const unsigned long long v = r < M ? W.T[r] : 0ull;
@@ -1193,6 +1304,53 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
       for (int o = bw; o < 32; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
       tb += sum;
     }
+  }
+  if (MC == 32 && tier == T_GLOBAL) {
+    // 32-byte segments, lanes = residues.  For a warp whose active lane
+    // addresses are non-decreasing, lane i > 0 opens a new segment for the
+    // residues r with ((a[i-1] + r) mod 32) >= 32 - d (d = a[i] - a[i-1]),
+    // a cyclic interval of d residues (all of them when d >= 32), so the
+    // T-weighted count of the warp is a sum of interval sums of T: one
+    // prefix scan of T per read, then O(1) per lane per emulated warp.
+    const unsigned long long tv = W.T[lane];
+    unsigned long long incl = tv;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    const unsigned long long pex = incl - tv;                       // sum of T[0..lane)
+    const unsigned long long tsum = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long total = 0;
+    WarpWalk<ND> walk(h, ts, bs, cst, lane);
+    for (int w = 0; w < nwarps; ++w, walk.next()) {
+      bool active;
+      const int64_t org = walk.origin(active);
+      const int64_t up = __shfl_up_sync(0xffffffffu, org, 1);
+      if (__all_sync(0xffffffffu, lane == 0 || !active || org >= up)) {
+        unsigned long long c = 0;
+        int lo = 0, hi = 0;
+        if (active && lane > 0) {
+          const int64_t d = org - up;
+          if (d >= 32) c = tsum;
+          else { lo = (int)((32 - d - (up & 31)) & 31); hi = lo + (int)d; }
+        } else if (active) {
+          c = tsum;                                                 // lane 0: the first segment
+        }
+        const unsigned long long plo = __shfl_sync(0xffffffffu, pex, lo);
+        const unsigned long long phi = __shfl_sync(0xffffffffu, pex, hi & 31);
+        if (hi > lo) c = hi <= 32 ? (hi == 32 ? tsum : phi) - plo : (tsum - plo) + phi;
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        total += c;
+      } else {
+        for (int r = 0; r < 32; ++r) {
+          const unsigned long long wr = __shfl_sync(0xffffffffu, tv, r);
+          if (wr) total += wr * warp_count((unsigned long long)(org + r), active, tier, mm, bw_lg, bw, banks);
+        }
+      }
+    }
+    __syncwarp();
+    GS_SUB(14);
+    return total;
   }
   // two classes: weights in H (class 0) and S (class 1); registers are
   // named, not indexed, so they stay out of local memory
@@ -1368,9 +1526,10 @@ enum FeatIdx {
 
 template <int ND>
 __device__ void parallel_feats(double* v, const GsMachine& M, int n, const CF<ND>& kern) {
-  // featurize.py:317-363
-  const int64_t kt = kern.k_threads, ws = M.warp_size;
-  const int64_t aw = (n + ws - 1) / ws;
+  // featurize.py:317-363.  Thread / warp / block counts are < 2^31: 32-bit
+  // integer division (the 64-bit routine is ~70 dependent instructions).
+  const int kt = kern.k_threads, ws = M.warp_size;
+  const int aw = (n + ws - 1) / ws;
   v[F_NUM_BLOCKS] = (double)kern.n_blocks;
   v[F_WARPS_PB] = (double)((kt + ws - 1) / ws);
   v[F_ACTIVE_WARPS] = (double)aw;
@@ -1378,11 +1537,13 @@ __device__ void parallel_feats(double* v, const GsMachine& M, int n, const CF<ND
   v[F_WARP_UTIL] = (double)n / (double)(ws * aw);
   v[F_IDLE] = (double)(ws * aw - n) / (double)M.max_threads_per_block;
   v[F_BLOCK_OCC] = (double)kt / (double)M.max_threads_per_block;
-  int64_t wpb = (kt + ws - 1) / ws;
+  int wpb = (kt + ws - 1) / ws;
   if (wpb < 1) wpb = 1;
-  int64_t by_shared;
+  int by_shared;
   if (kern.k_shared > 0) {
-    by_shared = M.shared_mem_per_sm / kern.k_shared;
+    // shared_mem_per_sm fits 32 bits; a kernel needing more than that
+    // fits zero blocks
+    by_shared = kern.k_shared > (int64_t)M.shared_mem_per_sm ? 0 : M.shared_mem_per_sm / (int)kern.k_shared;
     if (by_shared < 1) by_shared = 1;
     double o = (double)kern.k_shared / (double)M.shared_mem_per_block_limit;
     v[F_SH_OCC] = o < 1.0 ? o : 1.0;
@@ -1390,13 +1551,13 @@ __device__ void parallel_feats(double* v, const GsMachine& M, int n, const CF<ND
     by_shared = M.max_active_blocks_per_sm;
     v[F_SH_OCC] = 0.0;
   }
-  int64_t mb = M.max_active_blocks_per_sm;
+  const int mb = M.max_active_blocks_per_sm;
   v[F_SH_LIMIT] = (double)(by_shared < mb ? by_shared : mb) / (double)mb;
-  int64_t act = mb;
+  int act = mb;
   if (by_shared < act) act = by_shared;
   if (M.max_active_warps_per_sm / wpb < act) act = M.max_active_warps_per_sm / wpb;
   if (act < 1) act = 1;
-  int64_t awsm = act * wpb;
+  int64_t awsm = (int64_t)act * wpb;
   if (awsm > M.max_active_warps_per_sm) awsm = M.max_active_warps_per_sm;
   v[F_MAX_WARP_OCC] = (double)awsm / (double)M.max_active_warps_per_sm;
   v[F_MAX_BLOCK_OCC] = (double)act / (double)mb;
