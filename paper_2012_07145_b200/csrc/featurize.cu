@@ -1352,6 +1352,26 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
     GS_SUB(14);
     return total;
   }
+  if (kFold4 && fold) {
+    // shared banks, 4-byte words: each emulated warp is evaluated once per
+    // constant residue mod 4 that occurs (one, for 4-byte elements)
+    const unsigned ew = __ballot_sync(0xffffffffu, lane < 4 && tb != 0) & 0xFu;
+    unsigned long long total = 0;
+    WarpWalk<ND> walk(h, ts, bs, cst, lane);
+    for (int w = 0; w < nwarps; ++w, walk.next()) {
+      bool active;
+      const int64_t org = walk.origin(active);
+      unsigned m4 = ew;
+      while (m4) {
+        const int e = __ffs(m4) - 1; m4 &= m4 - 1;
+        const unsigned long long we = __shfl_sync(0xffffffffu, tb, e);
+        total += we * warp_count((unsigned long long)(org + e), active, tier, mm, bw_lg, bw, banks);
+      }
+    }
+    __syncwarp();
+    GS_SUB(14);
+    return total;
+  }
   // two classes: weights in H (class 0) and S (class 1); registers are
   // named, not indexed, so they stay out of local memory
   for (int j = 0; j < pp; ++j) { int r = lane + 32 * j; if (r < P) { W.H[r] = 0; W.S[r] = 0; } }
