@@ -267,10 +267,10 @@ def run_gpu(args):
     stream = torch.cuda.current_stream()
     plan = shard.StepPlan(sc, N, world, rank, PASS_INDEX, PHASE_SEED, BEAM, 2.0, NUM_PASSES, TIE_BAND)
 
-    k1_ms = []
+    phase_ms = {}
 
-    def step(d, timed_k1=False):
-        return plan.run(d, k1_times=k1_ms if timed_k1 else None)
+    def step(d, timed=False):
+        return plan.run(d, times=phase_ms if timed else None)
 
     for _ in range(args.warmup):
         step(dec)
@@ -279,7 +279,7 @@ def run_gpu(args):
     if world > 1:
         dist.barrier()
     l0 = lib.gs_launch_count()
-    k1_ms.clear()
+    phase_ms.clear()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         torch.cuda.synchronize()
@@ -287,7 +287,7 @@ def run_gpu(args):
             dist.barrier()
         ev0.record(stream)
         for _ in range(args.steps):
-            res = step(dec, timed_k1=True)
+            res = step(dec, timed=True)
         ev1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -324,7 +324,8 @@ def run_gpu(args):
     if rank == 0:
         R = sc.R
         n_local = plan.local_count
-        k1 = float(np.mean(k1_ms)) if k1_ms else None
+        k1 = phase_ms["featurize"] / args.steps if phase_ms else None
+        breakdown = {k: round(v / args.steps, 3) for k, v in phase_ms.items()}
         # K1 algorithmic bytes per launch: 16 B decision record per row in,
         # 448 B fp64 feature row + 4 B row key per row out, 4+1 B per candidate
         bytes_k1 = n_local * (R * (16 + 448 + 4) + 5)
@@ -364,6 +365,7 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "e2e": {"value": N / (e / 1e3), "unit": UNIT, "ms_per_step": e,
                     "h2d_bytes_per_step": int(out["h2d_bytes"]), "d2h_bytes_per_step": int(out["d2h_bytes"])},
+            "step_breakdown_ms": breakdown,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "beam": res["beam"][:8],

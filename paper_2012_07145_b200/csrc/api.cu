@@ -20,7 +20,8 @@ int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* f
                 const int32_t* n_rows, const int32_t* row_src, int64_t n, int R, double* total, double* row_cost,
                 double* basis_gh, int num_sms, cudaStream_t st);
 int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, const int32_t* sorted_funcs,
-                const uint8_t* names, const int32_t* name_off, uint64_t* out, uint8_t* head, cudaStream_t st);
+                const uint8_t* names, const int32_t* name_off, uint64_t* out, uint8_t* head, int repr_bound,
+                int num_sms, cudaStream_t st);
 int64_t select_workspace_bytes(int64_t n);
 int select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, uint64_t phase_seed, void* ws,
                 int64_t ws_bytes, int64_t* rep_idx, int64_t* n_reps, int64_t* n_rejects, int64_t* rej_idx,
@@ -64,6 +65,7 @@ struct GsPipeline {
   int reuse = 1;
   int nwarps = kK1MaxWarps;
   int last_warps = 0, last_slice = 0;   // K1 launch shape (diagnostics)
+  int repr_bound = 1 << 30;             // longest possible canonical repr (K3)
   uint8_t* hscratch = nullptr;   // K3 run-head flags (grow-only)
   uint8_t* gscratch = nullptr;   // K1 spilled structure arrays (grow-only)
   uint8_t* k1heads = nullptr;    // K1 run-head flags (grow-only)
@@ -168,6 +170,15 @@ int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
   CK(cudaMalloc(&p->sorted, 4 * h.nf));
   CK(cudaMemcpy(p->sorted, sorted.data(), 4 * h.nf, cudaMemcpyHostToDevice));
   const int nb = d->name_off[h.nf];
+  {   // longest canonical repr any decision log can produce (K3 buffer choice):
+      // header + per func "(name, 'fuse_at_thread', kernel, consumer, False, False), "
+    int maxn = 4;
+    for (int f = 0; f < h.nf; ++f) maxn = std::max(maxn, d->name_off[f + 1] - d->name_off[f]);
+    long long b = 16;
+    for (int f = 0; f < h.nf; ++f)
+      b += 2 + 1 + (d->name_off[f + 1] - d->name_off[f]) + 2 + 16 + 2 + maxn + 2 + maxn + 14 + 1;
+    p->repr_bound = (int)std::min<long long>(b, 1 << 30);
+  }
   CK(cudaMalloc(&p->names, std::max(1, nb)));
   CK(cudaMemcpy(p->names, d->name_repr, nb, cudaMemcpyHostToDevice));
   CK(cudaMalloc(&p->name_off, 4 * (h.nf + 1)));
@@ -305,7 +316,7 @@ int gs_struct_hash(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, int
     p->hcap = n;
   }
   int rc = launch_hash(dec, n, S, p->host.nf, depth, p->sorted, p->names, p->name_off, out, p->hscratch,
-                       (cudaStream_t)stream);
+                       p->repr_bound, p->num_sms, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "too many funcs for the hash kernel");
   CK(cudaGetLastError());
   return GS_OK;

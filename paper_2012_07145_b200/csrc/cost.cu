@@ -107,7 +107,28 @@ __device__ double stage_row_cost(const NetDev& net, const double* __restrict__ s
 #pragma unroll
   for (int o = 0; o < GS_NUM_COEFFS; ++o) zo[o] = bo[o];
   const double* hp = net.hoisted + (int64_t)stage * H;
-  for (int i = 0; i < H; ++i) {
+  // four hidden units at a time: four independent FMA chains over the
+  // embedding (the single chain is latency-bound), same per-unit order
+  int i = 0;
+  for (; i + 4 <= H; i += 4) {
+    double z0 = __ldg(hp + i), z1 = __ldg(hp + i + 1), z2 = __ldg(hp + i + 2), z3 = __ldg(hp + i + 3);
+#pragma unroll
+    for (int j = 0; j < MAXE; ++j)
+      if (j < E) {
+        const double* wr = whs + j * H + i;
+        z0 = fma(es[j], wr[0], z0); z1 = fma(es[j], wr[1], z1);
+        z2 = fma(es[j], wr[2], z2); z3 = fma(es[j], wr[3], z3);
+      }
+    const double zz[4] = {z0, z1, z2, z3};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (zz[u] > 0.0) {
+#pragma unroll
+        for (int o = 0; o < GS_NUM_COEFFS; ++o) zo[o] = fma(zz[u], wo[(i + u) * GS_NUM_COEFFS + o], zo[o]);
+      }
+    }
+  }
+  for (; i < H; ++i) {
     double z = __ldg(hp + i);
 #pragma unroll
     for (int j = 0; j < MAXE; ++j) if (j < E) z = fma(es[j], whs[j * H + i], z);

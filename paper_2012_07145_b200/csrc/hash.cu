@@ -194,6 +194,151 @@ __global__ void hash_kernel(const GsDecision* __restrict__ dec, int64_t n, int S
   out[c] = b.final();
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-candidate variant: the 32 lanes render the canonical repr in
+// parallel (one decision entry per lane, offsets by a warp scan of entry
+// lengths) into this warp's shared-memory buffer, then one lane runs the
+// blake2b compressions over it.  Used whenever the longest possible repr
+// fits the buffer (kHashBuf); the thread-per-candidate kernel above covers
+// the rest.
+constexpr int kHashBuf = 8192;
+constexpr int kHashWarps = 4;   // warps per block
+
+__device__ __forceinline__ int cstr_len(const char* s) { int n = 0; while (s[n]) ++n; return n; }
+__device__ __forceinline__ int put(uint8_t* buf, int o, const char* s) { while (*s) buf[o++] = (uint8_t)*s++; return o; }
+
+__device__ __forceinline__ uint64_t blake_buf(const uint8_t* buf, int len) {
+  uint64_t h[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) h[i] = kIV[i];
+  h[0] ^= 0x01010000ULL ^ 8ULL;
+  const int nblk = len == 0 ? 1 : (len + 127) / 128;
+  for (int b = 0; b < nblk; ++b) {
+    uint64_t m[16], v[16];
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(buf + 128 * b);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) m[i] = w[i];
+    const bool last = b == nblk - 1;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { v[i] = h[i]; v[i + 8] = kIV[i]; }
+    v[12] ^= (uint64_t)(last ? len : 128 * (b + 1));
+    if (last) v[14] = ~v[14];
+    blake_round<0>(v, m); blake_round<1>(v, m); blake_round<2>(v, m); blake_round<3>(v, m);
+    blake_round<4>(v, m); blake_round<5>(v, m); blake_round<6>(v, m); blake_round<7>(v, m);
+    blake_round<8>(v, m); blake_round<9>(v, m); blake_round<10>(v, m); blake_round<11>(v, m);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[i] ^= v[i] ^ v[i + 8];
+  }
+  return h[0];
+}
+
+__global__ void __launch_bounds__(kHashWarps * 32) hash_warp_kernel(
+    const GsDecision* __restrict__ dec, int64_t n, int S, int nf, int depth, const int32_t* __restrict__ sorted_funcs,
+    const uint8_t* __restrict__ names, const int32_t* __restrict__ name_off, uint64_t* __restrict__ out,
+    const uint8_t* __restrict__ head) {
+  extern __shared__ __align__(16) uint8_t smh[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint8_t* buf = smh + wib * (kHashBuf + 2 * kHashMaxFuncs);
+  int16_t* didx = reinterpret_cast<int16_t*>(buf + kHashBuf);
+  const int64_t nwarps = (int64_t)gridDim.x * kHashWarps;
+  for (int64_t c = (int64_t)blockIdx.x * kHashWarps + wib; c < n; c += nwarps) {
+    if (head && !head[c]) continue;
+    const GsDecision* d = dec + c * S;
+    for (int f = lane; f < nf; f += 32) didx[f] = -1;
+    __syncwarp();
+    for (int i = lane; i < S; i += 32) {
+      const int f = d[i].func;
+      if (f != 0xFFFF && f < nf) didx[f] = (int16_t)i;
+    }
+    __syncwarp();
+    int pos;
+    if (depth == 0) {
+      if (lane == 0) put(buf, 0, "('kernels', (");
+      pos = 13;
+    } else {
+      if (lane == 0) { buf[0] = '('; buf[1] = (uint8_t)('0' + depth); put(buf, 2, ", ("); }
+      pos = 5;
+    }
+    int cnt = 0;
+    for (int q0 = 0; q0 < nf; q0 += 32) {
+      const int q = q0 + lane;
+      const int f = q < nf ? sorted_funcs[q] : -1;
+      const int i = f >= 0 ? didx[f] : -1;
+      const bool incl = i >= 0 && (depth > 0 || d[i].kind == GS_ROOT);
+      const unsigned bal = __ballot_sync(0xffffffffu, incl);
+      const int before = cnt + __popc(bal & ((1u << lane) - 1));
+      int len = 0, kf = -1;
+      if (incl) {
+        const int nl = name_off[f + 1] - name_off[f];
+        len = (before ? 2 : 0) + nl;
+        if (depth > 0) {
+          // kernel_of (loopnest.py:87-94)
+          int ki = i, guard = 0;
+          kf = f;
+          while (ki >= 0 && (d[ki].kind == GS_FUSE_BLOCK || d[ki].kind == GS_FUSE_THREAD) && guard++ < nf) {
+            kf = d[ki].consumer;
+            ki = kf < nf ? didx[kf] : -1;
+          }
+          if (ki < 0 || d[ki].kind == GS_INLINE) kf = -1;
+          len += 1 + 2 + cstr_len(kind_repr(d[i].kind)) + 2 +
+                 (kf >= 0 ? name_off[kf + 1] - name_off[kf] : 4) + 1;
+          if (depth >= 2) {
+            const int cf = d[i].consumer;
+            len += 2 + (cf == 0xFFFF ? 4 : name_off[cf + 1] - name_off[cf]);
+          }
+          if (depth >= 3) len += ((d[i].flags & 1) ? 6 : 7) + ((d[i].flags & 2) ? 6 : 7);
+        }
+      }
+      int ex = len;   // exclusive scan of entry lengths
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, ex, o);
+        if (lane >= o) ex += u;
+      }
+      const int tot = __shfl_sync(0xffffffffu, ex, 31);
+      ex -= len;
+      if (incl && pos + ex + len <= kHashBuf) {
+        int o = pos + ex;
+        if (before) { buf[o++] = ','; buf[o++] = ' '; }
+        if (depth > 0) buf[o++] = '(';
+        for (int k = name_off[f]; k < name_off[f + 1]; ++k) buf[o++] = names[k];
+        if (depth > 0) {
+          o = put(buf, o, ", ");
+          o = put(buf, o, kind_repr(d[i].kind));
+          o = put(buf, o, ", ");
+          if (kf >= 0) { for (int k = name_off[kf]; k < name_off[kf + 1]; ++k) buf[o++] = names[k]; }
+          else o = put(buf, o, "None");
+          if (depth >= 2) {
+            o = put(buf, o, ", ");
+            const int cf = d[i].consumer;
+            if (cf == 0xFFFF) o = put(buf, o, "None");
+            else for (int k = name_off[cf]; k < name_off[cf + 1]; ++k) buf[o++] = names[k];
+          }
+          if (depth >= 3) {
+            o = put(buf, o, (d[i].flags & 1) ? ", True" : ", False");
+            o = put(buf, o, (d[i].flags & 2) ? ", True" : ", False");
+          }
+          buf[o++] = ')';
+        }
+      }
+      pos += tot;
+      cnt += __popc(bal);
+    }
+    // trailer, zero padding of the last block, compression
+    int len = pos + (cnt == 1 ? 1 : 0) + 2;
+    if (lane == 0 && len <= kHashBuf) {
+      int o = pos;
+      if (cnt == 1) buf[o++] = ',';
+      buf[o++] = ')';
+      buf[o++] = ')';
+    }
+    const int padded = ((len + 127) / 128) * 128;
+    for (int k = len + lane; k < padded && k < kHashBuf; k += 32) buf[k] = 0;
+    __syncwarp();
+    if (lane == 0) out[c] = len <= kHashBuf ? blake_buf(buf, len) : 0ull;
+    __syncwarp();
+  }
+}
+
 // non-head candidates copy the hash of the head of their run
 __global__ void hash_fill_kernel(const uint8_t* __restrict__ head, int64_t n, uint64_t* __restrict__ out) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -204,7 +349,8 @@ __global__ void hash_fill_kernel(const uint8_t* __restrict__ head, int64_t n, ui
 }
 
 int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, const int32_t* sorted_funcs,
-                const uint8_t* names, const int32_t* name_off, uint64_t* out, uint8_t* head, cudaStream_t st) {
+                const uint8_t* names, const int32_t* name_off, uint64_t* out, uint8_t* head, int repr_bound,
+                int num_sms, cudaStream_t st) {
   if (n == 0) return 0;
   if (nf > kHashMaxFuncs) return -1;
   if (depth > 3) depth = 3;
@@ -213,7 +359,16 @@ int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, cons
     hash_head_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(dec, n, S, head);
     g_launch_count++;
   }
-  hash_kernel<<<(unsigned)blocks, 128, 0, st>>>(dec, n, S, nf, depth, sorted_funcs, names, name_off, out, head);
+  if (repr_bound <= kHashBuf) {
+    const int smem = kHashWarps * (kHashBuf + 2 * kHashMaxFuncs);
+    cudaFuncSetAttribute(hash_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int64_t want = (n + kHashWarps - 1) / kHashWarps;
+    const int grid = (int)(want < (int64_t)num_sms * 8 ? want : (int64_t)num_sms * 8);
+    hash_warp_kernel<<<grid, kHashWarps * 32, smem, st>>>(dec, n, S, nf, depth, sorted_funcs, names, name_off, out,
+                                                           head);
+  } else {
+    hash_kernel<<<(unsigned)blocks, 128, 0, st>>>(dec, n, S, nf, depth, sorted_funcs, names, name_off, out, head);
+  }
   g_launch_count++;
   if (head) {
     hash_fill_kernel<<<(unsigned)blocks, 128, 0, st>>>(head, n, out);

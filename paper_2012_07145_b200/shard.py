@@ -42,8 +42,20 @@ class StepPlan:
             self.sc.featurize(d, out=self.fbuf)
         return self.fbuf
 
-    def run(self, dec, k1_times=None):
+    def run(self, dec, times=None):
+        """One beam step.  `times` (optional dict) accumulates the device
+        milliseconds of each phase: hash, featurize (K1), cost (K2), select
+        (K4 + exchange), cut (K5), memo (K3 at depths 1..num_passes)."""
         sc = self.sc
+        ev = []
+
+        def mark():
+            if times is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                ev.append(e)
+
+        mark()
         h = sc.struct_hash(dec, self.pass_index)
         if self.world > 1:
             mine = torch.nonzero(torch.remainder(h, self.world) == self.rank).flatten()
@@ -52,13 +64,11 @@ class StepPlan:
         else:
             mine, d, hl = None, dec, h
         self.local_count = d.shape[0]
-        if k1_times is not None:
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
+        mark()
         f = self._features(d)
-        if k1_times is not None:
-            b.record()
+        mark()
         total, _, _ = sc.cost(f, scratch=self.rcbuf)
+        mark()
         rep, _, cnt = sc.select(hl, f["verdict"], self.phase_seed, rejects=False)
         nrep = int(cnt[0].item())
         rep = rep[:nrep]
@@ -67,18 +77,22 @@ class StepPlan:
         cand = rep if mine is None else mine.index_select(0, rep)
         if self.world > 1:
             costs, ph, cand = self._exchange(costs, ph, cand, nrep)
-        if k1_times is not None:
-            torch.cuda.synchronize()
-            k1_times.append(a.elapsed_time(b))
+        mark()
         pos, kcnt, bot = sc.beam_topk(costs, ph, None, self.penalty, 0.0, self.phase_seed,
                                       min(self.beam, costs.shape[0]), tie_band=self.tie_band)
         beam = cand.index_select(0, pos[:int(kcnt.item())])
+        mark()
         # bad-hash memo: hashes of the bottom half at every pass depth
         if costs.shape[0] > 1:
             bdec = dec.index_select(0, cand.index_select(0, torch.nonzero(bot).flatten()))
             memo = sc.memo_hashes(bdec, self.num_passes)
         else:
             memo = []
+        mark()
+        if times is not None:
+            torch.cuda.synchronize()
+            for name, a, b in zip(("hash", "featurize", "cost", "select", "cut", "memo"), ev[:-1], ev[1:]):
+                times[name] = times.get(name, 0.0) + a.elapsed_time(b)
         return {"beam": beam.cpu().tolist(), "total": total, "verdict": f["verdict"], "memo": memo,
                 "n_reps": int(costs.shape[0])}
 

@@ -3,5 +3,5 @@ mkdir -p gpurun_out
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 600 python tools/k1_stats.py 1000 > gpurun_out/k1_stats.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:featurize_kernel -s 1 -c 1 \
-   -o gpurun_out/prof_k1 -f python tools/prof_k1.py 200 > gpurun_out/ncu_full.log 2>&1
+   -o gpurun_out/prof_k1 -f python tools/prof_k1.py 1000 > gpurun_out/ncu_full.log 2>&1
 exit 0

@@ -1,5 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:featurize_kernel -s 1 -c 1 \
-   -o gpurun_out/prof_k1 -f python tools/prof_k1.py 400 > gpurun_out/ncu_full.log 2>&1
+   -o gpurun_out/prof_k1 -f python tools/prof_k1.py 1000 > gpurun_out/ncu_full.log 2>&1
 exit 0
