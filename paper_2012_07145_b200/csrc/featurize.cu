@@ -1826,9 +1826,9 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   k.dec = reinterpret_cast<GsDecision*>(ws + L.dec);
   k.didx = reinterpret_cast<int16_t*>(ws + L.didx);
   k.cf = reinterpret_cast<CF<ND>*>(ws + L.cf);
-  k.rd = reinterpret_cast<RRead*>(wgs + L.reads);
-  k.path = reinterpret_cast<int16_t*>(wgs + L.paths);
-  k.rdb = reinterpret_cast<int32_t*>(wgs + L.rdb);
+  k.rd = reinterpret_cast<RRead*>(wg + L.reads);
+  k.path = reinterpret_cast<int16_t*>(wg + L.paths);
+  k.rdb = reinterpret_cast<int32_t*>(ws + L.rdb);
   k.rows = reinterpret_cast<int32_t*>(ws + L.rows);
   k.stack = reinterpret_cast<Frame*>(ws + L.stack);
   k.volacc = reinterpret_cast<int64_t*>(ws + L.volacc);
@@ -2057,9 +2057,9 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   int cfs = nd == 1 ? cf_size<1>() : nd == 2 ? cf_size<2>() : nd == 3 ? cf_size<3>() : cf_size<4>();
   L.cf = o; o += al(nf * cfs);
   L.pcf = 0;
-  L.reads = gplace(rcap * (int)sizeof(RRead));
-  L.paths = gplace(pcap * 2);
-  L.rdb = gplace(2 * ns * 4);
+  L.reads = place(rcap * (int)sizeof(RRead));
+  L.paths = place(pcap * 2);
+  L.rdb = o; o += al(2 * ns * 4);
   L.rows = o; o += al(R * 4);
   L.icall = gplace(pcap * (int)sizeof(ICall));
   L.srcb = gplace((nf + 1) * 4);
