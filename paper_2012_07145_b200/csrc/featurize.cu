@@ -1150,12 +1150,121 @@ __device__ unsigned long long residue_hist(const GsAccess* A, const int16_t* pat
   return T;
 }
 
+// Default machine (32-byte segments, 32 banks x 4 bytes): compact counters
+// with only the code that machine runs, to keep the hot instruction
+// footprint small.  bs: byte stride per dim of the producer's allocation;
+// ts: chain stride product per dim; cst: address of the constant-0 access
+// of thread 0 (+ bias).
+template <int ND>
+__device__ __forceinline__ void tx_strides(const GsAccess* A, const int16_t* path, int plen, bool identity,
+                                           const CF<ND>& prod, int eb, int64_t* bs, int64_t* ts) {
+  int64_t acc = eb;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    bs[d] = acc;
+    acc *= (int64_t)prod.rhi[d] - prod.rlo[d] + 1;
+    ts[d] = 1;
+    if (!identity)
+#pragma unroll 1
+      for (int q = 0; q < plen; ++q) ts[d] *= A[path[q]].s[d];
+  }
+}
+
+// global: register histogram mod 32 + interval sums over its prefix scan
+template <int ND>
+__device__ __noinline__ unsigned long long tx_global32(const GsAccess* A, const int16_t* path, int plen,
+                                                       bool identity, const CF<ND>& h, const CF<ND>& prod, int eb,
+                                                       WarpScr& W, int& err) {
+  const int lane = lane_id();
+  int64_t bs[ND], ts[ND];
+  tx_strides<ND>(A, path, plen, identity, prod, eb, bs, ts);
+  const unsigned long long tv = residue_hist<ND, 32>(A, path, plen, identity, h, bs, W, err);
+  int64_t cst = kAddrBias;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) cst += ((int64_t)h.base[d] * ts[d] - prod.rlo[d]) * bs[d];
+  unsigned long long incl = tv;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  const unsigned long long pex = incl - tv;
+  const unsigned long long tsum = __shfl_sync(0xffffffffu, incl, 31);
+  const ModM<32> mm(32);
+  unsigned long long total = 0;
+  const int nwarps = (h.n_threads + 31) / 32;
+  WarpWalk<ND> walk(h, ts, bs, cst, lane);
+  for (int w = 0; w < nwarps; ++w, walk.next()) {
+    bool active;
+    const int64_t org = walk.origin(active);
+    const int64_t up = __shfl_up_sync(0xffffffffu, org, 1);
+    if (__all_sync(0xffffffffu, lane == 0 || !active || org >= up)) {
+      unsigned long long c = 0;
+      int lo = 0, hi = 0;
+      if (active && lane > 0) {
+        const int64_t d = org - up;
+        if (d >= 32) c = tsum;
+        else { lo = (int)((32 - d - (up & 31)) & 31); hi = lo + (int)d; }
+      } else if (active) {
+        c = tsum;
+      }
+      const unsigned long long plo = __shfl_sync(0xffffffffu, pex, lo);
+      const unsigned long long phi = __shfl_sync(0xffffffffu, pex, hi & 31);
+      if (hi > lo) c = hi <= 32 ? (hi == 32 ? tsum : phi) - plo : (tsum - plo) + phi;
+      for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      total += c;
+    } else {
+#pragma unroll 1
+      for (int r = 0; r < 32; ++r) {
+        const unsigned long long wr = __shfl_sync(0xffffffffu, tv, r);
+        if (wr) total += wr * warp_count((unsigned long long)(org + r), active, T_GLOBAL, mm, 2, 4, 32);
+      }
+    }
+  }
+  return total;
+}
+
+// shared: register histogram mod the 4-byte bank width, one evaluation
+// per emulated warp per residue mod 4 that occurs
+template <int ND>
+__device__ __noinline__ unsigned long long tx_shared4(const GsAccess* A, const int16_t* path, int plen,
+                                                      bool identity, const CF<ND>& h, const CF<ND>& prod, int eb,
+                                                      WarpScr& W, int& err) {
+  const int lane = lane_id();
+  int64_t bs[ND], ts[ND];
+  tx_strides<ND>(A, path, plen, identity, prod, eb, bs, ts);
+  const unsigned long long tb = residue_hist<ND, 4>(A, path, plen, identity, h, bs, W, err);
+  int64_t cst = kAddrBias;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) cst += ((int64_t)h.base[d] * ts[d] - prod.rlo[d]) * bs[d];
+  const ModM<128> mm(128);
+  const unsigned ew = __ballot_sync(0xffffffffu, lane < 4 && tb != 0) & 0xFu;
+  unsigned long long total = 0;
+  const int nwarps = (h.n_threads + 31) / 32;
+  WarpWalk<ND> walk(h, ts, bs, cst, lane);
+  for (int w = 0; w < nwarps; ++w, walk.next()) {
+    bool active;
+    const int64_t org = walk.origin(active);
+    unsigned m4 = ew;
+    while (m4) {
+      const int e = __ffs(m4) - 1; m4 &= m4 - 1;
+      const unsigned long long we = __shfl_sync(0xffffffffu, tb, e);
+      total += we * warp_count((unsigned long long)(org + e), active, T_SHARED, mm, 2, 4, 32);
+    }
+  }
+  return total;
+}
+
 // MC / BW / NB: compile-time period, bank width and bank count for the
 // common machines (0 = read them from Mc at run time).
 template <int ND, int MC, int BW, int NB>
 __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int16_t* path, int plen, bool identity,
                                       const CF<ND>& h, const CF<ND>& prod, int eb, int tier,
                                       const GsMachine& Mc, WarpScr& W, int& err) {
+  if constexpr (MC == 32) {
+    return tx_global32<ND>(A, path, plen, identity, h, prod, eb, W, err);
+  } else if constexpr (MC == 128 && BW == 4) {
+    return tx_shared4<ND>(A, path, plen, identity, h, prod, eb, W, err);
+  }
   const int lane = lane_id();
 #ifdef GS_PHASES
   long long tsub = clock64();
