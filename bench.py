@@ -44,6 +44,13 @@ UNIT = "candidates/s"
 PARENTS_FILE = os.path.join(ROOT, "bench_data", "c5_parents_seed0.npz")
 
 
+def _parents(parents):
+    from paper_2012_07145_b200.descriptor import DECISION_DTYPE
+    z = np.load(PARENTS_FILE)
+    par = np.ascontiguousarray(z["parents"]).view(DECISION_DTYPE).reshape(len(z["parents"]), -1)
+    return par[:parents], z["steps"][:parents]
+
+
 def _workload(parents):
     """The committed prune-valid parents (bench_data/make_c5.py) expanded to
     every tiling of their step root (host, untimed)."""
@@ -263,7 +270,11 @@ def run_gpu(args):
     lib = _lib.load()
     sc = Scorer(graph, MachineParams(), DEFAULT_THRESHOLDS, init_weights(0))
     dec = sc.to_device(recs)                       # inputs resident in HBM
-    host = torch.from_numpy(recs.view(np.uint8).reshape(N, -1)).pin_memory()
+    # the beam as the search holds it (parents + step-root index), pinned,
+    # for the end-to-end arm: candidates are generated on the device
+    par, steps = _parents(args.parents)
+    host_par = torch.from_numpy(par.view(np.uint8).reshape(len(par), -1)).pin_memory()
+    host_steps = torch.from_numpy(np.asarray(steps, dtype=np.int32)).pin_memory()
     stream = torch.cuda.current_stream()
     plan = shard.StepPlan(sc, N, world, rank, PASS_INDEX, PHASE_SEED, BEAM, 2.0, NUM_PASSES, TIE_BAND)
 
@@ -300,8 +311,10 @@ def run_gpu(args):
         ms = float(t.item())
     value = N / (ms / 1e3)
 
-    # e2e through the public batch API: pinned host records in, totals +
-    # verdicts + beam out, copies inside the timed region
+    # e2e through the public beam-step API: pinned host beam in (parents +
+    # step-root indices; the 1M candidates are generated on the device by
+    # gs_expand_step), totals + verdicts + beam out, copies inside the
+    # timed region
     e2e_ms = []
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
@@ -309,7 +322,7 @@ def run_gpu(args):
             dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        out = plan.run_host(host)
+        out = plan.run_beam_host(host_par, host_steps, total=N)
         b.record(stream)
         torch.cuda.synchronize()
         if i >= args.warmup:
@@ -364,6 +377,7 @@ def run_gpu(args):
                                  "the HBM fraction is reported as the north star asks"},
             "cpu_baseline": cpu,
             "e2e": {"value": N / (e / 1e3), "unit": UNIT, "ms_per_step": e,
+                    "path": "StepPlan.run_beam_host: H2D beam, gs_expand_step on device, step, D2H results",
                     "h2d_bytes_per_step": int(out["h2d_bytes"]), "d2h_bytes_per_step": int(out["d2h_bytes"])},
             "step_breakdown_ms": breakdown,
             "gpu_launches": int(launches),

@@ -217,6 +217,33 @@ int gs_stats(gs_pipeline_t p, int64_t* out, void* stream);
  * (13 = loads end).  Synchronizes the device. */
 int gs_debug_phases(int64_t* out);
 
+/* ---- beam-step expansion --------------------------
+ * Menus of reference options.py:25-37 (TilingConfig). */
+typedef struct {
+  int32_t serial_powers[8], n_serial_powers;
+  int32_t odd_serial[8], n_odd_serial;
+  int32_t innermost_thread[8], n_innermost;
+  int32_t outer_thread[8], n_outer;
+  int32_t unroll_budget, warp_size;
+} GsTilingMenus;
+
+/* Every phase-2 tiling of each parent's step-root decision, parents in
+ * order, tilings in the reference order (search.py:223-235
+ * `_phase2_candidates`, options.py:144-183).  parents: [n][S] records;
+ * step[p]: index of the step root's (compute_root) record in parent p.
+ * Writes offsets[0..n] (device int64: candidate range of each parent; the
+ * total is offsets[n]) and, when out != NULL, the expanded records
+ * out[offsets[n]][S] and (nullable) owner[] = parent index.  Call once with
+ * out == NULL to size `out`.  Workspace: gs_expand_workspace_bytes(n).
+ * More than 4096 tilings for one parent, or a step record that is not a
+ * compute_root decision, raise GS_ERR_CAPACITY / GS_ERR_SCHEDULE at
+ * gs_check. */
+int64_t gs_expand_workspace_bytes(int64_t n_parents);
+int gs_expand_step(gs_pipeline_t p, const GsDecision* parents, int64_t n_parents, int s,
+                   const int32_t* step, const GsTilingMenus* menus, int64_t* offsets,
+                   void* workspace, int64_t ws_bytes, GsDecision* out, int32_t* owner,
+                   void* stream);
+
 /* Device-side error word of the last K1 launch (capacity overflow etc.);
  * synchronizes `stream`. */
 int gs_check(gs_pipeline_t p, void* stream);

@@ -27,6 +27,10 @@ int select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, uint6
                 int64_t ws_bytes, int64_t* rep_idx, int64_t* n_reps, int64_t* n_rejects, int64_t* rej_idx,
                 cudaStream_t st);
 int64_t topk_workspace_bytes(int64_t n);
+int64_t expand_workspace_bytes(int64_t n);
+int launch_expand(const GsFunc* funcs, const GsDecision* parents, int64_t n, int S, const int32_t* step,
+                  const GsTilingMenus& m, int64_t* offsets, void* ws, int64_t ws_bytes, GsDecision* out,
+                  int32_t* owner, int* gerr, int num_sms, cudaStream_t st);
 int beam_topk(const double* costs, const uint64_t* ph, int64_t n, const uint64_t* flagged, int64_t nflag,
               double penalty, double temperature, uint64_t phase_seed, int64_t k, double band, void* ws,
               int64_t ws_bytes, int64_t* out_pos, int64_t* n_out, uint8_t* bottom, cudaStream_t st);
@@ -351,6 +355,31 @@ int gs_select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, ui
 }
 
 int64_t gs_topk_workspace_bytes(int64_t n) { return topk_workspace_bytes(n); }
+
+int64_t gs_expand_workspace_bytes(int64_t n_parents) { return expand_workspace_bytes(n_parents); }
+
+int gs_expand_step(gs_pipeline_t p, const GsDecision* parents, int64_t n_parents, int s, const int32_t* step,
+                   const GsTilingMenus* menus, int64_t* offsets, void* workspace, int64_t ws_bytes, GsDecision* out,
+                   int32_t* owner, void* stream) {
+  if (!p || !menus || !offsets || s < 1 || n_parents < 0) return fail(GS_ERR_ARG, "bad expand arguments");
+  const GsTilingMenus& m = *menus;
+  if (m.n_serial_powers < 0 || m.n_serial_powers > 8 || m.n_odd_serial < 0 || m.n_odd_serial > 8 ||
+      m.n_innermost < 1 || m.n_innermost > 8 || m.n_outer < 1 || m.n_outer > 8 || m.warp_size < 1)
+    return fail(GS_ERR_ARG, "tiling menus out of range");
+  for (int i = 0; i < m.n_serial_powers; ++i)
+    if (m.serial_powers[i] < 1 || m.serial_powers[i] > 255) return fail(GS_ERR_ARG, "serial menu value out of range");
+  for (int i = 0; i < m.n_odd_serial; ++i)
+    if (m.odd_serial[i] < 1 || m.odd_serial[i] > 255) return fail(GS_ERR_ARG, "serial menu value out of range");
+  for (int i = 0; i < m.n_innermost; ++i)
+    if (m.innermost_thread[i] < 1 || m.innermost_thread[i] > 255) return fail(GS_ERR_ARG, "thread menu value out of range");
+  for (int i = 0; i < m.n_outer; ++i)
+    if (m.outer_thread[i] < 1 || m.outer_thread[i] > 255) return fail(GS_ERR_ARG, "thread menu value out of range");
+  int rc = launch_expand(reinterpret_cast<const GsFunc*>(p->blob), parents, n_parents, s, step, m, offsets, workspace,
+                         ws_bytes, out, owner, p->err, p->num_sms, (cudaStream_t)stream);
+  if (rc) return fail(GS_ERR_ARG, "expand: workspace too small or too many parents");
+  CK(cudaGetLastError());
+  return GS_OK;
+}
 
 int gs_beam_topk(const double* costs, const uint64_t* pass_hash, int64_t n, const uint64_t* flagged,
                  int64_t n_flagged, double penalty, double temperature, uint64_t phase_seed, int64_t k, double tie_band, void* ws,

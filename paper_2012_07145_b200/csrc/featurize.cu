@@ -399,8 +399,8 @@ __device__ __noinline__ bool geometry_one(K1<ND>& k, int i) {
 #pragma unroll
     for (int dd = 0; dd < ND; ++dd) {
       int e = dd < fn.ndim ? fn.extent[dd] : 1;
-      ser[dd] = tiled ? d.serial[dd] : 1;
-      thr[dd] = tiled ? d.thread[dd] : (dd == inner ? (e < 32 ? e : 32) : 1);
+      ser[dd] = tiled && dd < fn.ndim ? d.serial[dd] : 1;
+      thr[dd] = tiled ? (dd < fn.ndim ? d.thread[dd] : 1) : (dd == inner ? (e < 32 ? e : 32) : 1);
       int64_t st = (int64_t)ser[dd] * thr[dd];
       int64_t b = udiv(e + st - 1, st);
       if (b < 1) b = 1;
@@ -472,7 +472,7 @@ __device__ __noinline__ bool geometry_one(K1<ND>& k, int i) {
     int64_t nt = 1, sp = 1;
 #pragma unroll
     for (int dd = 0; dd < ND; ++dd) {
-      int s = (d.flags & 1) ? d.serial[dd] : 1;
+      int s = (d.flags & 1) && dd < fn.ndim ? d.serial[dd] : 1;
       int64_t t = hi[dd] - lo[dd] + 1 + s - 1 >= 0 ? udiv(hi[dd] - lo[dd] + 1 + s - 1, s) : (hi[dd] - lo[dd] + s) / s;
       if (t < 1) t = 1;
       c.rlo[dd] = (int32_t)lo[dd];

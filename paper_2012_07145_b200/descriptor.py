@@ -52,6 +52,31 @@ class GsThresholds(C.Structure):
                 ("thread_alloc_bytes", C.c_int64)]
 
 
+class GsTilingMenus(C.Structure):
+    _fields_ = [("serial_powers", C.c_int32 * 8), ("n_serial_powers", C.c_int32),
+                ("odd_serial", C.c_int32 * 8), ("n_odd_serial", C.c_int32),
+                ("innermost_thread", C.c_int32 * 8), ("n_innermost", C.c_int32),
+                ("outer_thread", C.c_int32 * 8), ("n_outer", C.c_int32),
+                ("unroll_budget", C.c_int32), ("warp_size", C.c_int32)]
+
+
+def tiling_menus(menus) -> GsTilingMenus:
+    """Pack a TilingConfig-like object (reference options.py:25-37)."""
+    m = GsTilingMenus()
+    for name, cnt in (("serial_powers", "n_serial_powers"), ("odd_serial", "n_odd_serial"),
+                      ("innermost_thread", "n_innermost"), ("outer_thread", "n_outer")):
+        vals = tuple(getattr(menus, name))
+        if len(vals) > 8:
+            raise ValueError(f"{name}: at most 8 menu values")
+        arr = getattr(m, name)
+        for i, v in enumerate(vals):
+            arr[i] = int(v)
+        setattr(m, cnt, len(vals))
+    m.unroll_budget = int(menus.unroll_budget)
+    m.warp_size = int(menus.warp_size)
+    return m
+
+
 class GsPipelineDesc(C.Structure):
     _fields_ = [("n_funcs", C.c_int32), ("n_stages", C.c_int32), ("n_access", C.c_int32),
                 ("funcs", C.POINTER(GsFunc)), ("stages", C.POINTER(GsStage)),

@@ -175,6 +175,31 @@ class Scorer:
                 out.append(self.struct_hash(dec, depth))
         return out
 
+    # -- beam-step expansion -------------------------------------------------
+    def expand_step(self, parents: torch.Tensor, steps: torch.Tensor, menus=None, total=None):
+        """Every phase-2 tiling of each parent's step root on the device
+        (search.py:223-235).  parents: uint8 [P, S*16] decision records on the
+        device; steps: int32 [P] record index of each parent's step root.
+        Returns (records [N, S*16], owner int32 [N], offsets int64 [P+1]).
+        `total` (N) skips the sizing pass when already known."""
+        from .descriptor import tiling_menus
+        from .gen import Menus
+        P, S = parents.shape[0], parents.shape[1] // 16
+        m = tiling_menus(menus or Menus)
+        wsb = self.lib.gs_expand_workspace_bytes(P)
+        ws = torch.empty((max(1, wsb),), dtype=torch.uint8, device=self.device)
+        offsets = torch.empty((P + 1,), dtype=torch.int64, device=self.device)
+        if total is None:
+            _lib.check(self.lib.gs_expand_step(self.handle, _ptr(parents), P, S, _ptr(steps), C.byref(m),
+                                               _ptr(offsets), _ptr(ws), wsb, C.c_void_p(0), C.c_void_p(0),
+                                               _stream()))
+            total = int(offsets[-1].item())
+        out = torch.empty((total, S * 16), dtype=torch.uint8, device=self.device)
+        owner = torch.empty((max(1, total),), dtype=torch.int32, device=self.device)
+        _lib.check(self.lib.gs_expand_step(self.handle, _ptr(parents), P, S, _ptr(steps), C.byref(m),
+                                           _ptr(offsets), _ptr(ws), wsb, _ptr(out), _ptr(owner), _stream()))
+        return out, owner[:total], offsets
+
     # -- K4 -------------------------------------------------------------------
     def select(self, hashes: torch.Tensor, verdict: torch.Tensor, phase_seed: int, rejects=True):
         n = hashes.shape[0]

@@ -109,6 +109,21 @@ class StepPlan:
         return {"h2d_bytes": host_u8.numel(), "d2h_bytes": tot.numel() * 8 + ver.numel() + 8 * len(out["beam"]),
                 "beam": out["beam"]}
 
+    def run_beam_host(self, parents_u8, steps_i32, total=None):
+        """Public beam-step entry with host buffers, as the search drives it:
+        H2D of the beam (parent decision records + step-root indices), the
+        candidates generated on the device (every phase-2 tiling of each
+        parent's step root, gs_expand_step), one step, D2H of every
+        candidate's total + verdict and the beam."""
+        par = parents_u8.to(self.sc.device, non_blocking=True)
+        st = steps_i32.to(self.sc.device, non_blocking=True)
+        dec, _, _ = self.sc.expand_step(par, st, total=total)
+        out = self.run(dec)
+        tot = out["total"].cpu()
+        ver = out["verdict"].cpu()
+        return {"h2d_bytes": parents_u8.numel() + 4 * steps_i32.numel(),
+                "d2h_bytes": tot.numel() * 8 + ver.numel() + 8 * len(out["beam"]), "beam": out["beam"]}
+
 
 def exchange_reps(costs, ph, cand, world, group=None):
     """All-gather every rank's representative records and merge them into
