@@ -12,7 +12,11 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
                      const Layout& L, int nwarps, int grid, int* gerr, int reuse, uint8_t* gscratch,
-                     uint8_t* heads, cudaStream_t st);
+                     uint8_t* heads, int mode, const int32_t* run_id, const int32_t* run_head, int64_t nruns,
+                     uint8_t* slots, int64_t slot_bytes, cudaStream_t st);
+int64_t k1_prepare_runs(const GsDecision* dec, int64_t n, int S, uint8_t* heads, int32_t* run_id,
+                        int32_t* run_head, void* tmp, size_t tmp_bytes, cudaStream_t st);
+size_t k1_runs_tmp_bytes(int64_t n);
 int featurize_warps(const Layout& L1, int max_smem);
 int read_phases(long long* out);
 int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st);
@@ -74,6 +78,10 @@ struct GsPipeline {
   uint8_t* gscratch = nullptr;   // K1 spilled structure arrays (grow-only)
   uint8_t* k1heads = nullptr;    // K1 run-head flags (grow-only)
   int64_t k1cap = 0;
+  uint8_t* runbuf = nullptr;     // K1 two-phase: run ids, run heads, scan scratch (grow-only)
+  int64_t runcap = 0;
+  uint8_t* slots = nullptr;      // K1 two-phase: per-run warp state (grow-only)
+  int64_t slotcap = 0;
   int64_t gcap = 0;
   int64_t hcap = 0;
 };
@@ -196,7 +204,7 @@ int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
 int gs_pipeline_destroy(gs_pipeline_t p) {
   if (!p) return GS_OK;
   cudaFree(p->dev); cudaFree(p->blob); cudaFree(p->stage_of_func); cudaFree(p->algo); cudaFree(p->sorted);
-  cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err); cudaFree(p->hscratch); cudaFree(p->gscratch); cudaFree(p->k1heads);
+  cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err); cudaFree(p->hscratch); cudaFree(p->gscratch); cudaFree(p->k1heads); cudaFree(p->runbuf); cudaFree(p->slots);
   for (double* b : p->wbufs) cudaFree(b);
   delete p;
   return GS_OK;
@@ -279,8 +287,52 @@ int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, doubl
   }
   p->last_warps = nwarps;
   p->last_slice = L.warp_bytes;
-  int rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, nwarps,
-                            (int)grid, p->err, p->reuse, p->gscratch, p->k1heads, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  // Two-phase schedule for large batches of long sibling runs: run heads
+  // first (each saves its warp state), then the siblings in small slices
+  // that resume from their head's state, so runs split across warps without
+  // re-resolving.  Needs one host sync to size the per-run state.
+  int rc = 0;
+  bool two_phase = false;
+  if (p->reuse && feats && n >= 8192) {
+    const size_t tmpb = (k1_runs_tmp_bytes(n) + 255) & ~(size_t)255;
+    const int64_t need = (int64_t)tmpb + 8 * n + 256;
+    if (need > p->runcap) {
+      CK(cudaStreamSynchronize(st));
+      if (p->runbuf) CK(cudaFree(p->runbuf));
+      p->runbuf = nullptr;
+      p->runcap = 0;
+      CK(cudaMalloc(&p->runbuf, (size_t)need));
+      p->runcap = need;
+    }
+    int32_t* run_id = reinterpret_cast<int32_t*>(p->runbuf + tmpb);
+    int32_t* run_head = run_id + n;
+    const int64_t nruns = k1_prepare_runs(dec, n, S, p->k1heads, run_id, run_head, p->runbuf, tmpb, st);
+    if (nruns < 0) return fail(GS_ERR_CUDA, "run preparation failed");
+    const int64_t slot_bytes = (int64_t)L.warp_bytes + L.gl_bytes;
+    if (nruns * 8 <= n && nruns * slot_bytes <= (int64_t)4 << 30) {
+      two_phase = true;
+      if (nruns * slot_bytes > p->slotcap) {
+        CK(cudaStreamSynchronize(st));
+        if (p->slots) CK(cudaFree(p->slots));
+        p->slots = nullptr;
+        p->slotcap = 0;
+        CK(cudaMalloc(&p->slots, (size_t)(nruns * slot_bytes)));
+        p->slotcap = nruns * slot_bytes;
+      }
+      rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L,
+                            nwarps, (int)grid, p->err, p->reuse, p->gscratch, p->k1heads, 1, run_id, run_head, nruns,
+                            p->slots, slot_bytes, st);
+      if (!rc)
+        rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L,
+                              nwarps, (int)grid, p->err, p->reuse, p->gscratch, p->k1heads, 2, run_id, run_head,
+                              nruns, p->slots, slot_bytes, st);
+    }
+  }
+  if (!two_phase)
+    rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L,
+                          nwarps, (int)grid, p->err, p->reuse, p->gscratch, p->k1heads, 0, nullptr, nullptr, 0,
+                          nullptr, 0, st);
   if (rc) return fail(GS_ERR_ARG, "unsupported ndim");
   CK(cudaGetLastError());
   return GS_OK;

@@ -17,6 +17,7 @@
 //     histograms, then counts each distinct residue once per emulated warp
 //     with __match_any_sync / __ballot_sync / __popc on the real lanes.
 #include "gs_internal.cuh"
+#include <cub/cub.cuh>
 #include <cuda/std/cstdint>
 
 namespace gs {
@@ -1916,7 +1917,9 @@ __global__ void __launch_bounds__(kK1MaxWarps * 32, 1)
 featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob, const GsDecision* __restrict__ dec,
                  int64_t n, int S, double* __restrict__ feats, int32_t* __restrict__ row_key,
                  int32_t* __restrict__ n_rows, uint8_t* __restrict__ verdict, int32_t* __restrict__ row_src,
-                 Layout L, int* gerr, int reuse, uint8_t* __restrict__ gscratch, const uint8_t* __restrict__ heads) {
+                 Layout L, int* gerr, int reuse, uint8_t* __restrict__ gscratch, const uint8_t* __restrict__ heads,
+                 int mode, const int32_t* __restrict__ run_id, const int32_t* __restrict__ run_head, int64_t nruns,
+                 uint8_t* __restrict__ slots, int64_t slot_bytes) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar;
   const int warp = threadIdx.x >> 5, lane = lane_id(), nw = blockDim.x >> 5;
@@ -1985,18 +1988,53 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     }
     return n;
   };
+  // Modes (see launch_featurize): 0 run-aligned units; 1 run heads only,
+  // each head's warp state saved to its run's slot; 2 siblings in kChunk2
+  // slices, a slice resuming from its run head's saved state (no re-resolve,
+  // no row recompute), so runs split freely across warps.
+  const int64_t nchunks = (n + kChunk2 - 1) / kChunk2;
+  // warp state <-> run slot: the shared-memory slice and the global scratch
+  auto slot_copy = [&](int64_t r, bool save) {
+    uint8_t* sl = slots + r * slot_bytes;
+    int4* a = reinterpret_cast<int4*>(sl);
+    int4* b = reinterpret_cast<int4*>(ws);
+    const int nw1 = L.warp_bytes / 16;
+    for (int i = lane; i < nw1; i += 32) { if (save) a[i] = b[i]; else b[i] = a[i]; }
+    int4* a2 = reinterpret_cast<int4*>(sl + L.warp_bytes);
+    int4* b2 = reinterpret_cast<int4*>(wgs);
+    const int nw2 = L.gl_bytes / 16;
+    for (int i = lane; i < nw2; i += 32) { if (save) a2[i] = b2[i]; else b2[i] = a2[i]; }
+    __syncwarp();
+  };
   bulk_wait(&bar);
   __syncthreads();   // the only CTA barrier: descriptor staged
   for (;;) {
   unsigned uj = 0;
   if (lane == 0) uj = atomicAdd(work, 1u);
   const int64_t j = __shfl_sync(0xffffffffu, uj, 0);
-  if (j >= nunits) break;
-  const int64_t c0 = snap(j * kUnit), c1 = snap((j + 1) * kUnit);
+  int64_t c0, c1;
+  if (mode == 0) {
+    if (j >= nunits) break;
+    c0 = snap(j * kUnit); c1 = snap((j + 1) * kUnit);
+  } else if (mode == 1) {
+    if (j >= nruns) break;
+    c0 = run_head[j]; c1 = c0 + 1;
+  } else {
+    if (j >= nchunks) break;
+    c0 = j * kChunk2; c1 = c0 + kChunk2 < n ? c0 + kChunk2 : n;
+  }
   if (c0 >= c1) continue;
-  if (lane == 0) { m.prev_valid = 0; m.same_struct = 0; m.ndec = 0; st_cand += c1 - c0; }
+  if (lane == 0) { m.prev_valid = 0; m.same_struct = 0; m.ndec = 0; }
   __syncwarp();
+  int64_t pc = c0;          // the candidate this warp's state and feature rows follow
+  int64_t cur_run = -1;
   for (int64_t c = c0; c < c1; ++c) {
+    if (mode == 2) {
+      if (heads[c]) { cur_run = -1; continue; }   // run heads: done in mode 1
+      const int64_t r = run_id[c];
+      if (r != cur_run) { slot_copy(r, false); pc = run_head[r]; cur_run = r; }
+    }
+    if (lane == 0) st_cand++;
 #ifdef GS_PHASES
     tph = clock64();
 #endif
@@ -2008,7 +2046,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
       __syncwarp();
       unsigned cnt = 0, diff = 0;
       // the previous candidate's records: still in L2 (this warp just read them)
-      const uint4* prv = reinterpret_cast<const uint4*>(dec + (c > c0 ? c - 1 : c) * S);
+      const uint4* prv = reinterpret_cast<const uint4*>(dec + pc * S);
       for (int i0 = 0; i0 < S; i0 += 32) {
         const int i = i0 + lane;
         const bool live = i < S && k.dec[i].func != 0xFFFF;
@@ -2025,6 +2063,9 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
         diff |= __ballot_sync(0xffffffffu, d);
       }
       __syncwarp();
+#ifdef GS_DEBUG_DIFF
+      if (lane == 0 && n < 64) printf("c=%lld pc=%lld diff=%x prev_valid=%d cnt=%u ndec=%d mode=%d\n", (long long)c, (long long)pc, diff, m.prev_valid, cnt, m.ndec, mode);
+#endif
       if (lane == 0) {
         m.same_struct = reuse && m.prev_valid && diff == 0 && (int)cnt == m.ndec;
         m.ndec = (int)cnt; m.err = 0; m.ngeo = 0;
@@ -2077,7 +2118,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     // are then recomputed over it
     GS_MARK(3);
     if (diffable && nd < nr) {
-      const int4* src = reinterpret_cast<const int4*>(feats + (int64_t)(c - 1) * L.R * GS_NUM_FEATURES);
+      const int4* src = reinterpret_cast<const int4*>(feats + (int64_t)pc * L.R * GS_NUM_FEATURES);
       int4* dst = reinterpret_cast<int4*>(feats + (int64_t)c * L.R * GS_NUM_FEATURES);
       const int nv = nr * (GS_NUM_FEATURES * 8 / 16);
       int i = lane;
@@ -2104,7 +2145,9 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     GS_MARK(6);
     if (lane == 0) m.prev_valid = (m.err == 0) && feats != nullptr;
     __syncwarp();
+    pc = c;
   }
+  if (mode == 1) slot_copy(j, true);
   }
 #ifdef GS_PHASES
   if (lane == 0)
@@ -2134,6 +2177,22 @@ __global__ void k1_heads_kernel(const GsDecision* __restrict__ dec, int64_t n, i
   }
   diff = __any_sync(0xffffffffu, diff);
   if (lane == 0) head[c] = diff;
+}
+
+struct HeadToInt {
+  __host__ __device__ int operator()(const uint8_t& h) const { return (int)h; }
+};
+
+// run_head[r] = first candidate of run r (run_id = inclusive scan of heads - 1)
+__global__ void k1_run_heads_kernel(const uint8_t* __restrict__ head, const int32_t* __restrict__ run_id, int64_t n,
+                                    int32_t* __restrict__ run_head) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n && head[c]) run_head[run_id[c]] = (int32_t)c;
+}
+
+__global__ void k1_run_ids_kernel(int32_t* __restrict__ run_id, int64_t n) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n) run_id[c] -= 1;
 }
 
 }  // namespace gs
@@ -2222,12 +2281,41 @@ int featurize_warps(const Layout& L1, int max_smem) {
   return w < 1 ? 0 : (w > kK1MaxWarps ? kK1MaxWarps : w);
 }
 
+// Run heads of a batch (K1 sibling structure) and, for the two-phase
+// schedule, each candidate's run index and each run's head.  Returns the
+// number of runs (synchronizes `st` to read it) or -1.
+int64_t k1_prepare_runs(const GsDecision* dec, int64_t n, int S, uint8_t* heads, int32_t* run_id,
+                        int32_t* run_head, void* tmp, size_t tmp_bytes, cudaStream_t st) {
+  k1_heads_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(dec, n, S, heads);
+  g_launch_count++;
+  cub::TransformInputIterator<int, HeadToInt, const uint8_t*> it(heads, HeadToInt());
+  size_t need = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, need, it, run_id, (int)n, st);
+  if (need > tmp_bytes) return -1;
+  cub::DeviceScan::InclusiveSum(tmp, need, it, run_id, (int)n, st);
+  k1_run_ids_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(run_id, n);
+  k1_run_heads_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(heads, run_id, n, run_head);
+  g_launch_count += 2;
+  int32_t last = 0;
+  if (cudaMemcpyAsync(&last, run_id + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess) return -1;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
+  return (int64_t)last + 1;
+}
+
+size_t k1_runs_tmp_bytes(int64_t n) {
+  cub::TransformInputIterator<int, HeadToInt, const uint8_t*> it(nullptr, HeadToInt());
+  size_t need = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, need, it, (int32_t*)nullptr, (int)(n > 0 ? n : 1));
+  return need;
+}
+
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
                      const Layout& L, int nwarps, int grid, int* gerr, int reuse, uint8_t* gscratch,
-                     uint8_t* heads, cudaStream_t st) {
+                     uint8_t* heads, int mode, const int32_t* run_id, const int32_t* run_head, int64_t nruns,
+                     uint8_t* slots, int64_t slot_bytes, cudaStream_t st) {
   dim3 b(nwarps * 32);
-  if (heads && reuse) {
+  if (heads && reuse && mode == 0) {
     k1_heads_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(dec, n, S, heads);
     g_launch_count++;
   }
@@ -2236,7 +2324,7 @@ int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDeci
 #define GS_CASE(D)                                                                                  \
   case D:                                                                                           \
     cudaFuncSetAttribute(featurize_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total); \
-    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, gerr, reuse, gscratch, reuse ? heads : nullptr); \
+    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, gerr, reuse, gscratch, reuse ? heads : nullptr, mode, run_id, run_head, nruns, slots, slot_bytes); \
     g_launch_count++;                                                                               \
     break;
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4)
