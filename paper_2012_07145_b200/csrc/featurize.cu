@@ -1946,8 +1946,8 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   k.volacc = reinterpret_cast<int64_t*>(ws + L.volacc);
   k.touched = reinterpret_cast<int16_t*>(ws + L.touched);
   k.icall = reinterpret_cast<ICall*>(wgs + L.icall);
-  k.srcb = reinterpret_cast<int32_t*>(wgs + L.srcb);
-  k.srcl = reinterpret_cast<int16_t*>(wgs + L.srcl);
+  k.srcb = reinterpret_cast<int32_t*>(ws + L.srcb);
+  k.srcl = reinterpret_cast<int16_t*>(wg + L.srcl);
   k.rdepb = reinterpret_cast<int32_t*>(ws + L.rdepb);
   k.rdep = reinterpret_cast<int16_t*>(wg + L.rdep);
   k.dirty = reinterpret_cast<uint8_t*>(ws + L.dirty);
@@ -1955,8 +1955,8 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   k.kern = reinterpret_cast<int16_t*>(ws + L.kern);
   k.dm = reinterpret_cast<uint32_t*>(ws + L.dm);
   k.cmask = reinterpret_cast<uint32_t*>(ws + L.cmask);
-  k.kmb = reinterpret_cast<int32_t*>(wgs + L.kmb);
-  k.kml = reinterpret_cast<int16_t*>(wgs + L.kml);
+  k.kmb = reinterpret_cast<int32_t*>(ws + L.kmb);
+  k.kml = reinterpret_cast<int16_t*>(ws + L.kml);
   k.icb = reinterpret_cast<int32_t*>(ws + L.icb);
   k.icl = reinterpret_cast<int16_t*>(wgs + L.icl);
   k.dlist = reinterpret_cast<int16_t*>(ws + L.dlist);
@@ -2230,8 +2230,8 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   L.rdb = o; o += al(2 * ns * 4);
   L.rows = o; o += al(R * 4);
   L.icall = gplace(pcap * (int)sizeof(ICall));
-  L.srcb = gplace((nf + 1) * 4);
-  L.srcl = gplace(rcap * 2);
+  L.srcb = o; o += al((nf + 1) * 4);
+  L.srcl = place(rcap * 2);
   L.rdepb = o; o += al((R + 1) * 4);
   L.rdep = place((rcap + nf) * 2);
   L.dirty = o; o += al(nf);
@@ -2242,8 +2242,8 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   L.kern = o; o += al(nf * 2);
   L.dm = o; o += al(nf * L.mw * 4);
   L.cmask = o; o += al(kMaxMaskWords * 4);
-  L.kmb = gplace((nf + 1) * 4);
-  L.kml = gplace(nf * 2);
+  L.kmb = o; o += al((nf + 1) * 4);
+  L.kml = o; o += al(nf * 2);
   L.icb = o; o += al((nf + 1) * 4);
   L.icl = gplace(pcap * 2);
   L.dlist = o; o += al(nf * 2);
