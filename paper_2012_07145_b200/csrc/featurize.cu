@@ -377,7 +377,7 @@ __device__ __forceinline__ void cf_store(K1<ND>& k, int f, const CF<ND>& c) {
 // no member's geometry reads them, so the result is the same and a
 // sibling that changes one member recomputes only its kernel's sums.
 template <int ND>
-__device__ __noinline__ bool geometry_one(K1<ND>& k, int i) {
+__device__ __forceinline__ bool geometry_one(K1<ND>& k, int i) {
   const int lane = lane_id();
   Misc& m = *k.misc;
   const GsDecision d = k.dec[i];
@@ -594,9 +594,24 @@ __device__ void inline_one(K1<ND>& k, int f) {
 // candidate's, which is what a full resolve would recompute bit for bit
 // (geometry is a pure function of those records).  k.dirty[f] ends up 1 iff
 // f's record may differ from the previous candidate's (rows use it).
+// Per-phase cycle accounting of the scorer warps (diagnostics; build with
+// -DGS_PHASES): 0 record load + diff, 1 resolve, 2 prune, 3 row flags,
+// 4 sibling block copy, 5 row features, 6 key/source writes.
+__device__ unsigned long long g_phase[16];
+#ifdef GS_PHASES
+#define GS_SUB(i) do { if (lane_id() == 0) { long long t_ = clock64(); atomicAdd(&g_phase[i], (unsigned long long)(t_ - tsub)); tsub = t_; } } while (0)
+#define GS_MARK(i) do { if (lane == 0) { long long t_ = clock64(); ph[i] += t_ - tph; tph = t_; } } while (0)
+#else
+#define GS_SUB(i) do { } while (0)
+#define GS_MARK(i) do { } while (0)
+#endif
+
 template <int ND>
 __device__ void resolve(K1<ND>& k) {
   const int lane = lane_id();
+#ifdef GS_PHASES
+  long long tsub = clock64();
+#endif
   Misc& m = *k.misc;
   const int nf = k.P->nf;
   const bool diff = m.same_struct;            // k.cf holds the previous candidate's geometry
@@ -647,8 +662,10 @@ __device__ void resolve(K1<ND>& k) {
   }
   __syncwarp();
   if (lane == 0) k.misc->ngeo = cnt;
+  if (diff) GS_SUB(7); else GS_SUB(14);
   for (int q = 0; q < cnt; ++q)
     if (!geometry_one(k, k.dlist[q])) return;
+  if (diff) GS_SUB(15); else GS_SUB(14);
   for (int f = lane; f < nf; f += 32)
     if ((k.F[f].is_external || k.didx[f] < 0) && k.gdirty[f]) external_one(k, f);
   __syncwarp();
@@ -785,30 +802,35 @@ __device__ bool footprint_ap(const GsAccess* A, const int16_t* p, int plen, int 
   return true;
 }
 
+// A group of one read: closed form per dim, no interval lists (inlined:
+// the common case); false = use the general union below.
+template <int ND>
+__device__ __forceinline__ bool union_count_one(const GsAccess* A, const RRead* rd, const int16_t* paths,
+                                                const int16_t* rl, const int8_t* grp, int nr, int g,
+                                                const int32_t* blo, const int32_t* bhi, int64_t& vol,
+                                                int64_t& lines) {
+  int K1 = 0, only = -1;
+  for (int q = 0; q < nr; ++q) if (grp[q] == g) { ++K1; only = q; }
+  if (K1 != 1) return false;
+  const RRead& r = rd[rl[only]];
+  int64_t pv[ND], rv[ND];
+  bool ok = true;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) ok = ok && footprint_ap(A, paths + r.pbeg, r.plen, d, blo[d], bhi[d], pv[d], rv[d]);
+  if (!ok) return false;
+  int64_t outer = 1;
+#pragma unroll
+  for (int d = 1; d < ND; ++d) outer *= pv[d];
+  vol = pv[0] * outer;
+  lines = rv[0] * outer;
+  return true;
+}
+
 template <int ND>
 __device__ __noinline__ void union_count(const GsAccess* A, const RRead* rd, const int16_t* paths,
                             const int16_t* rl, const int8_t* grp, int nr, int g,
                             const int32_t* blo, const int32_t* bhi,
                             int64_t& vol, int64_t& lines, int& err) {
-  {   // a group of one read: closed form per dim, no interval lists
-    int K1 = 0, only = -1;
-    for (int q = 0; q < nr; ++q) if (grp[q] == g) { ++K1; only = q; }
-    if (K1 == 1) {
-      const RRead& r = rd[rl[only]];
-      int64_t pv[ND], rv[ND];
-      bool ok = true;
-#pragma unroll
-      for (int d = 0; d < ND; ++d) ok = ok && footprint_ap(A, paths + r.pbeg, r.plen, d, blo[d], bhi[d], pv[d], rv[d]);
-      if (ok) {
-        int64_t outer = 1;
-#pragma unroll
-        for (int d = 1; d < ND; ++d) outer *= pv[d];
-        vol = pv[0] * outer;
-        lines = rv[0] * outer;
-        return;
-      }
-    }
-  }
   Iv buf[kLaneIv];
   int16_t off[kGroupReads][ND], cnt[kGroupReads][ND];
   int K = 0, used = 0;
@@ -937,17 +959,6 @@ __device__ __noinline__ void union_count(const GsAccess* A, const RRead* rd, con
 // ---------------------------------------------------------------------------
 // Residue arithmetic modulo the transaction / bank period M: shifts and
 // masks when M is a power of two (every real machine), divisions otherwise.
-// Per-phase cycle accounting of the scorer warps (diagnostics; build with
-// -DGS_PHASES): 0 record load + diff, 1 resolve, 2 prune, 3 row flags,
-// 4 sibling block copy, 5 row features, 6 key/source writes.
-__device__ unsigned long long g_phase[16];
-#ifdef GS_PHASES
-#define GS_SUB(i) do { if (lane_id() == 0) { long long t_ = clock64(); atomicAdd(&g_phase[i], (unsigned long long)(t_ - tsub)); tsub = t_; } } while (0)
-#define GS_MARK(i) do { if (lane == 0) { long long t_ = clock64(); ph[i] += t_ - tph; tph = t_; } } while (0)
-#else
-#define GS_SUB(i) do { } while (0)
-#define GS_MARK(i) do { } while (0)
-#endif
 
 // out-of-line slow paths (non-power-of-two periods): keep 64-bit division
 // code out of the hot loops' instruction footprint
@@ -1173,7 +1184,7 @@ __device__ __forceinline__ void tx_strides(const GsAccess* A, const int16_t* pat
 
 // global: register histogram mod 32 + interval sums over its prefix scan
 template <int ND>
-__device__ __noinline__ unsigned long long tx_global32(const GsAccess* A, const int16_t* path, int plen,
+__device__ __forceinline__ unsigned long long tx_global32(const GsAccess* A, const int16_t* path, int plen,
                                                        bool identity, const CF<ND>& h, const CF<ND>& prod, int eb,
                                                        WarpScr& W, int& err) {
   const int lane = lane_id();
@@ -1227,7 +1238,7 @@ __device__ __noinline__ unsigned long long tx_global32(const GsAccess* A, const 
 // shared: register histogram mod the 4-byte bank width, one evaluation
 // per emulated warp per residue mod 4 that occurs
 template <int ND>
-__device__ __noinline__ unsigned long long tx_shared4(const GsAccess* A, const int16_t* path, int plen,
+__device__ __forceinline__ unsigned long long tx_shared4(const GsAccess* A, const int16_t* path, int plen,
                                                       bool identity, const CF<ND>& h, const CF<ND>& prod, int eb,
                                                       WarpScr& W, int& err) {
   const int lane = lane_id();
@@ -1699,7 +1710,7 @@ __device__ void parallel_feats(double* v, const GsMachine& M, int n, const CF<ND
 
 
 template <int ND>
-__device__ __noinline__ void row_features(K1<ND>& k, WarpScr& W, int func, int si, bool inl, double* out) {
+__device__ __forceinline__ void row_features(K1<ND>& k, WarpScr& W, int func, int si, bool inl, double* out) {
   const int lane = lane_id();
 #ifdef GS_PHASES
   long long tsub = clock64();
@@ -1775,7 +1786,8 @@ __device__ __noinline__ void row_features(K1<ND>& k, WarpScr& W, int func, int s
     else if (box == 2) { for (int d = 0; d < ND; ++d) { blo[d] = bhi[d] = h.base[d]; } }
     else block_box(h, blo, bhi);
     int64_t vol, lines;
-    union_count<ND>(k.A, k.rd, k.path, W.rl, W.grp, nr, gi, blo, bhi, vol, lines, err);
+    if (!union_count_one<ND>(k.A, k.rd, k.path, W.rl, W.grp, nr, gi, blo, bhi, vol, lines))
+      union_count<ND>(k.A, k.rd, k.path, W.rl, W.grp, nr, gi, blo, bhi, vol, lines, err);
     const int eb = k.F[W.gprod[gi]].elem_bytes;
     atomicAdd(&W.acc[box][W.gtier[gi]][0], (unsigned long long)(vol * eb));
     atomicAdd(&W.acc[box][W.gtier[gi]][1], (unsigned long long)lines);
@@ -1789,8 +1801,8 @@ __device__ __noinline__ void row_features(K1<ND>& k, WarpScr& W, int func, int s
   auto tx = [&](const int16_t* path, int plen, bool identity, const CF<ND>& host, const CF<ND>& prod, int eb,
                 int tier) -> unsigned long long {
     if (vdef) {
-      if (tier == T_GLOBAL) return warp_tx<ND, 32, 4, 32>(k.A, path, plen, identity, host, prod, eb, tier, M, W, err);
-      return warp_tx<ND, 128, 4, 32>(k.A, path, plen, identity, host, prod, eb, tier, M, W, err);
+      if (tier == T_GLOBAL) return tx_global32<ND>(k.A, path, plen, identity, host, prod, eb, W, err);
+      return tx_shared4<ND>(k.A, path, plen, identity, host, prod, eb, W, err);
     }
     return warp_tx<ND, 0, 0, 0>(k.A, path, plen, identity, host, prod, eb, tier, M, W, err);
   };

@@ -42,6 +42,5 @@ if ph.sum():
     st = sum(sub.values())
     if st:
         print("row phases:", {n: f"{100 * v / st:.1f}%" for n, v in sub.items()})
-    tx = {"T build": ph[7], "classes": ph[14], "evaluate": ph[15]}
-    if sum(tx.values()):
-        print("warp_tx phases:", {n: f"{100 * v / sum(tx.values()):.1f}%" for n, v in tx.items()})
+    print("resolve cycles: sibling pre-geometry", ph[7], "sibling geometry", ph[15], "full (structure+geometry)", ph[14],
+          "of resolve total", ph[1])
