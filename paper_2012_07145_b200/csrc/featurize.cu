@@ -356,19 +356,25 @@ __device__ __forceinline__ void zero_cf(CF<ND>& c) {
 // or of a fuse_at_thread child (strides, allocation bytes).
 template <int ND>
 __device__ __forceinline__ void cf_store(K1<ND>& k, int f, const CF<ND>& c) {
+  static_assert(sizeof(CF<ND>) % 16 == 0, "CF records are copied as 16-byte vectors");
+  constexpr int NV = (int)(sizeof(CF<ND>) / 16);
+  int4* dst = reinterpret_cast<int4*>(&k.cf[f]);
+  const int4* src = reinterpret_cast<const int4*>(&c);
   if (k.track) {
     const CF<ND>& o = k.cf[f];
-    const int32_t* a = reinterpret_cast<const int32_t*>(&o);
-    const int32_t* b = reinterpret_cast<const int32_t*>(&c);
-    bool d = false;
-#pragma unroll
-    for (int w = 0; w < (int)(sizeof(CF<ND>) / 4); ++w) d |= a[w] != b[w];
     bool l = o.tier != c.tier;
 #pragma unroll
     for (int dd = 0; dd < ND; ++dd) l |= o.rlo[dd] != c.rlo[dd] || o.rhi[dd] != c.rhi[dd];
+    bool d = false;
+#pragma unroll
+    for (int w = 0; w < NV; ++w) {
+      const int4 a = dst[w], b = src[w];
+      d |= a.x != b.x || a.y != b.y || a.z != b.z || a.w != b.w;
+    }
     k.dirty[f] |= (uint8_t)(d | (l << 1));
   }
-  k.cf[f] = c;
+#pragma unroll
+  for (int w = 0; w < NV; ++w) dst[w] = src[w];
 }
 
 // Geometry of the non-inline decision i (resolve.py:232-333); warp-wide.

@@ -41,7 +41,7 @@ struct PipeDev {              // device copy of the pipeline (global memory)
 // Per-func resolved geometry (reference resolve.py:82-129 ConcreteFunc,
 // 132-142 KernelInfo folded into the kernel owner's record).
 template <int ND>
-struct CF {
+struct alignas(16) CF {
   int8_t kind, tier, unrolled, has_serial;
   int16_t kernel;     // kernel owner func id, -1 = none
   int16_t consumer;   // fused: d.consumer; inline: primary consumer
