@@ -469,10 +469,14 @@ __device__ __forceinline__ bool geometry_one(K1<ND>& k, int i) {
       }
     }
   }
+  // the bounds are stored as int32 (CF); reduce them as int32 in one
+  // redux.sync each
 #pragma unroll
   for (int dd = 0; dd < ND; ++dd) {
-    lo[dd] = wmin64(lo[dd]); hi[dd] = wmax64(hi[dd]);
-    tlo[dd] = wmin64(tlo[dd]); thi[dd] = wmax64(thi[dd]);
+    lo[dd] = __reduce_min_sync(0xffffffffu, (int)(lo[dd] < INT32_MAX ? lo[dd] : INT32_MAX));
+    hi[dd] = __reduce_max_sync(0xffffffffu, (int)(hi[dd] > INT32_MIN ? hi[dd] : INT32_MIN));
+    tlo[dd] = __reduce_min_sync(0xffffffffu, (int)(tlo[dd] < INT32_MAX ? tlo[dd] : INT32_MAX));
+    thi[dd] = __reduce_max_sync(0xffffffffu, (int)(thi[dd] > INT32_MIN ? thi[dd] : INT32_MIN));
   }
   const CF<ND>& K = k.cf[cg0.kernel];
   if (d.kind == GS_FUSE_BLOCK) {
@@ -1155,13 +1159,18 @@ __device__ unsigned long long residue_hist(const GsAccess* A, const int16_t* pat
       const unsigned long long g = __shfl_sync(0xffffffffu, u, src);
       S2 = mine && (lane & ((1 << a) - 1)) == 0 ? g : 0;
     }
-    // T <- T (*) S2 (cyclic)
+    // T <- T (*) S2 (cyclic), summing over the sparser operand (S2 is
+    // usually a single residue for outer dims: row pitches of 32 B multiples)
     unsigned long long Tn = 0;
-    unsigned nz = __ballot_sync(0xffffffffu, mine && T != 0);
+    unsigned nzt = __ballot_sync(0xffffffffu, mine && T != 0);
+    unsigned nzs = __ballot_sync(0xffffffffu, mine && S2 != 0);
+    const bool over_s = __popc(nzs) < __popc(nzt);
+    unsigned nz = over_s ? nzs : nzt;
+    const unsigned long long X = over_s ? S2 : T, Y = over_s ? T : S2;
     while (nz) {
       const int r = __ffs(nz) - 1; nz &= nz - 1;
-      const unsigned long long tr = __shfl_sync(0xffffffffu, T, r);
-      Tn += tr * __shfl_sync(0xffffffffu, S2, (lane - r) & (Q - 1));
+      const unsigned long long xr = __shfl_sync(0xffffffffu, X, r);
+      Tn += xr * __shfl_sync(0xffffffffu, Y, (lane - r) & (Q - 1));
     }
     T = mine ? Tn : 0;
   }
