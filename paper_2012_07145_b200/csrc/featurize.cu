@@ -353,7 +353,9 @@ __device__ __forceinline__ void zero_cf(CF<ND>& c) {
 // func dirty: rows depending only on unchanged records are bit-identical.
 // dirty bits: 1 = any field changed, 2 = the allocation layout (tier,
 // realization region) changed — all a consumer's row reads of a producer
-// or of a fuse_at_thread child (strides, allocation bytes).
+// or of a fuse_at_thread child (strides, allocation bytes); 4 = the
+// kernel-owner aggregates (blocks, threads per block, shared bytes) — all
+// a row reads of its host's kernel record.
 template <int ND>
 __device__ __forceinline__ void cf_store(K1<ND>& k, int f, const CF<ND>& c) {
   static_assert(sizeof(CF<ND>) % 16 == 0, "CF records are copied as 16-byte vectors");
@@ -371,7 +373,8 @@ __device__ __forceinline__ void cf_store(K1<ND>& k, int f, const CF<ND>& c) {
       const int4 a = dst[w], b = src[w];
       d |= a.x != b.x || a.y != b.y || a.z != b.z || a.w != b.w;
     }
-    k.dirty[f] |= (uint8_t)(d | (l << 1));
+    const bool ag = o.n_blocks != c.n_blocks || o.k_threads != c.k_threads || o.k_shared != c.k_shared;
+    k.dirty[f] |= (uint8_t)(d | (l << 1) | (ag << 2));
   }
 #pragma unroll
   for (int w = 0; w < NV; ++w) dst[w] = src[w];
@@ -562,7 +565,7 @@ __device__ void kernel_aggregates(K1<ND>& k, int kf) {
     if (c.n_threads > kt) kt = c.n_threads;
     if (c.kind == K_BLOCK) sh += alloc_of(c) * k.F[f].elem_bytes;
   }
-  if (k.track && (o.k_threads != kt || o.k_shared != sh)) k.dirty[kf] |= 1;
+  if (k.track && (o.k_threads != kt || o.k_shared != sh)) k.dirty[kf] |= 1 | 4;
   o.k_threads = kt;
   o.k_shared = sh;
 }
@@ -658,7 +661,7 @@ __device__ void resolve(K1<ND>& k) {
   } else {
     for (int f = lane; f < nf; f += 32) { k.gdirty[f] = 1; k.kdirty[f] = 1; }
   }
-  for (int f = lane; f < nf; f += 32) k.dirty[f] = diff ? 0 : 3;
+  for (int f = lane; f < nf; f += 32) k.dirty[f] = diff ? 0 : 7;
   k.track = diff;
   __syncwarp();
   // decisions to re-resolve, in decision order
@@ -2126,7 +2129,8 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
           const CF<ND>& g = k.cf[f];
           const int host = g.kind == K_INLINE ? g.consumer : f;
           d = k.dirty[f] & 1;
-          if (host >= 0) { d |= k.dirty[host] & 1; if (k.cf[host].kernel >= 0) d |= k.dirty[k.cf[host].kernel] & 1; }
+          // own and host records: any field; the host's kernel: its aggregates
+          if (host >= 0) { d |= k.dirty[host] & 1; if (k.cf[host].kernel >= 0) d |= (k.dirty[k.cf[host].kernel] >> 2) & 1; }
           // read producers / thread children: only their layout matters
           for (int q = k.rdepb[r]; q < k.rdepb[r + 1] && !d; ++q) d |= (k.dirty[k.rdep[q]] >> 1) & 1;
         }
