@@ -292,6 +292,9 @@ def run_gpu(args):
     l0 = lib.gs_launch_count()
     phase_ms.clear()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    import gc
+    gc.collect()
+    gc.disable()   # no collector pauses between the step's kernel launches
     with Clocks(local) as clk:
         torch.cuda.synchronize()
         if world > 1:
@@ -303,6 +306,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+    gc.enable()
     launches = lib.gs_launch_count() - l0
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
@@ -316,6 +320,8 @@ def run_gpu(args):
     # gs_expand_step), totals + verdicts + beam out, copies inside the
     # timed region
     e2e_ms = []
+    gc.collect()
+    gc.disable()
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         if world > 1:
@@ -327,6 +333,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         if i >= args.warmup:
             e2e_ms.append(a.elapsed_time(b))
+    gc.enable()
     e = float(np.mean(e2e_ms))
     if world > 1:
         t = torch.tensor([e], device="cuda", dtype=torch.float64)

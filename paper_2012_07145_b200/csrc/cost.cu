@@ -97,7 +97,8 @@ __device__ double stage_row_cost(const NetDev& net, const double* __restrict__ s
 #pragma unroll
   for (int j = 0; j < MAXE; ++j) es[j] = j < E ? bs[j] : 0.0;
   for (int k = 0; k < GS_NUM_FEATURES; ++k) {
-    const double x = log1p(f[k]);
+    const double fk = f[k];
+    const double x = fk == 0.0 ? 0.0 : log1p(fk);   // log1p(+0) = +0: skip the sequence for absent features
 #pragma unroll
     for (int j = 0; j < MAXE; ++j) if (j < E) es[j] = fma(x, sw[k * E + j], es[j]);
   }
