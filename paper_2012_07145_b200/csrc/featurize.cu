@@ -1739,16 +1739,16 @@ __device__ __forceinline__ void row_features(K1<ND>& k, WarpScr& W, int func, in
   const GsFunc& fn = k.F[func];
   const int gstage = fn.stage_begin + si;
   int err = 0;
-  // defaults (featurize.py:78-147)
-  for (int i = lane; i < GS_NUM_FEATURES; i += 32) W.feat[i] = 0.0;
-  __syncwarp();
-  if (lane == 0) {
-    double* v = W.feat;
-    v[F_EXPR] = 1.0; v[F_BLOCK_OCC] = 1.0; v[F_WARP_UTIL] = 1.0;
-    v[F_SH_ST_EFF] = v[F_SH_LD_EFF] = v[F_GL_ST_EFF] = v[F_GL_LD_EFF] = 1.0;
-    v[F_SH_LIMIT] = 1.0; v[F_MAX_WARP_OCC] = 1.0; v[F_MAX_BLOCK_OCC] = 1.0;
-    v[F_INNER_PAR] = 1.0; v[F_NUM_CORES] = 1.0;
-    v[F_EXPR] = (double)k.ST[gstage].branching;
+  // defaults (featurize.py:78-147), one lane per feature
+  {
+    constexpr unsigned long long kOnes =
+        (1ull << F_BLOCK_OCC) | (1ull << F_WARP_UTIL) | (1ull << F_SH_ST_EFF) | (1ull << F_SH_LD_EFF) |
+        (1ull << F_GL_ST_EFF) | (1ull << F_GL_LD_EFF) | (1ull << F_SH_LIMIT) | (1ull << F_MAX_WARP_OCC) |
+        (1ull << F_MAX_BLOCK_OCC) | (1ull << F_INNER_PAR) | (1ull << F_NUM_CORES);
+    const double br = (double)k.ST[gstage].branching;
+    for (int i = lane; i < GS_NUM_FEATURES; i += 32)
+      W.feat[i] = i == F_EXPR ? br : ((kOnes >> i) & 1ull) ? 1.0 : 0.0;
+    if (lane < 24) (&W.acc[0][0][0])[lane] = 0ull;
   }
   __syncwarp();
   const CF<ND>* hp = inl ? (g.consumer >= 0 ? &k.cf[g.consumer] : nullptr) : &g;
@@ -1776,7 +1776,21 @@ __device__ __forceinline__ void row_features(K1<ND>& k, WarpScr& W, int func, in
   }
   if (nr > kRowReads) { if (lane == 0) atomicOr(k.gerr, E_ROWREADS); nr = kRowReads; }
   __syncwarp();
-  if (lane == 0) {
+  // (tier, producer) groups in first-appearance order: one lane per read
+  if (nr <= 32) {
+    bool has = lane < nr;
+    const RRead* r = has ? &k.rd[W.rl[lane]] : nullptr;
+    const unsigned key = has ? ((unsigned)(uint8_t)r->tier << 16) | (uint16_t)r->producer : 0xFFFFFFFFu - lane;
+    const unsigned same = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(same) - 1;
+    const unsigned leaders = __ballot_sync(0xffffffffu, has && leader == lane);
+    const int gi = __popc(leaders & ((1u << leader) - 1));
+    if (has) {
+      W.grp[lane] = (int8_t)gi;
+      if (leader == lane) { W.gtier[gi] = r->tier; W.gprod[gi] = r->producer; }
+    }
+    if (lane == 0) { W.ngroups = __popc(leaders); W.nr = nr; parallel_feats(W.feat, M, h.n_threads, kern); }
+  } else if (lane == 0) {
     int ng = 0;
     for (int q = 0; q < nr; ++q) {
       const RRead& r = k.rd[W.rl[q]];
@@ -1787,7 +1801,6 @@ __device__ __forceinline__ void row_features(K1<ND>& k, WarpScr& W, int func, in
     }
     W.ngroups = ng;
     W.nr = nr;
-    for (int b = 0; b < 4; ++b) for (int t = 0; t < 3; ++t) W.acc[b][t][0] = W.acc[b][t][1] = 0;
     parallel_feats(W.feat, M, h.n_threads, kern);
   }
   __syncwarp();
