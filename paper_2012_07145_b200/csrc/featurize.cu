@@ -1274,11 +1274,25 @@ __device__ __forceinline__ unsigned long long tx_shared4(const GsAccess* A, cons
   for (int w = 0; w < nwarps; ++w, walk.next()) {
     bool active;
     const int64_t org = walk.origin(active);
+    // non-decreasing lane addresses (row-major tiles): equal words are
+    // neighbours, so word leaders come from one shuffle, and only the bank
+    // needs a match
+    const int64_t up = __shfl_up_sync(0xffffffffu, org, 1);
+    const bool mono = __all_sync(0xffffffffu, lane == 0 || !active || org >= up);
     unsigned m4 = ew;
     while (m4) {
       const int e = __ffs(m4) - 1; m4 &= m4 - 1;
       const unsigned long long we = __shfl_sync(0xffffffffu, tb, e);
-      total += we * warp_count((unsigned long long)(org + e), active, T_SHARED, mm, 2, 4, 32);
+      if (mono) {
+        const int64_t word = (org + e) >> 2, wup = (up + e) >> 2;
+        const bool lead = active && (lane == 0 || word != wup);
+        const unsigned bank = lead ? (unsigned)(word & 31) : 0x80000000u + lane;
+        const unsigned bmask = __match_any_sync(0xffffffffu, bank);
+        const unsigned per_bank = lead ? __popc(bmask) : 0u;
+        total += we * __reduce_max_sync(0xffffffffu, per_bank);
+      } else {
+        total += we * warp_count((unsigned long long)(org + e), active, T_SHARED, mm, 2, 4, 32);
+      }
     }
   }
   return total;
