@@ -1098,6 +1098,7 @@ __device__ unsigned long long residue_hist(const GsAccess* A, const int16_t* pat
   const bool mine = lane < Q;
   const ModM<Q> mq(Q);
   unsigned long long T = lane == 0;
+#pragma unroll 1
   for (int d = 0; d < ND; ++d) {
     const int e = h.ext[d];
     unsigned long long H = 0;
@@ -1803,7 +1804,7 @@ __device__ __forceinline__ void row_features(K1<ND>& k, WarpScr& W, int func, in
       W.grp[lane] = (int8_t)gi;
       if (leader == lane) { W.gtier[gi] = r->tier; W.gprod[gi] = r->producer; }
     }
-    if (lane == 0) { W.ngroups = __popc(leaders); W.nr = nr; parallel_feats(W.feat, M, h.n_threads, kern); }
+    if (lane == 0) { W.ngroups = __popc(leaders); W.nr = nr; }
   } else if (lane == 0) {
     int ng = 0;
     for (int q = 0; q < nr; ++q) {
@@ -1815,8 +1816,8 @@ __device__ __forceinline__ void row_features(K1<ND>& k, WarpScr& W, int func, in
     }
     W.ngroups = ng;
     W.nr = nr;
-    parallel_feats(W.feat, M, h.n_threads, kern);
   }
+  if (lane == 0) parallel_feats(W.feat, M, h.n_threads, kern);
   __syncwarp();
   const int ng = W.ngroups;
   GS_SUB(8);
@@ -1851,15 +1852,21 @@ __device__ __forceinline__ void row_features(K1<ND>& k, WarpScr& W, int func, in
     }
     return warp_tx<ND, 0, 0, 0>(k.A, path, plen, identity, host, prod, eb, tier, M, W, err);
   };
-  unsigned long long ld[2] = {0, 0};
-  for (int q = 0; q < nr; ++q) {
-    const RRead& r = k.rd[W.rl[q]];
-    if (r.tier != T_GLOBAL && r.tier != T_SHARED) continue;
-    ld[r.tier] += tx(k.path + r.pbeg, r.plen, false, h, k.cf[r.producer], k.F[r.producer].elem_bytes, r.tier);
+  // one call site for loads and the store (q == nr) keeps a single copy of
+  // the counters in the instruction stream
+  unsigned long long ld[2] = {0, 0}, st = 0;
+#pragma unroll 1
+  for (int q = 0; q <= nr; ++q) {
+    const bool store = q == nr;
+    const RRead* r = store ? nullptr : &k.rd[W.rl[q]];
+    const int tier = store ? (inl ? -1 : g.tier) : r->tier;
+    if (tier != T_GLOBAL && tier != T_SHARED) continue;
+    const int pr = store ? func : r->producer;
+    const unsigned long long c = tx(store ? nullptr : k.path + r->pbeg, store ? 0 : r->plen, store, store ? g : h,
+                                    k.cf[pr], k.F[pr].elem_bytes, tier);
+    if (store) st = c; else ld[tier] += c;
   }
   GS_SUB(13);
-  unsigned long long st = 0;
-  if (!inl && (g.tier == T_GLOBAL || g.tier == T_SHARED)) st = tx(nullptr, 0, true, g, g, fn.elem_bytes, g.tier);
   GS_SUB(10);
   // ---- working set at thread: fuse_at_thread children (featurize.py:482-492)
   int64_t wsc = 0;
