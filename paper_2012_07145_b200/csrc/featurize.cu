@@ -1269,6 +1269,10 @@ __device__ __forceinline__ unsigned long long tx_shared4(const GsAccess* A, cons
   for (int d = 0; d < ND; ++d) cst += ((int64_t)h.base[d] * ts[d] - prod.rlo[d]) * bs[d];
   const ModM<128> mm(128);
   const unsigned ew = __ballot_sync(0xffffffffu, lane < 4 && tb != 0) & 0xFu;
+  unsigned long long tb_all = lane < 4 ? tb : 0;
+  tb_all += __shfl_xor_sync(0xffffffffu, tb_all, 1);
+  tb_all += __shfl_xor_sync(0xffffffffu, tb_all, 2);
+  tb_all = __shfl_sync(0xffffffffu, tb_all, 0);
   unsigned long long total = 0;
   const int nwarps = (h.n_threads + 31) / 32;
   WarpWalk<ND> walk(h, ts, bs, cst, lane);
@@ -1279,7 +1283,13 @@ __device__ __forceinline__ unsigned long long tx_shared4(const GsAccess* A, cons
     // neighbours, so word leaders come from one shuffle, and only the bank
     // needs a match
     const int64_t up = __shfl_up_sync(0xffffffffu, org, 1);
+    const unsigned act = __ballot_sync(0xffffffffu, active);
     const bool mono = __all_sync(0xffffffffu, lane == 0 || !active || org >= up);
+    // the active lanes are a prefix starting at lane 0; when their bytes
+    // span at most 124 (+3 for the residue), every distinct word falls in
+    // a distinct bank: one transaction per instruction
+    const int64_t span = __shfl_sync(0xffffffffu, org, 31 - __clz(act)) - __shfl_sync(0xffffffffu, org, 0);
+    if (mono && span <= 124) { total += tb_all; continue; }
     unsigned m4 = ew;
     while (m4) {
       const int e = __ffs(m4) - 1; m4 &= m4 - 1;
@@ -1699,18 +1709,15 @@ enum FeatIdx {
 };
 
 template <int ND>
-__device__ void parallel_feats(double* v, const GsMachine& M, int n, const CF<ND>& kern) {
-  // featurize.py:317-363.  Thread / warp / block counts are < 2^31: 32-bit
-  // integer division (the 64-bit routine is ~70 dependent instructions).
+__device__ __forceinline__ void parallel_feats(double* v, const GsMachine& M, int n, const CF<ND>& kern) {
+  // featurize.py:317-363, warp-wide: every lane derives the integer
+  // occupancy terms (thread / warp / block counts are < 2^31: 32-bit
+  // division), then lane i forms feature i as ONE quotient, so the eight
+  // IEEE divisions run side by side and exist once in the instruction
+  // stream.  Quotients by 1 are the integer values themselves.
+  const int lane = lane_id();
   const int kt = kern.k_threads, ws = M.warp_size;
   const int aw = (n + ws - 1) / ws;
-  v[F_NUM_BLOCKS] = (double)kern.n_blocks;
-  v[F_WARPS_PB] = (double)((kt + ws - 1) / ws);
-  v[F_ACTIVE_WARPS] = (double)aw;
-  v[F_THREADS_PB] = (double)n;
-  v[F_WARP_UTIL] = (double)n / (double)(ws * aw);
-  v[F_IDLE] = (double)(ws * aw - n) / (double)M.max_threads_per_block;
-  v[F_BLOCK_OCC] = (double)kt / (double)M.max_threads_per_block;
   int wpb = (kt + ws - 1) / ws;
   if (wpb < 1) wpb = 1;
   int by_shared;
@@ -1719,26 +1726,43 @@ __device__ void parallel_feats(double* v, const GsMachine& M, int n, const CF<ND
     // fits zero blocks
     by_shared = kern.k_shared > (int64_t)M.shared_mem_per_sm ? 0 : M.shared_mem_per_sm / (int)kern.k_shared;
     if (by_shared < 1) by_shared = 1;
-    double o = (double)kern.k_shared / (double)M.shared_mem_per_block_limit;
-    v[F_SH_OCC] = o < 1.0 ? o : 1.0;
   } else {
     by_shared = M.max_active_blocks_per_sm;
-    v[F_SH_OCC] = 0.0;
   }
   const int mb = M.max_active_blocks_per_sm;
-  v[F_SH_LIMIT] = (double)(by_shared < mb ? by_shared : mb) / (double)mb;
   int act = mb;
   if (by_shared < act) act = by_shared;
   if (M.max_active_warps_per_sm / wpb < act) act = M.max_active_warps_per_sm / wpb;
   if (act < 1) act = 1;
   int64_t awsm = (int64_t)act * wpb;
   if (awsm > M.max_active_warps_per_sm) awsm = M.max_active_warps_per_sm;
-  v[F_MAX_WARP_OCC] = (double)awsm / (double)M.max_active_warps_per_sm;
-  v[F_MAX_BLOCK_OCC] = (double)act / (double)mb;
-  v[F_NUM_TASKS] = (double)kern.n_blocks;
-  v[F_INNER_PAR] = (double)n;
-  v[F_NUM_CORES] = (double)M.num_sms;
-  v[F_TASKS_PER_CORE] = (double)kern.n_blocks / (double)M.num_sms;
+  int idx = -1;
+  double num = 0.0, den = 1.0;
+  bool clamp = false;
+  switch (lane) {
+    case 0: idx = F_NUM_BLOCKS; num = (double)kern.n_blocks; break;
+    case 1: idx = F_WARPS_PB; num = (double)((kt + ws - 1) / ws); break;
+    case 2: idx = F_ACTIVE_WARPS; num = (double)aw; break;
+    case 3: idx = F_THREADS_PB; num = (double)n; break;
+    case 4: idx = F_WARP_UTIL; num = (double)n; den = (double)(ws * aw); break;
+    case 5: idx = F_IDLE; num = (double)(ws * aw - n); den = (double)M.max_threads_per_block; break;
+    case 6: idx = F_BLOCK_OCC; num = (double)kt; den = (double)M.max_threads_per_block; break;
+    case 7:
+      idx = F_SH_OCC;
+      if (kern.k_shared > 0) { num = (double)kern.k_shared; den = (double)M.shared_mem_per_block_limit; clamp = true; }
+      break;
+    case 8: idx = F_SH_LIMIT; num = (double)(by_shared < mb ? by_shared : mb); den = (double)mb; break;
+    case 9: idx = F_MAX_WARP_OCC; num = (double)awsm; den = (double)M.max_active_warps_per_sm; break;
+    case 10: idx = F_MAX_BLOCK_OCC; num = (double)act; den = (double)mb; break;
+    case 11: idx = F_NUM_TASKS; num = (double)kern.n_blocks; break;
+    case 12: idx = F_INNER_PAR; num = (double)n; break;
+    case 13: idx = F_NUM_CORES; num = (double)M.num_sms; break;
+    case 14: idx = F_TASKS_PER_CORE; num = (double)kern.n_blocks; den = (double)M.num_sms; break;
+    default: break;
+  }
+  double q = num / den;
+  if (clamp && !(q < 1.0)) q = 1.0;
+  if (idx >= 0) v[idx] = q;
 }
 
 
@@ -1817,7 +1841,8 @@ __device__ __forceinline__ void row_features(K1<ND>& k, WarpScr& W, int func, in
     W.ngroups = ng;
     W.nr = nr;
   }
-  if (lane == 0) parallel_feats(W.feat, M, h.n_threads, kern);
+  __syncwarp();
+  parallel_feats(W.feat, M, h.n_threads, kern);
   __syncwarp();
   const int ng = W.ngroups;
   GS_SUB(8);

@@ -82,18 +82,20 @@ class StepPlan:
                                       min(self.beam, costs.shape[0]), tie_band=self.tie_band)
         beam = cand.index_select(0, pos[:int(kcnt.item())])
         mark()
-        # bad-hash memo: hashes of the bottom half at every pass depth
-        if costs.shape[0] > 1:
-            bdec = dec.index_select(0, cand.index_select(0, torch.nonzero(bot).flatten()))
-            memo = sc.memo_hashes(bdec, self.num_passes)
-        else:
-            memo = []
+        # bad-hash memo: hashes of the bottom half at every pass depth.  All
+        # representatives are hashed and the bottom half is picked after the
+        # step's one closing sync, so the host never waits mid-step here.
+        memo = sc.memo_hashes(dec.index_select(0, cand), self.num_passes) if costs.shape[0] > 1 else []
         mark()
         if times is not None:
             torch.cuda.synchronize()
             for name, a, b in zip(("hash", "featurize", "cost", "select", "cut", "memo"), ev[:-1], ev[1:]):
                 times[name] = times.get(name, 0.0) + a.elapsed_time(b)
-        return {"beam": beam.cpu().tolist(), "total": total, "verdict": f["verdict"], "memo": memo,
+        beam_host = beam.cpu().tolist()
+        if memo:
+            keep = torch.nonzero(bot).flatten()
+            memo = [m.index_select(0, keep) for m in memo]
+        return {"beam": beam_host, "total": total, "verdict": f["verdict"], "memo": memo,
                 "n_reps": int(costs.shape[0])}
 
     def _exchange(self, costs, ph, cand, nrep):
