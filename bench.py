@@ -346,8 +346,12 @@ def run_gpu(args):
         n_local = plan.local_count
         k1 = phase_ms["featurize"] / args.steps if phase_ms else None
         breakdown = {k: round(v / args.steps, 3) for k, v in phase_ms.items()}
-        # K1 algorithmic bytes per launch: 16 B decision record per row in,
-        # 448 B fp64 feature row + 4 B row key per row out, 4+1 B per candidate
+        # K1 algorithmic bytes per launch (SURVEY 8(d)'s north-star dataflow,
+        # the K1 share of B(R)): 16 B decision record per row in, 448 B fp64
+        # feature row + 4 B row key per row out, 4+1 B per candidate.  The
+        # step runs K1 in reuse mode 2, which writes only the computed rows
+        # (K2 reads repeated rows through row_src), so the measured DRAM
+        # traffic (roofline.traffic) is below this figure by design.
         bytes_k1 = n_local * (R * (16 + 448 + 4) + 5)
         peak, peak_kind = _peaks()
         achieved = bytes_k1 / (k1 / 1e3) / 1e9 if k1 else None
@@ -372,7 +376,7 @@ def run_gpu(args):
             "config": {"workload": "chain100@1024^2 beam step: 4167 parents x 240 tilings",
                        "candidates_per_step": N, "stage_rows_per_candidate": R,
                        "beam_size": BEAM, "pass_index": PASS_INDEX,
-                       "l2": "inputs larger than L2 (1.6 GB records, 44.8 GB features)",
+                       "l2": "inputs larger than L2 (1.6 GB records in, 3.7 computed feature rows of 100 per candidate out)",
                        "parallelism": f"bucket-sharded x{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "kernel": "K1 featurize (gs::featurize_kernel)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -380,8 +384,9 @@ def run_gpu(args):
                          "peak_source": peak_kind, "k1_ms_per_launch": k1,
                          "k1_share_of_step": (k1 / ms) if k1 else None,
                          "algorithmic_bytes_per_launch": bytes_k1,
-                         "note": "K1 is integer-ALU bound (resolve + warp transaction emulation); "
-                                 "the HBM fraction is reported as the north star asks"},
+                         "note": "K1 is integer-ALU / instruction-latency bound (resolve + warp transaction "
+                                 "emulation); achieved = SURVEY 8(d) algorithmic bytes / K1 time as the north "
+                                 "star asks; K1 writes only computed rows (reuse mode 2), traffic = ncu DRAM bytes"},
             "cpu_baseline": cpu,
             "e2e": {"value": N / (e / 1e3), "unit": UNIT, "ms_per_step": e,
                     "path": "StepPlan.run_beam_host: H2D beam, gs_expand_step on device, step, D2H results",

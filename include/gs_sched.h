@@ -145,7 +145,11 @@ int gs_set_weights(gs_pipeline_t p, int embed_dim, int hidden_dim,
  * every candidate is computed).  `row_src` (nullable, [N][R] int32) then
  * names, per row, the candidate whose row was actually computed and whose
  * features this row repeats bit for bit (itself when computed); gs_cost
- * uses it to evaluate the network once per distinct row. */
+ * uses it to evaluate the network once per distinct row.  2 = reuse, and
+ * feats holds only the computed rows (row_src[c*R + r] == c): repeated rows
+ * are left unwritten, for callers that consume features only through
+ * gs_cost with row_src (the beam step) — gs_featurize then requires
+ * row_src. */
 int gs_set_reuse(gs_pipeline_t p, int enable);
 
 int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,

@@ -243,13 +243,15 @@ static Layout layout_for(gs_pipeline_t p, int S, int nwarps, bool spill) {
 
 int gs_set_reuse(gs_pipeline_t p, int enable) {
   if (!p) return fail(GS_ERR_ARG, "null pipeline");
-  p->reuse = enable ? 1 : 0;
+  if (enable < 0 || enable > 2) return fail(GS_ERR_ARG, "reuse mode must be 0, 1 or 2");
+  p->reuse = enable;
   return GS_OK;
 }
 
 int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, double* feats, int32_t* row_key,
                  int32_t* n_rows, uint8_t* verdict, int32_t* row_src, void* stream) {
   if (!p || S < 1 || n < 0) return fail(GS_ERR_ARG, "bad featurize arguments");
+  if (p->reuse == 2 && feats && !row_src) return fail(GS_ERR_ARG, "reuse mode 2 (computed rows only) needs row_src");
   if (n == 0) return GS_OK;
   // one CTA per SM, as many independent scorer warps as shared memory
   // holds; pipelines whose worst-case inline expansion would leave fewer

@@ -2207,7 +2207,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     // of 16-byte vectors with four loads in flight per lane; the dirty rows
     // are then recomputed over it
     GS_MARK(3);
-    if (diffable && nd < nr) {
+    if (diffable && nd < nr && reuse != 2) {
       const int4* src = reinterpret_cast<const int4*>(feats + (int64_t)pc * L.R * GS_NUM_FEATURES);
       int4* dst = reinterpret_cast<int4*>(feats + (int64_t)c * L.R * GS_NUM_FEATURES);
       const int nv = nr * (GS_NUM_FEATURES * 8 / 16);

@@ -49,6 +49,7 @@ class Scorer:
         self.R = max(1, self.lib.gs_pipeline_max_rows(self.handle))
         self.S = max(1, self.packed.max_decisions())
         self._weights_key = None
+        self.reuse_mode = 1   # gs_set_reuse default
         if weights is not None:
             self.set_weights(weights)
 
@@ -59,9 +60,12 @@ class Scorer:
         except Exception:
             pass
 
-    def set_reuse(self, enable: bool):
-        """Exact sibling reuse in K1 (see gs_set_reuse in include/gs_sched.h)."""
-        _lib.check(self.lib.gs_set_reuse(self.handle, int(bool(enable))))
+    def set_reuse(self, enable):
+        """Exact sibling reuse in K1 (see gs_set_reuse in include/gs_sched.h):
+        False/True, or 2 = reuse with only the computed rows materialised."""
+        mode = enable if isinstance(enable, int) and not isinstance(enable, bool) else int(bool(enable))
+        _lib.check(self.lib.gs_set_reuse(self.handle, mode))
+        self.reuse_mode = mode
 
     # -- weights --------------------------------------------------------------
     def set_weights(self, weights):
@@ -113,6 +117,7 @@ class Scorer:
         _lib.check(self.lib.gs_featurize(self.handle, _ptr(dec), n, S, _ptr(out["feats"]),
                                          _ptr(out["row_key"]), _ptr(out["n_rows"]),
                                          _ptr(out["verdict"]), _ptr(out.get("row_src")), _stream()))
+        out["rows_only"] = self.reuse_mode == 2
         return out
 
     def stats(self):
@@ -142,6 +147,8 @@ class Scorer:
             reuse = src is not None and not basis
         if not reuse:
             src = None
+        if f.get("rows_only") and src is None:
+            raise ValueError("features from reuse mode 2 hold only the computed rows: cost them with row_src")
         rc = None
         if rows or src is not None:
             rc = scratch if scratch is not None else torch.empty((n, self.R), dtype=torch.float64,

@@ -32,6 +32,18 @@ class StepPlan:
         self.local_count = n
 
     def _features(self, d):
+        # the step consumes features only through K2 with row_src, so K1
+        # writes just the computed rows (reuse mode 2)
+        prev = self.sc.reuse_mode
+        if prev:
+            self.sc.set_reuse(2)
+        try:
+            return self._features_into(d)
+        finally:
+            if prev:
+                self.sc.set_reuse(prev)
+
+    def _features_into(self, d):
         m = d.shape[0]
         if self.fbuf is None or self.fbuf["feats"].shape[0] != m:
             self.fbuf = self.rcbuf = None

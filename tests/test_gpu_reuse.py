@@ -46,7 +46,7 @@ def _run(sc, recs, reuse):
     full, _, _ = sc.cost(f, reuse=False)
     sc.check()
     assert torch.equal(total, full), "row-reuse K2 differs from the full network pass"
-    return {k: v.cpu().numpy() for k, v in f.items()}, total.cpu().numpy()
+    return {k: v.cpu().numpy() for k, v in f.items() if torch.is_tensor(v)}, total.cpu().numpy()
 
 
 @pytest.mark.parametrize("src", ["chain100", "stencil_chain", "diamond", "conv"])
@@ -96,3 +96,46 @@ def test_reuse_is_bit_exact(src, dev):
         rows = features.featurize_rows(graph, _decisions(info, recs[i]), PARAMS)
         want = np.array([f for _, f, _ in rows])
         assert np.array_equal(on["feats"][i, :len(rows)], want), (src, i)
+
+
+@pytest.mark.parametrize("src,parents", [("chain100", 40), ("diamond", 6)])
+def test_rows_only_mode(src, parents, dev):
+    """Reuse mode 2 (the beam step's mode): K1 writes only the computed rows;
+    those rows, row_src, verdicts and the K2 totals equal mode 1's."""
+    from paper_2012_07145_b200 import gen
+    from paper_2012_07145_b200.engine import Scorer
+    from paper_2012_07145_b200.params import OPEN_THRESHOLDS
+    from golden_io import candidate_set
+    if src == "chain100":
+        import bench
+        graph, recs, _ = bench._workload(parents)   # >= 8192 candidates: two-phase K1
+        th = None
+    else:
+        graph = candidate_set(src).graph
+        par, _, _ = gen.random_schedules(graph, parents, seed=11)
+        steps = np.array([[i for i in range(par.shape[1]) if par[p, i]["kind"] == 0][0]
+                          for p in range(len(par))])
+        recs, _ = gen.expand_step(par, steps, graph)
+        th = OPEN_THRESHOLDS
+    sc = Scorer(graph, PARAMS, th, weights())
+    d = sc.to_device(recs)
+    sc.set_reuse(True)
+    f1 = sc.featurize(d)
+    t1, _, _ = sc.cost(f1)
+    a = {k: v.cpu().numpy() for k, v in f1.items() if torch.is_tensor(v)}
+    sc.set_reuse(2)
+    f2 = sc.featurize(d)
+    f2["feats"].fill_(float("nan"))   # unwritten rows must never be read
+    f2 = sc.featurize(d, out=f2)
+    t2, _, _ = sc.cost(f2)
+    sc.check()
+    b = {k: v.cpu().numpy() for k, v in f2.items() if torch.is_tensor(v)}
+    for k in ("n_rows", "verdict", "row_key", "row_src"):
+        assert np.array_equal(a[k], b[k]), k
+    own = b["row_src"] == np.arange(len(recs))[:, None]
+    own &= np.arange(sc.R)[None, :] < b["n_rows"][:, None]
+    assert np.array_equal(a["feats"][own], b["feats"][own])
+    assert torch.equal(t1, t2)
+    with pytest.raises(ValueError):
+        sc.cost(f2, reuse=False)
+    sc.set_reuse(True)
