@@ -43,6 +43,9 @@ __device__ __forceinline__ double softplus(double z) {
 }
 
 // reference stage_cost_basis; returns h, writes g (may be null)
+// c: the 30 coefficients, strided by ZS (per-thread column of a
+// shared-memory scratch; ZS = threads per block)
+template <int ZS>
 __device__ double basis_dot(const double* __restrict__ f, const double* __restrict__ c, double* gout) {
   auto F = [&](int i) { return f[i]; };
   const bool inl = F(50) > 0;
@@ -78,7 +81,7 @@ __device__ double basis_dot(const double* __restrict__ f, const double* __restri
   g[9] = F(55);
   double dot = 0.0;
 #pragma unroll
-  for (int i = 0; i < GS_NUM_COEFFS; ++i) dot = fma(g[i], c[i], dot);
+  for (int i = 0; i < GS_NUM_COEFFS; ++i) dot = fma(g[i], c[i * ZS], dot);
   if (gout) {
 #pragma unroll
     for (int i = 0; i < GS_NUM_COEFFS; ++i) gout[i] = g[i];
@@ -87,11 +90,11 @@ __device__ double basis_dot(const double* __restrict__ f, const double* __restri
   return __dadd_rn(dot, h);
 }
 
-template <int MAXE>
+template <int MAXE, int ZS>
 __device__ double stage_row_cost(const NetDev& net, const double* __restrict__ sw, const double* __restrict__ whs,
                            const double* __restrict__ wo, const double* __restrict__ bs,
                            const double* __restrict__ bo, const double* __restrict__ f, int stage,
-                           double* gout) {
+                           double* gout, double* zs) {
   const int E = net.E, H = net.H;
   double es[MAXE];
 #pragma unroll
@@ -138,10 +141,14 @@ __device__ double stage_row_cost(const NetDev& net, const double* __restrict__ s
       for (int o = 0; o < GS_NUM_COEFFS; ++o) zo[o] = fma(z, wo[i * GS_NUM_COEFFS + o], zo[o]);
     }
   }
-  double c[GS_NUM_COEFFS];
+  // softplus through a per-thread shared-memory column and a rolled loop:
+  // thirty inlined exp + log1p sequences were ~80% of the kernel's code
+  // and overflowed the instruction cache
 #pragma unroll
-  for (int o = 0; o < GS_NUM_COEFFS; ++o) c[o] = softplus(zo[o]) + kEps;
-  return basis_dot(f, c, gout);
+  for (int o = 0; o < GS_NUM_COEFFS; ++o) zs[o * ZS] = zo[o];
+#pragma unroll 1
+  for (int o = 0; o < GS_NUM_COEFFS; ++o) zs[o * ZS] = softplus(zs[o * ZS]) + kEps;
+  return basis_dot<ZS>(f, zs, gout);
 }
 
 template <int MAXE>
@@ -159,6 +166,7 @@ __global__ void __launch_bounds__(128) cost_kernel(NetDev net, const int32_t* __
   double* bs = wo + H * GS_NUM_COEFFS;       // E
   double* bo = bs + E;                       // 30
   double* buf = bo + GS_NUM_COEFFS;          // CB*R
+  double* zs = buf + CB * R + threadIdx.x;   // 30 x 128 softplus scratch
   for (int i = threadIdx.x; i < GS_NUM_FEATURES * E; i += blockDim.x) sw[i] = net.sched_w[i];
   for (int i = threadIdx.x; i < E * H; i += blockDim.x) whs[i] = net.head_w[E * H + i];
   for (int i = threadIdx.x; i < H * GS_NUM_COEFFS; i += blockDim.x) wo[i] = net.out_w[i];
@@ -174,8 +182,8 @@ __global__ void __launch_bounds__(128) cost_kernel(NetDev net, const int32_t* __
       const int64_t row = c * R + r;
       const int key = row_key[row];
       const int stage = stage_of_func[key >> 8] + (key & 255);
-      const double v = stage_row_cost<MAXE>(net, sw, whs, wo, bs, bo, feats + row * GS_NUM_FEATURES, stage,
-                                       basis_gh ? basis_gh + row * (GS_NUM_COEFFS + 1) : nullptr);
+      const double v = stage_row_cost<MAXE, 128>(net, sw, whs, wo, bs, bo, feats + row * GS_NUM_FEATURES, stage,
+                                       basis_gh ? basis_gh + row * (GS_NUM_COEFFS + 1) : nullptr, zs);
       buf[idx] = v;
       if (row_cost) row_cost[row] = v;
     }
@@ -193,62 +201,85 @@ __global__ void __launch_bounds__(128) cost_kernel(NetDev net, const int32_t* __
 
 // Exact row reuse (gs_featurize row_src): a row whose features repeat
 // candidate row_src[row]'s row bit for bit has that row's cost, so the
-// network runs once per distinct row.  Pass A compacts the computed rows of
-// a chunk in shared memory (full warps run the network), pass B gathers
-// every row's cost from its source and adds a candidate's rows in order.
-constexpr int kChunk = 8192;
+// network runs once per distinct row.  Pass A: every warp scans 32-row
+// slabs (2048-row spans, round-robin over the grid) and queues its computed rows in a
+// 64-entry shared-memory ring; whenever 32 are queued, one per lane runs
+// the network, so lanes stay full and no block-wide barrier or per-chunk
+// tail idles the SM.  Pass B gathers every row's cost from its source and
+// adds a candidate's rows in order.
+constexpr int kRowsWarps = 12;   // one 384-thread CTA per SM (166 registers)
+constexpr unsigned kRing = 256;   // per-warp queue (>= 31 + kBatch slabs x 32)
 
 template <int MAXE>
-__global__ void __launch_bounds__(128) cost_rows_kernel(NetDev net, const int32_t* __restrict__ stage_of_func,
+__global__ void __launch_bounds__(kRowsWarps * 32, 1) cost_rows_kernel(NetDev net, const int32_t* __restrict__ stage_of_func,
                                                         const double* __restrict__ feats,
                                                         const int32_t* __restrict__ row_key,
                                                         const int32_t* __restrict__ n_rows,
                                                         const int32_t* __restrict__ row_src, int64_t n, int R,
                                                         double* __restrict__ row_cost) {
   extern __shared__ __align__(16) double smd[];
+  __shared__ int64_t ring[kRowsWarps][kRing];
   const int E = net.E, H = net.H;
   double* sw = smd;
   double* whs = sw + GS_NUM_FEATURES * E;
   double* wo = whs + E * H;
   double* bs = wo + H * GS_NUM_COEFFS;
   double* bo = bs + E;
-  int32_t* list = reinterpret_cast<int32_t*>(bo + GS_NUM_COEFFS);   // kChunk
-  __shared__ int cnt;
+  double* zs = bo + GS_NUM_COEFFS + threadIdx.x;   // 30 x (threads) softplus scratch
   for (int i = threadIdx.x; i < GS_NUM_FEATURES * E; i += blockDim.x) sw[i] = net.sched_w[i];
   for (int i = threadIdx.x; i < E * H; i += blockDim.x) whs[i] = net.head_w[E * H + i];
   for (int i = threadIdx.x; i < H * GS_NUM_COEFFS; i += blockDim.x) wo[i] = net.out_w[i];
   for (int i = threadIdx.x; i < E; i += blockDim.x) bs[i] = net.sched_b[i];
   for (int i = threadIdx.x; i < GS_NUM_COEFFS; i += blockDim.x) bo[i] = net.out_b[i];
+  __syncthreads();
   const int64_t total_rows = n * (int64_t)R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t base = (int64_t)blockIdx.x * kChunk; base < total_rows; base += (int64_t)gridDim.x * kChunk) {
-    if (threadIdx.x == 0) cnt = 0;
-    __syncthreads();
-    for (int i0 = 0; i0 < kChunk; i0 += blockDim.x) {
-      const int i = i0 + threadIdx.x;
-      const int64_t row = base + i;
-      bool t = false;
-      if (row < total_rows) {
-        const int64_t c = row / R;
-        const int r = (int)(row - c * R);
-        t = r < n_rows[c] && row_src[row] == (int32_t)c;
+  int64_t* q = ring[warp];
+  auto run = [&](int64_t row) {
+    const int key = row_key[row];
+    const int stage = stage_of_func[key >> 8] + (key & 255);
+    row_cost[row] = stage_row_cost<MAXE, kRowsWarps * 32>(net, sw, whs, wo, bs, bo, feats + row * GS_NUM_FEATURES, stage, nullptr,
+                                         zs);
+  };
+  // warps take 2048-row spans round-robin and walk a span's slabs in
+  // order, so a queue holds rows of neighbouring candidates (siblings: the
+  // same stages, similar features, little divergence).  The ownership
+  // flags of 4 slabs are loaded together (4 loads in flight per lane) into
+  // a circular queue; the network is evaluated at ONE call site (its code
+  // is large: a second inlined copy would thrash the instruction cache).
+  constexpr int64_t kSpan = 2048;
+  constexpr int kBatch = 4;
+  const int64_t nwarp = (int64_t)gridDim.x * kRowsWarps;
+  int64_t sp = (int64_t)blockIdx.x * kRowsWarps + warp, s0 = sp * kSpan;
+  unsigned head = 0, tail = 0;
+  for (;;) {
+    while (tail - head < 32 && s0 < total_rows) {
+      const int64_t end = sp * kSpan + kSpan < total_rows ? sp * kSpan + kSpan : total_rows;
+      unsigned tm = 0;
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int64_t row = s0 + 32 * u + lane;
+        if (row < end) {
+          const int64_t c = row / R;
+          const int r = (int)(row - c * R);
+          tm |= (unsigned)(r < __ldg(n_rows + c) && __ldg(row_src + row) == (int32_t)c) << u;
+        }
       }
-      const unsigned b = __ballot_sync(0xffffffffu, t);
-      int pos = 0;
-      if (lane == 0 && b) pos = atomicAdd(&cnt, __popc(b));
-      pos = __shfl_sync(0xffffffffu, pos, 0);
-      if (t) list[pos + __popc(b & ((1u << lane) - 1))] = i;
+#pragma unroll 1
+      for (int u = 0; u < kBatch; ++u) {
+        const bool t = (tm >> u) & 1u;
+        const unsigned b = __ballot_sync(0xffffffffu, t);
+        if (t) q[(tail + __popc(b & ((1u << lane) - 1))) & (kRing - 1)] = s0 + 32 * u + lane;
+        tail += __popc(b);
+      }
+      s0 += 32 * kBatch;
+      if (s0 >= end) { sp += nwarp; s0 = sp * kSpan; }
     }
-    __syncthreads();
-    const int m = cnt;
-    (void)warp;
-    for (int q = threadIdx.x; q < m; q += blockDim.x) {
-      const int64_t row = base + list[q];
-      const int key = row_key[row];
-      const int stage = stage_of_func[key >> 8] + (key & 255);
-      row_cost[row] = stage_row_cost<MAXE>(net, sw, whs, wo, bs, bo, feats + row * GS_NUM_FEATURES, stage, nullptr);
-    }
-    __syncthreads();
+    if (tail == head) break;
+    __syncwarp();
+    if (head + lane < tail) run(q[(head + lane) & (kRing - 1)]);
+    head += tail - head < 32 ? tail - head : 32;
+    __syncwarp();
   }
 }
 
@@ -289,7 +320,7 @@ int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream
 }
 
 int cost_smem_bytes(int E, int H, int CB, int R) {
-  return (GS_NUM_FEATURES * E + E * H + H * GS_NUM_COEFFS + E + GS_NUM_COEFFS + CB * R) * 8;
+  return (GS_NUM_FEATURES * E + E * H + H * GS_NUM_COEFFS + E + GS_NUM_COEFFS + CB * R + GS_NUM_COEFFS * 128) * 8;
 }
 
 int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
@@ -298,18 +329,18 @@ int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* f
   if (n == 0) return 0;
   if (row_src && row_cost && !basis_gh) {
     if (net.E > 64) return -1;
-    const int smA = (GS_NUM_FEATURES * net.E + net.E * net.H + net.H * GS_NUM_COEFFS + net.E + GS_NUM_COEFFS) * 8 +
-                    kChunk * 4;
-    const int64_t chunks = (n * (int64_t)R + kChunk - 1) / kChunk;
-    const int gridA = (int)(chunks < (int64_t)num_sms * 8 ? chunks : (int64_t)num_sms * 8);
+    const int smA = (GS_NUM_FEATURES * net.E + net.E * net.H + net.H * GS_NUM_COEFFS + net.E + GS_NUM_COEFFS +
+                     GS_NUM_COEFFS * kRowsWarps * 32) * 8;
+    const int64_t slabs = (n * (int64_t)R + kRowsWarps * 32 - 1) / (kRowsWarps * 32);
+    const int gridA = (int)(slabs < (int64_t)num_sms ? slabs : (int64_t)num_sms);
     if (net.E <= 32) {
       cudaFuncSetAttribute(cost_rows_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smA);
-      cost_rows_kernel<32><<<gridA, 128, smA, st>>>(net, stage_of_func, feats, row_key, n_rows, row_src, n, R,
-                                                    row_cost);
+      cost_rows_kernel<32><<<gridA, kRowsWarps * 32, smA, st>>>(net, stage_of_func, feats, row_key, n_rows, row_src,
+                                                                n, R, row_cost);
     } else {
       cudaFuncSetAttribute(cost_rows_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smA);
-      cost_rows_kernel<64><<<gridA, 128, smA, st>>>(net, stage_of_func, feats, row_key, n_rows, row_src, n, R,
-                                                    row_cost);
+      cost_rows_kernel<64><<<gridA, kRowsWarps * 32, smA, st>>>(net, stage_of_func, feats, row_key, n_rows, row_src,
+                                                                n, R, row_cost);
     }
     g_launch_count++;
     int CB = 1024 / (R > 0 ? R : 1);

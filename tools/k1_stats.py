@@ -13,6 +13,7 @@ from paper_2012_07145_b200.params import DEFAULT_THRESHOLDS, MachineParams, init
 n_par = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
 graph, recs, _ = bench._workload(n_par)
 sc = Scorer(graph, MachineParams(), DEFAULT_THRESHOLDS, init_weights(0))
+sc.set_reuse(int(os.environ.get("GS_REUSE", "2")))   # the beam step's mode
 dec = sc.to_device(recs)
 f = sc.featurize(dec)
 sc.cost(f)
