@@ -240,8 +240,14 @@ __global__ void __launch_bounds__(kHashWarps * 32) hash_warp_kernel(
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint8_t* buf = smh + wib * (kHashBuf + 2 * kHashMaxFuncs);
   int16_t* didx = reinterpret_cast<int16_t*>(buf + kHashBuf);
+  // contiguous candidate ranges per warp: run heads are periodic in a beam
+  // step (one per parent), and a grid stride sharing a factor with that
+  // period would hand all of them to a few warps
   const int64_t nwarps = (int64_t)gridDim.x * kHashWarps;
-  for (int64_t c = (int64_t)blockIdx.x * kHashWarps + wib; c < n; c += nwarps) {
+  const int64_t wid = (int64_t)blockIdx.x * kHashWarps + wib;
+  const int64_t per = (n + nwarps - 1) / nwarps;
+  const int64_t c_end = (wid + 1) * per < n ? (wid + 1) * per : n;
+  for (int64_t c = wid * per; c < c_end; ++c) {
     if (head && !head[c]) continue;
     const GsDecision* d = dec + c * S;
     for (int f = lane; f < nf; f += 32) didx[f] = -1;
