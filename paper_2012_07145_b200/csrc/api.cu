@@ -22,7 +22,7 @@ int read_phases(long long* out);
 int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st);
 int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
                 const int32_t* n_rows, const int32_t* row_src, int64_t n, int R, double* total, double* row_cost,
-                double* basis_gh, int num_sms, cudaStream_t st);
+                double* basis_gh, unsigned* work, int num_sms, cudaStream_t st);
 int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, const int32_t* sorted_funcs,
                 const uint8_t* names, const int32_t* name_off, uint64_t* out, uint8_t* head, int repr_bound,
                 int num_sms, cudaStream_t st);
@@ -195,7 +195,7 @@ int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
   CK(cudaMemcpy(p->names, d->name_repr, nb, cudaMemcpyHostToDevice));
   CK(cudaMalloc(&p->name_off, 4 * (h.nf + 1)));
   CK(cudaMemcpy(p->name_off, d->name_off, 4 * (h.nf + 1), cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&p->err, 64));   // [0] error word, [2..] K1 work counters (u64)
+  CK(cudaMalloc(&p->err, 64));   // [0] error word, [2..13] K1 stats (u64), [14] K1 / [15] K2 work-unit counters
   CK(cudaMemset(p->err, 0, 64));
   *out = p;
   return GS_OK;
@@ -356,7 +356,8 @@ int gs_cost(gs_pipeline_t p, const double* feats, const int32_t* row_key, const 
   if (!p || !p->net.sched_w) return fail(GS_ERR_ARG, "weights not set (gs_set_weights)");
   if (row_src && !row_cost) return fail(GS_ERR_ARG, "row reuse (row_src) needs the row_cost buffer");
   int rc = launch_cost(p->net, p->stage_of_func, feats, row_key, n_rows, row_src, n, std::max(1, p->host.max_rows),
-                       total, row_cost, basis_gh, p->num_sms, (cudaStream_t)stream);
+                       total, row_cost, basis_gh, reinterpret_cast<unsigned*>(p->err + 15), p->num_sms,
+                       (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "unsupported network dims");
   CK(cudaGetLastError());
   return GS_OK;

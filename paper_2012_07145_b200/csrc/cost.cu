@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) cost_rows_kernel(NetDev ne
                                                         const int32_t* __restrict__ row_key,
                                                         const int32_t* __restrict__ n_rows,
                                                         const int32_t* __restrict__ row_src, int64_t n, int R,
-                                                        double* __restrict__ row_cost) {
+                                                        double* __restrict__ row_cost, unsigned* __restrict__ work) {
   extern __shared__ __align__(16) double smd[];
   __shared__ int64_t ring[kRowsWarps][kRing];
   const int E = net.E, H = net.H;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) cost_rows_kernel(NetDev ne
     row_cost[row] = stage_row_cost<MAXE, kRowsWarps * 32>(net, sw, whs, wo, bs, bo, feats + row * GS_NUM_FEATURES, stage, nullptr,
                                          zs);
   };
-  // warps take 2048-row spans round-robin and walk a span's slabs in
+  // warps take 2048-row spans and walk a span's slabs in
   // order, so a queue holds rows of neighbouring candidates (siblings: the
   // same stages, similar features, little divergence).  The ownership
   // flags of 4 slabs are loaded together (4 loads in flight per lane) into
@@ -249,8 +249,14 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) cost_rows_kernel(NetDev ne
   // is large: a second inlined copy would thrash the instruction cache).
   constexpr int64_t kSpan = 2048;
   constexpr int kBatch = 4;
-  const int64_t nwarp = (int64_t)gridDim.x * kRowsWarps;
-  int64_t sp = (int64_t)blockIdx.x * kRowsWarps + warp, s0 = sp * kSpan;
+  // spans are claimed dynamically (the computed-row density varies along
+  // the batch, so a static round-robin leaves SMs idle at the end)
+  auto claim = [&]() -> int64_t {
+    unsigned v = 0;
+    if (lane == 0) v = atomicAdd(work, 1u);
+    return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+  };
+  int64_t sp = claim(), s0 = sp * kSpan;
   unsigned head = 0, tail = 0;
   for (;;) {
     while (tail - head < 32 && s0 < total_rows) {
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) cost_rows_kernel(NetDev ne
         tail += __popc(b);
       }
       s0 += 32 * kBatch;
-      if (s0 >= end) { sp += nwarp; s0 = sp * kSpan; }
+      if (s0 >= end) { sp = claim(); s0 = sp * kSpan; }
     }
     if (tail == head) break;
     __syncwarp();
@@ -325,9 +331,11 @@ int cost_smem_bytes(int E, int H, int CB, int R) {
 
 int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
                 const int32_t* n_rows, const int32_t* row_src, int64_t n, int R, double* total, double* row_cost,
-                double* basis_gh, int num_sms, cudaStream_t st) {
+                double* basis_gh, unsigned* work, int num_sms, cudaStream_t st) {
   if (n == 0) return 0;
   if (row_src && row_cost && !basis_gh) {
+    if (n * (int64_t)R / 2048 >= 0xFFFFFFFFll) return -1;
+    cudaMemsetAsync(work, 0, sizeof(unsigned), st);
     if (net.E > 64) return -1;
     const int smA = (GS_NUM_FEATURES * net.E + net.E * net.H + net.H * GS_NUM_COEFFS + net.E + GS_NUM_COEFFS +
                      GS_NUM_COEFFS * kRowsWarps * 32) * 8;
@@ -336,11 +344,11 @@ int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* f
     if (net.E <= 32) {
       cudaFuncSetAttribute(cost_rows_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smA);
       cost_rows_kernel<32><<<gridA, kRowsWarps * 32, smA, st>>>(net, stage_of_func, feats, row_key, n_rows, row_src,
-                                                                n, R, row_cost);
+                                                                n, R, row_cost, work);
     } else {
       cudaFuncSetAttribute(cost_rows_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smA);
       cost_rows_kernel<64><<<gridA, kRowsWarps * 32, smA, st>>>(net, stage_of_func, feats, row_key, n_rows, row_src,
-                                                                n, R, row_cost);
+                                                                n, R, row_cost, work);
     }
     g_launch_count++;
     int CB = 1024 / (R > 0 ? R : 1);
