@@ -2081,7 +2081,14 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   // each head's warp state saved to its run's slot; 2 siblings in kChunk2
   // slices, a slice resuming from its run head's saved state (no re-resolve,
   // no row recompute), so runs split freely across warps.
-  const int64_t nchunks = (n + kChunk2 - 1) / kChunk2;
+  // The last ~2 slices per warp are cut 4x finer (8 candidates), so the
+  // launch does not end waiting on a few warps' full 32-candidate slices;
+  // a slice costs one 26 KB state restore, small against 8 candidates.
+  const int64_t nbig_all = (n + kChunk2 - 1) / kChunk2;
+  const int64_t tail_big = 2 * (int64_t)gridDim.x * nw < nbig_all ? 2 * (int64_t)gridDim.x * nw : nbig_all;
+  const int64_t nbig = nbig_all - tail_big;
+  constexpr int kFine = kChunk2 / 4;
+  const int64_t nchunks = nbig + (n - nbig * kChunk2 + kFine - 1) / kFine;
   // warp state <-> run slot: the shared-memory slice and the global scratch
   auto slot_copy = [&](int64_t r, bool save) {
     uint8_t* sl = slots + r * slot_bytes;
@@ -2110,7 +2117,8 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     c0 = run_head[j]; c1 = c0 + 1;
   } else {
     if (j >= nchunks) break;
-    c0 = j * kChunk2; c1 = c0 + kChunk2 < n ? c0 + kChunk2 : n;
+    if (j < nbig) { c0 = j * kChunk2; c1 = c0 + kChunk2; }
+    else { c0 = nbig * kChunk2 + (j - nbig) * kFine; c1 = c0 + kFine < n ? c0 + kFine : n; }
   }
   if (c0 >= c1) continue;
   if (lane == 0) { m.prev_valid = 0; m.same_struct = 0; m.ndec = 0; }
