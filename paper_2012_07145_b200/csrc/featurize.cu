@@ -2085,9 +2085,9 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   // launch does not end waiting on a few warps' full 32-candidate slices;
   // a slice costs one 26 KB state restore, small against 8 candidates.
   const int64_t nbig_all = (n + kChunk2 - 1) / kChunk2;
-  const int64_t tail_big = 2 * (int64_t)gridDim.x * nw < nbig_all ? 2 * (int64_t)gridDim.x * nw : nbig_all;
+  const int64_t tail_big = 3 * (int64_t)gridDim.x * nw < nbig_all ? 3 * (int64_t)gridDim.x * nw : nbig_all;
   const int64_t nbig = nbig_all - tail_big;
-  constexpr int kFine = kChunk2 / 4;
+  constexpr int kFine = kChunk2 / 8;
   const int64_t nchunks = nbig + (n - nbig * kChunk2 + kFine - 1) / kFine;
   // warp state <-> run slot: the shared-memory slice and the global scratch
   auto slot_copy = [&](int64_t r, bool save) {
