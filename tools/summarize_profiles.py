@@ -28,7 +28,10 @@ RAW = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"
        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
        "smsp__issue_active.avg.pct_of_peak_sustained_active",
-       "sm__cycles_active.avg", "gpc__cycles_elapsed.max"]
+       "sm__cycles_active.avg", "gpc__cycles_elapsed.max",
+       "smsp__thread_inst_executed_per_inst_executed.ratio"] + [
+       f"smsp__average_warps_issue_stalled_{r}_per_issue_active.ratio"
+       for r in ("no_instruction", "long_scoreboard", "wait", "short_scoreboard", "barrier", "branch_resolving")]
 
 
 def ncu(*args):
