@@ -248,6 +248,25 @@ int gs_expand_step(gs_pipeline_t p, const GsDecision* parents, int64_t n_parents
                    void* workspace, int64_t ws_bytes, GsDecision* out, int32_t* owner,
                    void* stream);
 
+/* ---- machine oracle ------------------------------
+ * The throughput knobs of reference machine.py:26-31 (not hardware limits). */
+typedef struct {
+  int32_t registers_per_thread_budget;   /* register_bytes_per_thread = 4 x this */
+  int32_t pad;
+  double compute_throughput;             /* scalar ops / s at full occupancy */
+  double global_bandwidth, shared_bandwidth;   /* bytes / s */
+  double kernel_launch_overhead;         /* s */
+} GsOracleParams;
+
+/* K1 (every row materialised, plus each row's kernel) then K6: the
+ * reference's simulate_runtime (machine.py:108-167) for N candidates.
+ * Device outputs per candidate: runtime[c] (s; NaN unless status 0),
+ * spill_bytes[c] (> 0 iff registers spilled), status[c]: 0 ok, 1 a kernel
+ * breaks a hardware limit, 2 not fully scheduled (the reference raises
+ * ValueError for both).  Uses a grow-only internal feature workspace. */
+int gs_simulate(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s, const GsOracleParams* op,
+                double* runtime, int64_t* spill_bytes, uint8_t* status, void* stream);
+
 /* Device-side error word of the last K1 launch (capacity overflow etc.);
  * synchronizes `stream`. */
 int gs_check(gs_pipeline_t p, void* stream);

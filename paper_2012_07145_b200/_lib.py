@@ -19,7 +19,7 @@ EXPORTS = ("gs_last_error", "gs_version", "gs_launch_count", "gs_pipeline_create
            "gs_pipeline_max_rows", "gs_set_weights", "gs_set_reuse", "gs_featurize", "gs_cost",
            "gs_struct_hash", "gs_select_workspace_bytes", "gs_select_reps",
            "gs_topk_workspace_bytes", "gs_beam_topk", "gs_check", "gs_stats", "gs_debug_phases",
-           "gs_expand_workspace_bytes", "gs_expand_step")
+           "gs_expand_workspace_bytes", "gs_expand_step", "gs_simulate")
 
 
 class GsError(RuntimeError):
@@ -59,6 +59,7 @@ def load(path: str = LIB_PATH):
         "gs_debug_phases": (i32, [V]),
         "gs_expand_workspace_bytes": (i64, [i64]),
         "gs_expand_step": (i32, [P, V, i64, i32, V, V, V, V, i64, V, V, V]),
+        "gs_simulate": (i32, [P, V, i64, i32, V, V, V, V, V]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

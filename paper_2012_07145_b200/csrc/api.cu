@@ -13,7 +13,11 @@ int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDeci
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
                      const Layout& L, int nwarps, int grid, int* gerr, int reuse, uint8_t* gscratch,
                      uint8_t* heads, int mode, const int32_t* run_id, const int32_t* run_head, int64_t nruns,
-                     uint8_t* slots, int64_t slot_bytes, cudaStream_t st);
+                     uint8_t* slots, int64_t slot_bytes, int32_t* row_kernel, cudaStream_t st);
+int launch_simulate(const GsFunc* funcs, int nf, const GsDecision* dec, int64_t n, int S, const double* feats,
+                    const int32_t* row_key, const int32_t* n_rows, const int32_t* row_kernel, int R,
+                    const int32_t* stage_of_func, const double* algo, const GsMachine& m, const GsOracleParams& op,
+                    double* runtime, int64_t* spill_bytes, uint8_t* status, cudaStream_t st);
 int64_t k1_prepare_runs(const GsDecision* dec, int64_t n, int S, uint8_t* heads, int32_t* run_id,
                         int32_t* run_head, void* tmp, size_t tmp_bytes, cudaStream_t st);
 size_t k1_runs_tmp_bytes(int64_t n);
@@ -84,6 +88,8 @@ struct GsPipeline {
   int64_t slotcap = 0;
   int64_t gcap = 0;
   int64_t hcap = 0;
+  uint8_t* simbuf = nullptr;     // K6: features, row keys / kernels, n_rows, verdicts (grow-only)
+  int64_t simcap = 0;
 };
 
 extern "C" {
@@ -204,7 +210,7 @@ int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
 int gs_pipeline_destroy(gs_pipeline_t p) {
   if (!p) return GS_OK;
   cudaFree(p->dev); cudaFree(p->blob); cudaFree(p->stage_of_func); cudaFree(p->algo); cudaFree(p->sorted);
-  cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err); cudaFree(p->hscratch); cudaFree(p->gscratch); cudaFree(p->k1heads); cudaFree(p->runbuf); cudaFree(p->slots);
+  cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err); cudaFree(p->hscratch); cudaFree(p->gscratch); cudaFree(p->k1heads); cudaFree(p->runbuf); cudaFree(p->slots); cudaFree(p->simbuf);
   for (double* b : p->wbufs) cudaFree(b);
   delete p;
   return GS_OK;
@@ -248,10 +254,12 @@ int gs_set_reuse(gs_pipeline_t p, int enable) {
   return GS_OK;
 }
 
-int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, double* feats, int32_t* row_key,
-                 int32_t* n_rows, uint8_t* verdict, int32_t* row_src, void* stream) {
-  if (!p || S < 1 || n < 0) return fail(GS_ERR_ARG, "bad featurize arguments");
-  if (p->reuse == 2 && feats && !row_src) return fail(GS_ERR_ARG, "reuse mode 2 (computed rows only) needs row_src");
+}  // extern "C"
+
+// K1 with an explicit reuse mode and the optional per-row kernel output
+static int featurize_impl(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, double* feats,
+                          int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
+                          int32_t* row_kernel, int reuse, void* stream) {
   if (n == 0) return GS_OK;
   // one CTA per SM, as many independent scorer warps as shared memory
   // holds; pipelines whose worst-case inline expansion would leave fewer
@@ -296,7 +304,7 @@ int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, doubl
   // re-resolving.  Needs one host sync to size the per-run state.
   int rc = 0;
   bool two_phase = false;
-  if (p->reuse && feats && n >= 8192) {
+  if (reuse && feats && n >= 8192) {
     const size_t tmpb = (k1_runs_tmp_bytes(n) + 255) & ~(size_t)255;
     const int64_t need = (int64_t)tmpb + 8 * n + 256;
     if (need > p->runcap) {
@@ -323,19 +331,60 @@ int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, doubl
         p->slotcap = nruns * slot_bytes;
       }
       rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L,
-                            nwarps, (int)grid, p->err, p->reuse, p->gscratch, p->k1heads, 1, run_id, run_head, nruns,
-                            p->slots, slot_bytes, st);
+                            nwarps, (int)grid, p->err, reuse, p->gscratch, p->k1heads, 1, run_id, run_head, nruns,
+                            p->slots, slot_bytes, row_kernel, st);
       if (!rc)
         rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L,
-                              nwarps, (int)grid, p->err, p->reuse, p->gscratch, p->k1heads, 2, run_id, run_head,
-                              nruns, p->slots, slot_bytes, st);
+                              nwarps, (int)grid, p->err, reuse, p->gscratch, p->k1heads, 2, run_id, run_head,
+                              nruns, p->slots, slot_bytes, row_kernel, st);
     }
   }
   if (!two_phase)
     rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L,
-                          nwarps, (int)grid, p->err, p->reuse, p->gscratch, p->k1heads, 0, nullptr, nullptr, 0,
-                          nullptr, 0, st);
+                          nwarps, (int)grid, p->err, reuse, p->gscratch, p->k1heads, 0, nullptr, nullptr, 0,
+                          nullptr, 0, row_kernel, st);
   if (rc) return fail(GS_ERR_ARG, "unsupported ndim");
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
+extern "C" {
+
+int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, double* feats, int32_t* row_key,
+                 int32_t* n_rows, uint8_t* verdict, int32_t* row_src, void* stream) {
+  if (!p || S < 1 || n < 0) return fail(GS_ERR_ARG, "bad featurize arguments");
+  if (p->reuse == 2 && feats && !row_src) return fail(GS_ERR_ARG, "reuse mode 2 (computed rows only) needs row_src");
+  return featurize_impl(p, dec, n, S, feats, row_key, n_rows, verdict, row_src, nullptr, p->reuse, stream);
+}
+
+int gs_simulate(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, const GsOracleParams* op,
+                double* runtime, int64_t* spill_bytes, uint8_t* status, void* stream) {
+  if (!p || !op || S < 1 || n < 0 || (n > 0 && (!dec || !runtime || !spill_bytes || !status)))
+    return fail(GS_ERR_ARG, "bad simulate arguments");
+  if (op->registers_per_thread_budget <= 0) return fail(GS_ERR_ARG, "registers_per_thread_budget must be positive");
+  if (n == 0) return GS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int R = std::max(1, p->host.max_rows);
+  const int64_t fb = n * R * GS_NUM_FEATURES * 8, kb = ((n * R * 4 + 255) / 256) * 256;
+  const int64_t need = fb + 2 * kb + ((n * 4 + 255) / 256) * 256 + n + 256;
+  if (need > p->simcap) {
+    CK(cudaStreamSynchronize(st));
+    if (p->simbuf) CK(cudaFree(p->simbuf));
+    p->simbuf = nullptr;
+    p->simcap = 0;
+    CK(cudaMalloc(&p->simbuf, (size_t)need));
+    p->simcap = need;
+  }
+  double* feats = reinterpret_cast<double*>(p->simbuf);
+  int32_t* row_key = reinterpret_cast<int32_t*>(p->simbuf + fb);
+  int32_t* row_kernel = reinterpret_cast<int32_t*>(p->simbuf + fb + kb);
+  int32_t* n_rows = reinterpret_cast<int32_t*>(p->simbuf + fb + 2 * kb);
+  uint8_t* verdict = p->simbuf + fb + 2 * kb + ((n * 4 + 255) / 256) * 256;
+  int rc = featurize_impl(p, dec, n, S, feats, row_key, n_rows, verdict, nullptr, row_kernel, p->reuse ? 1 : 0,
+                          stream);
+  if (rc) return rc;
+  launch_simulate(reinterpret_cast<const GsFunc*>(p->blob), p->host.nf, dec, n, S, feats, row_key, n_rows,
+                  row_kernel, R, p->stage_of_func, p->algo, p->host.m, *op, runtime, spill_bytes, status, st);
   CK(cudaGetLastError());
   return GS_OK;
 }

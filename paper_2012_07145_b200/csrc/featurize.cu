@@ -2008,7 +2008,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
                  int32_t* __restrict__ n_rows, uint8_t* __restrict__ verdict, int32_t* __restrict__ row_src,
                  Layout L, int* gerr, int reuse, uint8_t* __restrict__ gscratch, const uint8_t* __restrict__ heads,
                  int mode, const int32_t* __restrict__ run_id, const int32_t* __restrict__ run_head, int64_t nruns,
-                 uint8_t* __restrict__ slots, int64_t slot_bytes) {
+                 uint8_t* __restrict__ slots, int64_t slot_bytes, int32_t* __restrict__ row_kernel) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar;
   const int warp = threadIdx.x >> 5, lane = lane_id(), nw = blockDim.x >> 5;
@@ -2238,6 +2238,18 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     for (int r = lane; r < nr; r += 32) {
       row_key[c * L.R + r] = k.rows[r];
       if (row_src) row_src[c * L.R + r] = rsrc[r];
+      if (row_kernel) {
+        // the row's kernel (resolve.py:251-355: an inline func runs in its
+        // primary consumer's kernel), bit 30 = that kernel breaks a hardware
+        // limit (machine.py:91-105 validate_limits)
+        const CF<ND>& g = k.cf[k.rows[r] >> 8];
+        const int kk = g.kind == K_INLINE ? (g.consumer >= 0 ? k.cf[g.consumer].kernel : -1) : g.kernel;
+        int32_t v = kk;
+        if (kk >= 0 && (k.cf[kk].k_threads > k.P->m.max_threads_per_block ||
+                        k.cf[kk].k_shared > (int64_t)k.P->m.shared_mem_per_block_limit))
+          v |= 0x40000000;
+        row_kernel[c * L.R + r] = v;
+      }
     }
     __syncwarp();
     GS_MARK(6);
@@ -2411,7 +2423,7 @@ int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDeci
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
                      const Layout& L, int nwarps, int grid, int* gerr, int reuse, uint8_t* gscratch,
                      uint8_t* heads, int mode, const int32_t* run_id, const int32_t* run_head, int64_t nruns,
-                     uint8_t* slots, int64_t slot_bytes, cudaStream_t st) {
+                     uint8_t* slots, int64_t slot_bytes, int32_t* row_kernel, cudaStream_t st) {
   dim3 b(nwarps * 32);
   if (heads && reuse && mode == 0) {
     k1_heads_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(dec, n, S, heads);
@@ -2422,7 +2434,7 @@ int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDeci
 #define GS_CASE(D)                                                                                  \
   case D:                                                                                           \
     cudaFuncSetAttribute(featurize_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total); \
-    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, gerr, reuse, gscratch, reuse ? heads : nullptr, mode, run_id, run_head, nruns, slots, slot_bytes); \
+    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, gerr, reuse, gscratch, reuse ? heads : nullptr, mode, run_id, run_head, nruns, slots, slot_bytes, row_kernel); \
     g_launch_count++;                                                                               \
     break;
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4)

@@ -60,6 +60,20 @@ class GsTilingMenus(C.Structure):
                 ("unroll_budget", C.c_int32), ("warp_size", C.c_int32)]
 
 
+class GsOracleParams(C.Structure):
+    """Machine-oracle throughput knobs (reference machine.py:24-31)."""
+    _fields_ = [("registers_per_thread_budget", C.c_int32), ("pad", C.c_int32),
+                ("compute_throughput", C.c_double), ("global_bandwidth", C.c_double),
+                ("shared_bandwidth", C.c_double), ("kernel_launch_overhead", C.c_double)]
+
+
+def oracle_params(mp) -> GsOracleParams:
+    """Pack the oracle knobs of a MachineParams-like object."""
+    return GsOracleParams(int(mp.registers_per_thread_budget), 0, float(mp.compute_throughput),
+                          float(mp.global_bandwidth), float(mp.shared_bandwidth),
+                          float(mp.kernel_launch_overhead))
+
+
 def tiling_menus(menus) -> GsTilingMenus:
     """Pack a TilingConfig-like object (reference options.py:25-37)."""
     m = GsTilingMenus()

@@ -182,6 +182,23 @@ class Scorer:
                 out.append(self.struct_hash(dec, depth))
         return out
 
+    # -- machine oracle (K6) -------------------------------------------------
+    def simulate(self, dec: torch.Tensor, params=None):
+        """Reference `simulate_runtime` (machine.py:108-167) for a batch of
+        fully scheduled candidates: K1 features and row kernels, then K6.
+        Returns (runtime f64 [N], spill_bytes i64 [N], status u8 [N]) with
+        status 0 ok, 1 hardware-limit violation, 2 not fully scheduled (the
+        two cases the reference raises ValueError for; runtime is NaN)."""
+        from .descriptor import oracle_params
+        n, S = dec.shape[0], dec.shape[1] // 16
+        op = oracle_params(params or self.params)
+        rt = torch.empty((n,), dtype=torch.float64, device=self.device)
+        sp = torch.empty((n,), dtype=torch.int64, device=self.device)
+        st = torch.empty((n,), dtype=torch.uint8, device=self.device)
+        _lib.check(self.lib.gs_simulate(self.handle, _ptr(dec), n, S, C.byref(op), _ptr(rt), _ptr(sp), _ptr(st),
+                                        _stream()))
+        return rt, sp, st
+
     # -- beam-step expansion -------------------------------------------------
     def expand_step(self, parents: torch.Tensor, steps: torch.Tensor, menus=None, total=None):
         """Every phase-2 tiling of each parent's step root on the device

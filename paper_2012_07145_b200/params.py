@@ -32,6 +32,15 @@ class MachineParams:
     global_transaction_bytes: int = 32
     shared_banks: int = 32
     bank_width_bytes: int = 4
+    # machine-oracle throughput knobs (machine.py:26-31), not hardware limits
+    compute_throughput: float = 2.5e12
+    global_bandwidth: float = 900e9
+    shared_bandwidth: float = 9e12
+    kernel_launch_overhead: float = 5e-6
+
+    @property
+    def register_bytes_per_thread(self) -> int:
+        return self.registers_per_thread_budget * 4
 
     def override(self, **kw):
         return replace(self, **{k: v for k, v in kw.items() if v is not None})

@@ -61,7 +61,7 @@ def test_host_only_calls(lib):
 def test_struct_layout_matches_c(tmp_path):
     from paper_2012_07145_b200 import descriptor as D
     names = ["GsFunc", "GsStage", "GsAccess", "GsMachine", "GsThresholds", "GsPipelineDesc",
-             "GsTilingMenus", "GsDecision"]
+             "GsTilingMenus", "GsOracleParams", "GsDecision"]
     prog = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', 'int main(void){']
     for n in names:
         prog.append(f'printf("{n} %zu\\n", sizeof({n}));')
