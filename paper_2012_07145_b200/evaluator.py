@@ -25,9 +25,18 @@ from .params import DEFAULT_THRESHOLDS
 try:  # the reference is the user's own installation; optional here
     from gpusched.search import CostEvaluator as _Base  # type: ignore
     from gpusched.options import PruneReport as _PruneReport  # type: ignore
+    from gpusched.machine import OracleResult as _OracleResult  # type: ignore
     HAVE_REFERENCE = True
 except Exception:  # pragma: no cover - standalone use
     HAVE_REFERENCE = False
+
+    class _OracleResult:  # mirror of machine.py:71-82
+        def __init__(self, runtime, spilled_registers, spill_bytes):
+            if runtime <= 0:
+                raise ValueError("oracle runtime must be positive")
+            if (spill_bytes > 0) != spilled_registers:
+                raise ValueError("spill_bytes > 0 iff spilled_registers")
+            self.runtime, self.spilled_registers, self.spill_bytes = runtime, spilled_registers, spill_bytes
 
     class _Base:  # mirror of search.py:90-101
         def __init__(self, weights, params):
@@ -58,6 +67,27 @@ def scorer_for(graph, params, thresholds, weights) -> Scorer:
         _SCORERS[key] = sc
     sc.set_weights(weights)
     return sc
+
+
+def simulate_runtime(state, graph, params):
+    """Drop-in for the reference machine oracle `simulate_runtime`
+    (machine.py:108-167; the driver's `oracle=` hook, driver.py:120, 158,
+    183): K1 + K6 on the B200.  Returns an OracleResult and raises
+    ValueError in the two cases the reference raises for."""
+    key = (id(graph), params, "oracle")
+    sc = _SCORERS.get(key)
+    if sc is None or sc.packed.graph is not graph:
+        sc = Scorer(graph, params, DEFAULT_THRESHOLDS)
+        _SCORERS[key] = sc
+    rt, sp, st = sc.simulate(sc.upload([state]), params)
+    sc.check()
+    status = int(st[0].item())
+    if status == 2:
+        raise ValueError("oracle requires a fully scheduled state")
+    if status == 1:
+        raise ValueError("hardware limit violation")
+    spill = int(sp[0].item())
+    return _OracleResult(runtime=float(rt[0].item()), spilled_registers=spill > 0, spill_bytes=spill)
 
 
 class GpuCostEvaluator(_Base):

@@ -68,3 +68,35 @@ def test_gpu_simulate_sibling_batch(dev):
     assert torch.equal(st, st0) and torch.equal(sp, sp0)
     ok = st == 0
     assert torch.equal(rt[ok], rt0[ok]) and int(ok.sum()) > 0
+
+
+def test_simulate_runtime_drop_in(dev):
+    """`evaluator.simulate_runtime` takes the reference's own states and
+    params and returns what the reference's simulate_runtime returns."""
+    from test_gpu_search import _reference_on_path
+    if not _reference_on_path():
+        pytest.skip("reference package not installed (baseline/_ref)")
+    import importlib
+    from gpusched.loopnest import replay_schedule
+    from gpusched.machine import MachineParams, simulate_runtime as ref_sim
+    from gpusched.pipeline import parse_pipeline
+    ev_mod = importlib.import_module("paper_2012_07145_b200.evaluator")
+    if not ev_mod.HAVE_REFERENCE:
+        ev_mod = importlib.reload(ev_mod)
+    for name in ("stencil_chain", "conv"):
+        with gzip.open(os.path.join(GOLDEN, f"{name}.json.gz"), "rt") as fh:
+            m = json.load(fh)
+        graph = parse_pipeline(m["pipeline"], name)
+        params = MachineParams(registers_per_thread_budget=16)
+        for dump in m["candidates"][:12]:
+            st = replay_schedule(graph, dump)
+            try:
+                want = ref_sim(st, graph, params)
+            except ValueError:
+                with pytest.raises(ValueError):
+                    ev_mod.simulate_runtime(st, graph, params)
+                continue
+            got = ev_mod.simulate_runtime(st, graph, params)
+            assert type(got) is type(want)
+            assert (got.runtime, got.spilled_registers, got.spill_bytes) == \
+                (want.runtime, want.spilled_registers, want.spill_bytes)
