@@ -75,7 +75,7 @@ struct GsPipeline {
   int max_smem = 0;
   int rcap = 0, pcap = 0;
   int reuse = 1;
-  int nwarps = kK1MaxWarps;
+  int nwarps = getenv("GS_K1_WARPS") ? atoi(getenv("GS_K1_WARPS")) : kK1MaxWarps;   // diagnostics override
   int last_warps = 0, last_slice = 0;   // K1 launch shape (diagnostics)
   int repr_bound = 1 << 30;             // longest possible canonical repr (K3)
   uint8_t* hscratch = nullptr;   // K3 run-head flags (grow-only)
