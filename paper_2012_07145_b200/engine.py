@@ -169,11 +169,11 @@ class Scorer:
                                            _ptr(out), _stream()))
         return out
 
-    def memo_hashes(self, dec: torch.Tensor, num_passes: int):
+    def memo_hashes(self, dec: torch.Tensor, num_passes: int, h3=None):
         """Hashes at depths 1..num_passes (the bad-hash memo, search.py:196-200).
         The canonical key caps the depth at 3 (loopnest.py:137), so deeper
-        depths reuse the depth-3 hashes."""
-        out, h3 = [], None
+        depths reuse the depth-3 hashes (`h3`, when the caller has them)."""
+        out = []
         for depth in range(1, num_passes + 1):
             if depth >= 3:
                 h3 = self.struct_hash(dec, 3) if h3 is None else h3

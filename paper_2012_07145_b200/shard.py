@@ -97,7 +97,10 @@ class StepPlan:
         # bad-hash memo: hashes of the bottom half at every pass depth.  All
         # representatives are hashed and the bottom half is picked after the
         # step's one closing sync, so the host never waits mid-step here.
-        memo = sc.memo_hashes(dec.index_select(0, cand), self.num_passes) if costs.shape[0] > 1 else []
+        # at pass depth >= 3 the representatives' bucket hashes ARE their
+        # depth-3 hashes (the key caps at 3)
+        memo = sc.memo_hashes(dec.index_select(0, cand), self.num_passes,
+                              h3=ph if self.pass_index >= 3 else None) if costs.shape[0] > 1 else []
         mark()
         if times is not None:
             torch.cuda.synchronize()
