@@ -248,7 +248,15 @@ __global__ void __launch_bounds__(kHashWarps * 32) hash_warp_kernel(
   const int64_t per = (n + nwarps - 1) / nwarps;
   const int64_t c_end = (wid + 1) * per < n ? (wid + 1) * per : n;
   for (int64_t c = wid * per; c < c_end; ++c) {
-    if (head && !head[c]) continue;
+    if (head) {   // next run head at or after c, 32 flags per probe
+      int64_t nxt = c_end;
+      for (int64_t b = c; b < c_end; b += 32) {
+        const unsigned m = __ballot_sync(0xffffffffu, b + lane < c_end && head[b + lane]);
+        if (m) { nxt = b + __ffs(m) - 1; break; }
+      }
+      c = nxt;
+      if (c >= c_end) break;
+    }
     const GsDecision* d = dec + c * S;
     for (int f = lane; f < nf; f += 32) didx[f] = -1;
     __syncwarp();
