@@ -348,12 +348,25 @@ __global__ void __launch_bounds__(kHashWarps * 32) hash_warp_kernel(
     const int padded = ((len + 127) / 128) * 128;
     for (int k = len + lane; k < padded && k < kHashBuf; k += 32) buf[k] = 0;
     __syncwarp();
-    if (lane == 0) out[c] = len <= kHashBuf ? blake_buf(buf, len) : 0ull;
+    unsigned long long hv = 0;
+    if (lane == 0) hv = len <= kHashBuf ? blake_buf(buf, len) : 0ull;
+    hv = __shfl_sync(0xffffffffu, hv, 0);
+    if (lane == 0) out[c] = hv;
+    if (head) {   // the run's followers (up to the next head, past this warp's range) copy it
+      for (int64_t b = c + 1; b < n; b += 32) {
+        const bool follower = b + lane < n && !head[b + lane];
+        const unsigned m = __ballot_sync(0xffffffffu, !follower);   // first head / end of batch
+        const int stop = m ? __ffs(m) - 1 : 32;
+        if (lane < stop) out[b + lane] = hv;
+        if (m) break;
+      }
+    }
     __syncwarp();
   }
 }
 
-// non-head candidates copy the hash of the head of their run
+// non-head candidates copy the hash of the head of their run (after the
+// per-thread hash_kernel; hash_warp_kernel fills followers itself)
 __global__ void hash_fill_kernel(const uint8_t* __restrict__ head, int64_t n, uint64_t* __restrict__ out) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n || head[c]) return;
@@ -384,7 +397,7 @@ int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, cons
     hash_kernel<<<(unsigned)blocks, 128, 0, st>>>(dec, n, S, nf, depth, sorted_funcs, names, name_off, out, head);
   }
   g_launch_count++;
-  if (head) {
+  if (head && repr_bound > kHashBuf) {   // the warp kernel writes followers itself
     hash_fill_kernel<<<(unsigned)blocks, 128, 0, st>>>(head, n, out);
     g_launch_count++;
   }
