@@ -1905,29 +1905,30 @@ __device__ __forceinline__ void row_features(K1<ND>& k, WarpScr& W, int func, in
   GS_SUB(11);
   int lerr = err;
   for (int o = 16; o; o >>= 1) lerr |= __shfl_xor_sync(0xffffffffu, lerr, o);
+  double* v = W.feat;
+  const int gtx = M.global_transaction_bytes, stx = M.shared_banks * M.bank_width_bytes;
+  // lane-parallel part of the assembly: the union counts (acc[box][tier]
+  // [bytes, lines]) as features, the per-task / per-point sums over tiers
+  // (the reference sums ints: integer sums), loads and load efficiencies
+  if (lane < 12) {
+    const int b = lane / 6, t = (lane % 6) >> 1, w = lane & 1;   // box 0 realization, 1 thread
+    if (b == 1 || !inl) v[(b == 1 ? F_UG_THREAD : F_UG_REAL) + 3 * w + t] = (double)W.acc[b][t][w];
+  } else if (lane < 16) {
+    const int b = lane < 14 ? 3 : 2, w = lane & 1;                // box 3 task, 2 point
+    const int idx = lane == 12 ? F_UB_TASK : lane == 13 ? F_UL_TASK : lane == 14 ? F_UB_POINT : F_UL_POINT;
+    v[idx] = (double)(W.acc[b][0][w] + W.acc[b][1][w] + W.acc[b][2][w]);
+  } else if (lane < 18) {
+    const int t = lane - 16;                                       // 0 global, 1 shared
+    const double loads = (double)ld[t];
+    v[t == 0 ? F_GL_LOADS : F_SH_LOADS] = loads;
+    if (loads > 0) {
+      const double e = (double)W.acc[3][t][0] / (loads * (t == 0 ? gtx : stx));
+      v[t == 0 ? F_GL_LD_EFF : F_SH_LD_EFF] = e < 1.0 ? e : 1.0;
+    }
+  }
+  __syncwarp();
   if (lane == 0) {
     if (lerr) atomicOr(k.gerr, lerr);
-    double* v = W.feat;
-    const int gtx = M.global_transaction_bytes, stx = M.shared_banks * M.bank_width_bytes;
-    auto A_ = [&](int b, int t, int w) { return (double)W.acc[b][t][w]; };
-    for (int t = 0; t < 3; ++t) {
-      v[F_UG_THREAD + t] = A_(1, t, 0);
-      v[F_UG_THREAD + 3 + t] = A_(1, t, 1);
-    }
-    v[F_GL_LOADS] = (double)ld[0];
-    v[F_SH_LOADS] = (double)ld[1];
-    const double used_g = A_(3, 0, 0), used_s = A_(3, 1, 0);
-    if (v[F_GL_LOADS] > 0) { double e = used_g / (v[F_GL_LOADS] * gtx); v[F_GL_LD_EFF] = e < 1.0 ? e : 1.0; }
-    if (v[F_SH_LOADS] > 0) { double e = used_s / (v[F_SH_LOADS] * stx); v[F_SH_LD_EFF] = e < 1.0 ? e : 1.0; }
-    v[F_UB_TASK] = A_(3, 0, 0) + A_(3, 1, 0) + A_(3, 2, 0);
-    v[F_UL_TASK] = A_(3, 0, 1) + A_(3, 1, 1) + A_(3, 2, 1);
-    v[F_UB_POINT] = A_(2, 0, 0) + A_(2, 1, 0) + A_(2, 2, 0);
-    v[F_UL_POINT] = A_(2, 0, 1) + A_(2, 1, 1) + A_(2, 2, 1);
-    // the reference sums ints, so do the sums in integers
-    v[F_UB_TASK] = (double)(W.acc[3][0][0] + W.acc[3][1][0] + W.acc[3][2][0]);
-    v[F_UL_TASK] = (double)(W.acc[3][0][1] + W.acc[3][1][1] + W.acc[3][2][1]);
-    v[F_UB_POINT] = (double)(W.acc[2][0][0] + W.acc[2][1][0] + W.acc[2][2][0]);
-    v[F_UL_POINT] = (double)(W.acc[2][0][1] + W.acc[2][1][1] + W.acc[2][2][1]);
     if (inl) {
       v[F_INLINED] = (double)g.calls;
       v[F_NUM_SCALARS] = (double)g.calls;
@@ -1938,10 +1939,6 @@ __device__ __forceinline__ void row_features(K1<ND>& k, WarpScr& W, int func, in
       v[F_NUM_SCALARS] = (double)(ppb * kern.n_blocks);
       v[F_PTS_PER_THREAD] = (double)ppt;
       v[F_NUM_REAL] = v[F_NUM_PROD] = (double)g.realizations;
-      for (int t = 0; t < 3; ++t) {
-        v[F_UG_REAL + t] = A_(0, t, 0);
-        v[F_UG_REAL + 3 + t] = A_(0, t, 1);
-      }
       int64_t alloc[3] = {0, 0, 0};
       for (int gi = 0; gi < ng; ++gi)
         alloc[W.gtier[gi]] += alloc_of(k.cf[W.gprod[gi]]) * k.F[W.gprod[gi]].elem_bytes;
