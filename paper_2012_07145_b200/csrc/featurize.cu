@@ -1736,30 +1736,41 @@ __device__ __forceinline__ void parallel_feats(double* v, const GsMachine& M, in
   if (act < 1) act = 1;
   int64_t awsm = (int64_t)act * wpb;
   if (awsm > M.max_active_warps_per_sm) awsm = M.max_active_warps_per_sm;
-  int idx = -1;
+  // operands selected per lane without branching (a switch on the lane
+  // would serialise fifteen divergent paths)
+  const bool shp = kern.k_shared > 0;
+  const double nb = (double)kern.n_blocks, nn = (double)n, mt = (double)M.max_threads_per_block;
   double num = 0.0, den = 1.0;
-  bool clamp = false;
-  switch (lane) {
-    case 0: idx = F_NUM_BLOCKS; num = (double)kern.n_blocks; break;
-    case 1: idx = F_WARPS_PB; num = (double)((kt + ws - 1) / ws); break;
-    case 2: idx = F_ACTIVE_WARPS; num = (double)aw; break;
-    case 3: idx = F_THREADS_PB; num = (double)n; break;
-    case 4: idx = F_WARP_UTIL; num = (double)n; den = (double)(ws * aw); break;
-    case 5: idx = F_IDLE; num = (double)(ws * aw - n); den = (double)M.max_threads_per_block; break;
-    case 6: idx = F_BLOCK_OCC; num = (double)kt; den = (double)M.max_threads_per_block; break;
-    case 7:
-      idx = F_SH_OCC;
-      if (kern.k_shared > 0) { num = (double)kern.k_shared; den = (double)M.shared_mem_per_block_limit; clamp = true; }
-      break;
-    case 8: idx = F_SH_LIMIT; num = (double)(by_shared < mb ? by_shared : mb); den = (double)mb; break;
-    case 9: idx = F_MAX_WARP_OCC; num = (double)awsm; den = (double)M.max_active_warps_per_sm; break;
-    case 10: idx = F_MAX_BLOCK_OCC; num = (double)act; den = (double)mb; break;
-    case 11: idx = F_NUM_TASKS; num = (double)kern.n_blocks; break;
-    case 12: idx = F_INNER_PAR; num = (double)n; break;
-    case 13: idx = F_NUM_CORES; num = (double)M.num_sms; break;
-    case 14: idx = F_TASKS_PER_CORE; num = (double)kern.n_blocks; den = (double)M.num_sms; break;
-    default: break;
-  }
+  num = lane == 0 || lane == 11 || lane == 14 ? nb : num;
+  num = lane == 1 ? (double)((kt + ws - 1) / ws) : num;
+  num = lane == 2 ? (double)aw : num;
+  num = lane == 3 || lane == 4 || lane == 12 ? nn : num;
+  num = lane == 5 ? (double)(ws * aw - n) : num;
+  num = lane == 6 ? (double)kt : num;
+  num = lane == 7 && shp ? (double)kern.k_shared : num;
+  num = lane == 8 ? (double)(by_shared < mb ? by_shared : mb) : num;
+  num = lane == 9 ? (double)awsm : num;
+  num = lane == 10 ? (double)act : num;
+  num = lane == 13 ? (double)M.num_sms : num;
+  den = lane == 4 ? (double)(ws * aw) : den;
+  den = lane == 5 || lane == 6 ? mt : den;
+  den = lane == 7 && shp ? (double)M.shared_mem_per_block_limit : den;
+  den = lane == 8 || lane == 10 ? (double)mb : den;
+  den = lane == 9 ? (double)M.max_active_warps_per_sm : den;
+  den = lane == 14 ? (double)M.num_sms : den;
+  const bool clamp = lane == 7 && shp;
+  // feature index of lane i: 6-bit fields of two constants (no local array)
+  constexpr unsigned long long kIdxLo =
+      (unsigned long long)F_NUM_BLOCKS | (unsigned long long)F_WARPS_PB << 6 |
+      (unsigned long long)F_ACTIVE_WARPS << 12 | (unsigned long long)F_THREADS_PB << 18 |
+      (unsigned long long)F_WARP_UTIL << 24 | (unsigned long long)F_IDLE << 30 |
+      (unsigned long long)F_BLOCK_OCC << 36 | (unsigned long long)F_SH_OCC << 42 |
+      (unsigned long long)F_SH_LIMIT << 48 | (unsigned long long)F_MAX_WARP_OCC << 54;
+  constexpr unsigned long long kIdxHi =
+      (unsigned long long)F_MAX_BLOCK_OCC | (unsigned long long)F_NUM_TASKS << 6 |
+      (unsigned long long)F_INNER_PAR << 12 | (unsigned long long)F_NUM_CORES << 18 |
+      (unsigned long long)F_TASKS_PER_CORE << 24;
+  const int idx = lane < 10 ? (int)((kIdxLo >> (6 * lane)) & 63) : lane < 15 ? (int)((kIdxHi >> (6 * (lane - 10))) & 63) : -1;
   double q = num / den;
   if (clamp && !(q < 1.0)) q = 1.0;
   if (idx >= 0) v[idx] = q;
