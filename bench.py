@@ -251,6 +251,52 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def bench_parity(sc, plan, dec, timed_out):
+    """Check the bench's own step against the reference fixture of this exact
+    step (tests/golden/c5_step.*, written by the unmodified reference via
+    tests/golden/make_c5_golden.py): the beam the timed region cut, and an
+    untimed re-run with rejects for representatives, rejects, representative
+    costs, the memo, and 1,024 strided candidates' totals and verdicts."""
+    import gzip
+    import torch
+    gold = os.path.join(ROOT, "tests", "golden")
+    try:
+        with gzip.open(os.path.join(gold, "c5_step.json.gz"), "rt") as fh:
+            meta = json.load(fh)
+        arr = np.load(os.path.join(gold, "c5_step.npz"))
+    except OSError:
+        return {"checked": False, "why": "fixture missing"}
+    if meta["n_candidates"] != dec.shape[0]:
+        return {"checked": False, "why": "not the fixture's step size"}
+    from paper_2012_07145_b200.descriptor import PRUNE_REASONS
+    v = meta["cut"]["variants"]["bench"]
+    out = plan.run(dec, rejects=True)
+    sc.check()
+    reps = out["reps"].cpu().numpy()
+    rep_cost = out["total"].index_select(0, out["reps"]).cpu().numpy()
+    idx = torch.as_tensor(arr["sample_index"], device=sc.device)
+    tot = out["total"].index_select(0, idx).cpu().numpy()
+    ver = out["verdict"].index_select(0, idx).cpu().numpy()
+    memo = {(dd, int(x)) for dd, hs in enumerate(out["memo"], start=1) for x in hs.cpu().numpy().view(np.uint64)}
+    want_memo = {(int(dd), int(h)) for dd, h in v["memo_after"]}
+    rel = lambda a, b: float(np.max(np.abs(a - b) / np.abs(b))) if len(b) else 0.0  # noqa: E731
+    res = {"checked": True, "fixture": "tests/golden/c5_step (unmodified reference _cut over this step)",
+           "timed_beam_exact": timed_out["beam"] == v["beam"],
+           "beam_exact": out["beam"] == v["beam"],
+           "reps_exact": bool(np.array_equal(reps, arr["rep_idx"])),
+           "rejects_exact": [i for i, _ in out["rejects"]] == arr["rej_idx"].tolist()
+           and [r for _, r in out["rejects"]] == meta["cut"]["reject_reasons"],
+           "memo_exact": memo == want_memo,
+           "rep_cost_max_rel_err": rel(rep_cost, arr["rep_cost"]),
+           "sample_n": int(len(idx)),
+           "sample_total_max_rel_err": rel(tot, arr["total"]),
+           "sample_verdicts_exact": [PRUNE_REASONS[c - 1] if c else None for c in ver] == meta["prune"]}
+    res["ok"] = bool(res["timed_beam_exact"] and res["beam_exact"] and res["reps_exact"] and res["rejects_exact"]
+                     and res["memo_exact"] and res["sample_verdicts_exact"] and res["rep_cost_max_rel_err"] <= 1e-9
+                     and res["sample_total_max_rel_err"] <= 1e-9)
+    return res
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -341,6 +387,7 @@ def run_gpu(args):
         e = float(t.item())
     sc.check()
 
+    parity = bench_parity(sc, plan, dec, res) if world == 1 else {"checked": False, "why": "N > 1"}
     if rank == 0:
         R = sc.R
         n_local = plan.local_count
@@ -395,6 +442,7 @@ def run_gpu(args):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "beam": res["beam"][:8],
+            "parity": parity,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -12,15 +12,16 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
                      const Layout& L, int nwarps, int grid, int* gerr, int reuse, uint8_t* gscratch,
-                     uint8_t* heads, int mode, const int32_t* run_id, const int32_t* run_head, int64_t nruns,
-                     uint8_t* slots, int64_t slot_bytes, int32_t* row_kernel, cudaStream_t st);
+                     uint8_t* heads, int mode, const int32_t* run_id, const int32_t* run_head,
+                     const uint32_t* nruns, int64_t max_runs, uint8_t* slots, int64_t slot_bytes,
+                     int32_t* row_kernel, cudaStream_t st);
 int launch_simulate(const GsFunc* funcs, int nf, const GsDecision* dec, int64_t n, int S, const double* feats,
                     const int32_t* row_key, const int32_t* n_rows, const int32_t* row_kernel, int R,
                     const int32_t* stage_of_func, const double* algo, const GsMachine& m, const GsOracleParams& op,
                     double* runtime, int64_t* spill_bytes, uint8_t* status, cudaStream_t st);
-int64_t k1_prepare_runs(const GsDecision* dec, int64_t n, int S, uint8_t* heads, int32_t* run_id,
-                        int32_t* run_head, void* tmp, size_t tmp_bytes, cudaStream_t st);
-size_t k1_runs_tmp_bytes(int64_t n);
+void k1_prepare_runs(const GsDecision* dec, int64_t n, int S, uint8_t* heads, int32_t* run_id, int32_t* run_head,
+                     uint32_t* sums, uint32_t* nruns, cudaStream_t st);
+size_t k1_runs_sums_bytes(int64_t n);
 int featurize_warps(const Layout& L1, int max_smem);
 int read_phases(long long* out);
 int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st);
@@ -78,16 +79,13 @@ struct GsPipeline {
   int nwarps = getenv("GS_K1_WARPS") ? atoi(getenv("GS_K1_WARPS")) : kK1MaxWarps;   // diagnostics override
   int last_warps = 0, last_slice = 0;   // K1 launch shape (diagnostics)
   int repr_bound = 1 << 30;             // longest possible canonical repr (K3)
-  uint8_t* hscratch = nullptr;   // K3 run-head flags (grow-only)
-  uint8_t* gscratch = nullptr;   // K1 spilled structure arrays (grow-only)
-  uint8_t* k1heads = nullptr;    // K1 run-head flags (grow-only)
-  int64_t k1cap = 0;
-  uint8_t* runbuf = nullptr;     // K1 two-phase: run ids, run heads, scan scratch (grow-only)
-  int64_t runcap = 0;
-  uint8_t* slots = nullptr;      // K1 two-phase: per-run warp state (grow-only)
-  int64_t slotcap = 0;
-  int64_t gcap = 0;
+  // Library-owned workspaces of the convenience entry points (gs_featurize,
+  // gs_struct_hash, gs_simulate), grown once per size class; the *_ws entry
+  // points take the caller's workspace instead and never allocate.
+  uint8_t* hscratch = nullptr;   // K3 run-head flags
   int64_t hcap = 0;
+  uint8_t* k1ws = nullptr;       // K1 workspace (see K1Ws)
+  int64_t k1cap = 0;
   uint8_t* simbuf = nullptr;     // K6: features, row keys / kernels, n_rows, verdicts (grow-only)
   int64_t simcap = 0;
 };
@@ -210,7 +208,7 @@ int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
 int gs_pipeline_destroy(gs_pipeline_t p) {
   if (!p) return GS_OK;
   cudaFree(p->dev); cudaFree(p->blob); cudaFree(p->stage_of_func); cudaFree(p->algo); cudaFree(p->sorted);
-  cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err); cudaFree(p->hscratch); cudaFree(p->gscratch); cudaFree(p->k1heads); cudaFree(p->runbuf); cudaFree(p->slots); cudaFree(p->simbuf);
+  cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err); cudaFree(p->hscratch); cudaFree(p->k1ws); cudaFree(p->simbuf);
   for (double* b : p->wbufs) cudaFree(b);
   delete p;
   return GS_OK;
@@ -256,14 +254,34 @@ int gs_set_reuse(gs_pipeline_t p, int enable) {
 
 }  // extern "C"
 
-// K1 with an explicit reuse mode and the optional per-row kernel output
-static int featurize_impl(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, double* feats,
-                          int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
-                          int32_t* row_kernel, int reuse, void* stream) {
-  if (n == 0) return GS_OK;
-  // one CTA per SM, as many independent scorer warps as shared memory
-  // holds; pipelines whose worst-case inline expansion would leave fewer
-  // than 4 warps keep the capacity-sized arrays in global scratch instead
+// K1 launch shape and workspace.  One CTA per SM, as many independent
+// scorer warps as shared memory holds; pipelines whose worst-case inline
+// expansion would leave fewer than 4 warps keep the capacity-sized arrays
+// in global scratch (`gscratch`) instead.  Batches of >= 8192 candidates
+// with features may use the two-phase schedule: run ids / heads / count
+// (device) and one saved warp state per run (`slots`, `max_runs` of them;
+// the kernel falls back to the one-phase schedule when the batch has more
+// runs, or runs shorter than 8 on average).
+struct K1Plan {
+  Layout L;
+  int nwarps = 0;
+  int64_t grid = 0;
+  bool two_phase = false;
+  int64_t slot_bytes = 0;
+};
+
+struct K1Ws {
+  uint8_t* gscratch = nullptr;
+  uint8_t* heads = nullptr;
+  int32_t* run_id = nullptr;
+  int32_t* run_head = nullptr;
+  uint32_t* sums = nullptr;
+  uint32_t* nruns = nullptr;
+  uint8_t* slots = nullptr;
+  int64_t max_runs = 0;
+};
+
+static int k1_plan(gs_pipeline_t p, int64_t n, int S, bool feats, int reuse, K1Plan& kp) {
   bool spill = false;
   int nwarps = std::min(p->nwarps, featurize_warps(layout_for(p, S, 1, false), p->max_smem));
   if (nwarps < 4) {
@@ -274,78 +292,86 @@ static int featurize_impl(gs_pipeline_t p, const GsDecision* dec, int64_t n, int
     return fail(GS_ERR_CAPACITY, "pipeline too large for one warp's shared-memory slice (" +
                                      std::to_string(layout_for(p, S, 1, true).total) + " > " +
                                      std::to_string(p->max_smem) + " bytes)");
-  Layout L = layout_for(p, S, nwarps, spill);
-  int64_t grid = std::min<int64_t>(p->num_sms, (n + nwarps - 1) / nwarps);
-  {
-    const int64_t need = grid * nwarps * (int64_t)L.gl_bytes;
-    if (need > p->gcap) {   // grow-only global scratch
-      CK(cudaStreamSynchronize((cudaStream_t)stream));
-      if (p->gscratch) CK(cudaFree(p->gscratch));
-      p->gscratch = nullptr;
-      p->gcap = 0;
-      CK(cudaMalloc(&p->gscratch, (size_t)need));
-      p->gcap = need;
-    }
+  kp.L = layout_for(p, S, nwarps, spill);
+  kp.nwarps = nwarps;
+  kp.grid = std::max<int64_t>(1, std::min<int64_t>(p->num_sms, (n + nwarps - 1) / nwarps));
+  kp.two_phase = reuse && feats && n >= 8192;
+  kp.slot_bytes = (int64_t)kp.L.warp_bytes + kp.L.gl_bytes;
+  return GS_OK;
+}
+
+static int64_t k1_default_runs(const K1Plan& kp, int64_t n) {
+  return std::max<int64_t>(1, std::min<int64_t>(n / 8, ((int64_t)1 << 30) / std::max<int64_t>(1, kp.slot_bytes)));
+}
+
+// carve (base may be null: size only)
+static int64_t k1_carve(const K1Plan& kp, int64_t n, int64_t max_runs, uint8_t* base, K1Ws& w) {
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) { uint8_t* r = base ? base + o : nullptr; o += (bytes + 255) & ~(int64_t)255; return r; };
+  w.gscratch = take(kp.grid * kp.nwarps * (int64_t)kp.L.gl_bytes);
+  w.heads = take(std::max<int64_t>(1, n));
+  w.max_runs = 0;
+  if (kp.two_phase) {
+    w.run_id = reinterpret_cast<int32_t*>(take(4 * n));
+    w.run_head = reinterpret_cast<int32_t*>(take(4 * n));
+    w.sums = reinterpret_cast<uint32_t*>(take((int64_t)k1_runs_sums_bytes(n)));
+    w.nruns = reinterpret_cast<uint32_t*>(take(16));
+    w.max_runs = max_runs;
+    w.slots = take(max_runs * kp.slot_bytes);
   }
-  if (n > p->k1cap) {   // grow-only run-head flags for the K1 work units
-    CK(cudaStreamSynchronize((cudaStream_t)stream));
-    if (p->k1heads) CK(cudaFree(p->k1heads));
-    p->k1heads = nullptr;
-    p->k1cap = 0;
-    CK(cudaMalloc(&p->k1heads, (size_t)n));
-    p->k1cap = n;
-  }
-  p->last_warps = nwarps;
-  p->last_slice = L.warp_bytes;
+  return o;
+}
+
+// K1 with an explicit reuse mode, workspace and the optional per-row kernel output
+static int featurize_impl(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, double* feats,
+                          int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
+                          int32_t* row_kernel, int reuse, const K1Plan& kp, const K1Ws& w, void* stream) {
+  if (n == 0) return GS_OK;
+  p->last_warps = kp.nwarps;
+  p->last_slice = kp.L.warp_bytes;
   cudaStream_t st = (cudaStream_t)stream;
-  // Two-phase schedule for large batches of long sibling runs: run heads
-  // first (each saves its warp state), then the siblings in small slices
-  // that resume from their head's state, so runs split across warps without
-  // re-resolving.  Needs one host sync to size the per-run state.
   int rc = 0;
-  bool two_phase = false;
-  if (reuse && feats && n >= 8192) {
-    const size_t tmpb = (k1_runs_tmp_bytes(n) + 255) & ~(size_t)255;
-    const int64_t need = (int64_t)tmpb + 8 * n + 256;
-    if (need > p->runcap) {
-      CK(cudaStreamSynchronize(st));
-      if (p->runbuf) CK(cudaFree(p->runbuf));
-      p->runbuf = nullptr;
-      p->runcap = 0;
-      CK(cudaMalloc(&p->runbuf, (size_t)need));
-      p->runcap = need;
-    }
-    int32_t* run_id = reinterpret_cast<int32_t*>(p->runbuf + tmpb);
-    int32_t* run_head = run_id + n;
-    const int64_t nruns = k1_prepare_runs(dec, n, S, p->k1heads, run_id, run_head, p->runbuf, tmpb, st);
-    if (nruns < 0) return fail(GS_ERR_CUDA, "run preparation failed");
-    const int64_t slot_bytes = (int64_t)L.warp_bytes + L.gl_bytes;
-    if (nruns * 8 <= n && nruns * slot_bytes <= (int64_t)4 << 30) {
-      two_phase = true;
-      if (nruns * slot_bytes > p->slotcap) {
-        CK(cudaStreamSynchronize(st));
-        if (p->slots) CK(cudaFree(p->slots));
-        p->slots = nullptr;
-        p->slotcap = 0;
-        CK(cudaMalloc(&p->slots, (size_t)(nruns * slot_bytes)));
-        p->slotcap = nruns * slot_bytes;
-      }
-      rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L,
-                            nwarps, (int)grid, p->err, reuse, p->gscratch, p->k1heads, 1, run_id, run_head, nruns,
-                            p->slots, slot_bytes, row_kernel, st);
-      if (!rc)
-        rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L,
-                              nwarps, (int)grid, p->err, reuse, p->gscratch, p->k1heads, 2, run_id, run_head,
-                              nruns, p->slots, slot_bytes, row_kernel, st);
-    }
+  if (kp.two_phase) {
+    // run heads first (each saves its warp state), then the siblings in
+    // small slices that resume from their head's state, so runs split
+    // across warps without re-resolving
+    k1_prepare_runs(dec, n, S, w.heads, w.run_id, w.run_head, w.sums, w.nruns, st);
+    for (int mode = 1; mode <= 2 && !rc; ++mode)
+      rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, kp.L,
+                            kp.nwarps, (int)kp.grid, p->err, reuse, w.gscratch, w.heads, mode, w.run_id, w.run_head,
+                            w.nruns, w.max_runs, w.slots, kp.slot_bytes, row_kernel, st);
+  } else {
+    rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, kp.L,
+                          kp.nwarps, (int)kp.grid, p->err, reuse, w.gscratch, w.heads, 0, nullptr, nullptr, nullptr,
+                          0, nullptr, 0, row_kernel, st);
   }
-  if (!two_phase)
-    rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L,
-                          nwarps, (int)grid, p->err, reuse, p->gscratch, p->k1heads, 0, nullptr, nullptr, 0,
-                          nullptr, 0, row_kernel, st);
   if (rc) return fail(GS_ERR_ARG, "unsupported ndim");
   CK(cudaGetLastError());
   return GS_OK;
+}
+
+// the convenience path: the library-owned K1 workspace, grown once per size
+// class (synchronizing `stream` then)
+static int featurize_owned(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, double* feats,
+                           int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
+                           int32_t* row_kernel, int reuse, void* stream) {
+  if (n == 0) return GS_OK;
+  K1Plan kp;
+  int rc = k1_plan(p, n, S, feats != nullptr, reuse, kp);
+  if (rc) return rc;
+  K1Ws w;
+  const int64_t runs = k1_default_runs(kp, n);
+  const int64_t need = k1_carve(kp, n, runs, nullptr, w);
+  if (need > p->k1cap) {
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    if (p->k1ws) CK(cudaFree(p->k1ws));
+    p->k1ws = nullptr;
+    p->k1cap = 0;
+    CK(cudaMalloc(&p->k1ws, (size_t)need));
+    p->k1cap = need;
+  }
+  k1_carve(kp, n, runs, p->k1ws, w);
+  return featurize_impl(p, dec, n, S, feats, row_key, n_rows, verdict, row_src, row_kernel, reuse, kp, w, stream);
 }
 
 extern "C" {
@@ -354,7 +380,32 @@ int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, doubl
                  int32_t* n_rows, uint8_t* verdict, int32_t* row_src, void* stream) {
   if (!p || S < 1 || n < 0) return fail(GS_ERR_ARG, "bad featurize arguments");
   if (p->reuse == 2 && feats && !row_src) return fail(GS_ERR_ARG, "reuse mode 2 (computed rows only) needs row_src");
-  return featurize_impl(p, dec, n, S, feats, row_key, n_rows, verdict, row_src, nullptr, p->reuse, stream);
+  return featurize_owned(p, dec, n, S, feats, row_key, n_rows, verdict, row_src, nullptr, p->reuse, stream);
+}
+
+int64_t gs_featurize_workspace_bytes(gs_pipeline_t p, int64_t n, int s, int64_t max_runs) {
+  if (!p || s < 1 || n < 0) return -1;
+  K1Plan kp;
+  if (k1_plan(p, std::max<int64_t>(n, 1), s, true, p->reuse, kp)) return -1;
+  K1Ws w;
+  return k1_carve(kp, n, max_runs > 0 ? max_runs : k1_default_runs(kp, n), nullptr, w);
+}
+
+int gs_featurize_ws(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, double* feats, int32_t* row_key,
+                    int32_t* n_rows, uint8_t* verdict, int32_t* row_src, int64_t max_runs, void* workspace,
+                    int64_t ws_bytes, void* stream) {
+  if (!p || S < 1 || n < 0) return fail(GS_ERR_ARG, "bad featurize arguments");
+  if (p->reuse == 2 && feats && !row_src) return fail(GS_ERR_ARG, "reuse mode 2 (computed rows only) needs row_src");
+  if (n == 0) return GS_OK;
+  K1Plan kp;
+  int rc = k1_plan(p, n, S, feats != nullptr, p->reuse, kp);
+  if (rc) return rc;
+  K1Ws w;
+  const int64_t runs = max_runs > 0 ? max_runs : k1_default_runs(kp, n);
+  if (k1_carve(kp, n, runs, nullptr, w) > ws_bytes || (!workspace && ws_bytes > 0))
+    return fail(GS_ERR_ARG, "featurize workspace too small (gs_featurize_workspace_bytes)");
+  k1_carve(kp, n, runs, static_cast<uint8_t*>(workspace), w);
+  return featurize_impl(p, dec, n, S, feats, row_key, n_rows, verdict, row_src, nullptr, p->reuse, kp, w, stream);
 }
 
 int gs_simulate(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, const GsOracleParams* op,
@@ -380,8 +431,8 @@ int gs_simulate(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, const 
   int32_t* row_kernel = reinterpret_cast<int32_t*>(p->simbuf + fb + kb);
   int32_t* n_rows = reinterpret_cast<int32_t*>(p->simbuf + fb + 2 * kb);
   uint8_t* verdict = p->simbuf + fb + 2 * kb + ((n * 4 + 255) / 256) * 256;
-  int rc = featurize_impl(p, dec, n, S, feats, row_key, n_rows, verdict, nullptr, row_kernel, p->reuse ? 1 : 0,
-                          stream);
+  int rc = featurize_owned(p, dec, n, S, feats, row_key, n_rows, verdict, nullptr, row_kernel, p->reuse ? 1 : 0,
+                           stream);
   if (rc) return rc;
   launch_simulate(reinterpret_cast<const GsFunc*>(p->blob), p->host.nf, dec, n, S, feats, row_key, n_rows,
                   row_kernel, R, p->stage_of_func, p->algo, p->host.m, *op, runtime, spill_bytes, status, st);
@@ -408,6 +459,20 @@ int gs_cost(gs_pipeline_t p, const double* feats, const int32_t* row_key, const 
                        total, row_cost, basis_gh, reinterpret_cast<unsigned*>(p->err + 15), p->num_sms,
                        (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "unsupported network dims");
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
+int64_t gs_struct_hash_workspace_bytes(int64_t n) { return (std::max<int64_t>(1, n) + 255) & ~(int64_t)255; }
+
+int gs_struct_hash_ws(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, int depth, uint64_t* out,
+                      void* workspace, int64_t ws_bytes, void* stream) {
+  if (!p || depth < 0) return fail(GS_ERR_ARG, "depth must be >= 0");
+  if (ws_bytes < gs_struct_hash_workspace_bytes(n) || !workspace)
+    return fail(GS_ERR_ARG, "hash workspace too small (gs_struct_hash_workspace_bytes)");
+  int rc = launch_hash(dec, n, S, p->host.nf, depth, p->sorted, p->names, p->name_off, out,
+                       static_cast<uint8_t*>(workspace), p->repr_bound, p->num_sms, (cudaStream_t)stream);
+  if (rc) return fail(GS_ERR_ARG, "too many funcs for the hash kernel");
   CK(cudaGetLastError());
   return GS_OK;
 }
@@ -490,7 +555,7 @@ int gs_beam_topk(const double* costs, const uint64_t* pass_hash, int64_t n, cons
                  int64_t ws_bytes, int64_t* out_pos, int64_t* n_out, uint8_t* bottom, void* stream) {
   int rc = beam_topk(costs, pass_hash, n, flagged, n_flagged, penalty, temperature, phase_seed, k, tie_band, ws, ws_bytes,
                      out_pos, n_out, bottom, (cudaStream_t)stream);
-  if (rc) return fail(GS_ERR_ARG, "beam_topk: workspace too small or k > 2048");
+  if (rc) return fail(GS_ERR_ARG, "beam_topk: workspace too small, k out of 1..16384 or negative tie band");
   CK(cudaGetLastError());
   return GS_OK;
 }

@@ -17,11 +17,13 @@ from .descriptor import DECISION_DTYPE, PackedPipeline
 from .params import DEFAULT_THRESHOLDS, MachineParams
 
 NF = 56
-# Relative distance under which two cut keys count as tied and keep
-# representative order (see csrc/select.cu band_flags).  Our fp64 totals sit
-# within ~1e-15 of the reference's; its ties between permuted per-stage cost
-# multisets are rounding coincidences we cannot reproduce bit for bit.
-TIE_BAND = 1e-12
+# Relative gap under which adjacent cut keys fall into one band group and
+# keep representative order (see csrc/select.cu cut_kernel).  Our fp64 totals
+# sit within a few ulp (~1e-15 relative) of the reference's; its exact ties
+# between permuted per-stage cost multisets are rounding coincidences we
+# cannot reproduce bit for bit, so two keys the reference ties may differ by
+# up to twice that here.  The band is a small multiple of it.
+TIE_BAND = 1e-14
 
 
 def _ptr(t):
@@ -69,10 +71,19 @@ class Scorer:
 
     # -- weights --------------------------------------------------------------
     def set_weights(self, weights):
-        key = id(weights)
+        """Upload the cost-model weights when their CONTENT changed (the
+        reference evaluator reads `.weights` on every call, search.py:117,
+        so in-place updates must be seen too; a 66 KB digest per call)."""
+        t = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in weights.tensors.items()}
+        import hashlib
+        hsh = hashlib.blake2b(digest_size=16)
+        for name in sorted(t):
+            hsh.update(name.encode())
+            hsh.update(str(t[name].shape).encode())
+            hsh.update(t[name].tobytes())
+        key = hsh.digest()
         if key == self._weights_key:
             return
-        t = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in weights.tensors.items()}
         E, H = t["algo_b"].shape[0], t["head_b"].shape[0]
         arrs = [t[n] for n in ("algo_w", "algo_b", "sched_w", "sched_b", "head_w", "head_b",
                                "out_w", "out_b")]
@@ -241,6 +252,9 @@ class Scorer:
     # -- K5 -------------------------------------------------------------------
     def beam_topk(self, costs, pass_hash, flagged, penalty, temperature, phase_seed, k,
                   bottom=True, tie_band=TIE_BAND):
+        """K5 (search.py:76-87, 168-201).  Returns (positions [k] in cut
+        order, count (device int64; negative if a tie group was wider than
+        the cut window), bottom-half flags u8 [n] or None)."""
         n = costs.shape[0]
         wsb = self.lib.gs_topk_workspace_bytes(n)
         ws = torch.empty((wsb,), dtype=torch.uint8, device=self.device)

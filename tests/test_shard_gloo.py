@@ -1,8 +1,11 @@
-"""Multi-rank sharding of one beam step, on CPU with the gloo backend
+"""Multi-rank sharding of one phase cut, on CPU with the gloo backend
 (world_size 2 and 4): buckets are owned by `hash % world`, every rank draws
-its own buckets' representatives, and `shard.exchange_reps` must rebuild
-exactly the single-process representative order of the reference
-(search.py:151-164) — hence the identical beam cut on every rank."""
+its own buckets' representatives, and `exchange.sharded_cut` — a
+fixed-size all-gather of each rank's top window plus a distributed radix
+select for the memo threshold — must give every rank exactly the beam and
+bottom half of the single-process reference cut (oracle `structure.cut`,
+search.py:168-201), including exact cost ties across ranks, the bad-hash
+penalty, and the fall-back path when a tie group outgrows a window."""
 
 import os
 import socket
@@ -23,7 +26,7 @@ def _free_port():
     return p
 
 
-def _workload(seed=7, n=3000, n_buckets=97):
+def _workload(seed, n=3000, n_buckets=97, ties=False):
     rng = np.random.default_rng(seed)
     pool = rng.integers(0, 2**63, size=n_buckets, dtype=np.int64).astype(np.uint64) * np.uint64(2) \
         + rng.integers(0, 2, size=n_buckets).astype(np.uint64)
@@ -31,19 +34,37 @@ def _workload(seed=7, n=3000, n_buckets=97):
     valid = rng.random(n) < 0.7
     costs = rng.random(n) * 100 + 1
     costs[::17] = costs[3]            # exact ties across buckets
-    return hashes, valid, costs
+    if ties:                          # a tie group far wider than any window
+        costs[np.arange(n) % 4 != 0] = 7.0
+    flagged = {int(h) for h in pool[::4]}
+    return hashes, valid, costs, flagged
 
 
-def _rank_main(rank, world, port, q):
+class _CpuCut:
+    """Stands in for the Scorer in the fall-back path: the oracle cut."""
+
+    def beam_topk(self, costs, ph, flagged, penalty, temperature, phase_seed, k, tie_band):
+        from oracle import structure
+        fl = set() if flagged is None else {int(x) & 0xFFFFFFFFFFFFFFFF for x in flagged.tolist()}
+        hs = [int(x) & 0xFFFFFFFFFFFFFFFF for x in ph.tolist()]
+        kept, bottom = structure.cut(list(range(len(hs))), costs.tolist(), hs, fl, penalty, k,
+                                     temperature, phase_seed)
+        bot = torch.zeros(len(hs), dtype=torch.uint8)
+        bot[bottom] = 1
+        return torch.tensor(kept, dtype=torch.int64), torch.tensor(len(kept)), bot
+
+
+def _rank_main(rank, world, port, seed, ties, q):
     import sys
     root = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
     sys.path.insert(0, root)
     from oracle import structure
-    from paper_2012_07145_b200.shard import exchange_reps
+    from paper_2012_07145_b200 import exchange
+    from paper_2012_07145_b200.shard import flagged_tensor
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        hashes, valid, costs = _workload()
+        hashes, valid, costs, flagged = _workload(seed, ties=ties)
         phase_seed = 3 * 101 + 11
         h_i64 = torch.from_numpy(hashes.view(np.int64).copy())
         mine = torch.nonzero(torch.remainder(h_i64, world) == rank).flatten().numpy()
@@ -51,33 +72,40 @@ def _rank_main(rank, world, port, q):
         cand = torch.tensor([int(mine[r]) for r in reps_l], dtype=torch.int64)
         c = torch.tensor(costs[cand.numpy()], dtype=torch.float64)
         ph = h_i64[cand]
-        gc, gph, gcand = exchange_reps(c, ph, cand, world)
-        q.put((rank, gcand.tolist(), gc.tolist(), gph.tolist()))
+        beam, bcost, bottom, n_all = exchange.sharded_cut(
+            _CpuCut(), c, ph, cand, flagged_tensor(flagged, "cpu"), 2.0, 0.0, phase_seed, 32, 1e-14, world)
+        q.put((rank, beam.tolist(), bcost.tolist(), cand[bottom].tolist(), n_all, exchange.LAST_BYTES,
+               exchange.LAST_FALLBACK))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_bucket_sharded_reps_merge_to_global_order(world):
+@pytest.mark.parametrize("world,seed,ties", [(2, 7, False), (4, 7, False), (2, 11, True)])
+def test_sharded_cut_matches_single_process_cut(world, seed, ties):
     from oracle import structure
-    hashes, valid, costs = _workload()
+    hashes, valid, costs, flagged = _workload(seed, ties=ties)
     phase_seed = 3 * 101 + 11
-    want, _ = structure.select_reps([int(h) for h in hashes], valid, phase_seed)
+    reps, _ = structure.select_reps([int(h) for h in hashes], valid, phase_seed)
+    kept, bottom = structure.cut(reps, [float(costs[i]) for i in reps], [int(hashes[i]) for i in reps],
+                                 flagged, 2.0, 32)
+    want_beam = [reps[p] for p in kept]
+    want_bottom = sorted(reps[p] for p in bottom)
     ctx = tmp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, seed, ties, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got = [q.get(timeout=120) for _ in range(world)]
+    got = [q.get(timeout=180) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, cand, c, ph in got:
-        assert cand == want, f"rank {rank} merged rep order differs"
-        assert c == [float(costs[i]) for i in want]
-        assert [x & 0xFFFFFFFFFFFFFFFF for x in ph] == [int(hashes[i]) for i in want]
-    # the cut every rank then performs is therefore identical to one GPU's
-    kept, bottom = structure.cut(want, [float(costs[i]) for i in want],
-                                 [int(hashes[i]) for i in want], set(), 2.0, 32)
-    assert len(kept) == min(32, len(want))
+    all_bottom = sorted(x for g in got for x in g[3])
+    assert all_bottom == want_bottom        # bottom halves partition across ranks
+    for rank, beam, bcost, _, n_all, nbytes, fell_back in got:
+        assert fell_back == ties
+        assert beam == want_beam, f"rank {rank} beam differs"
+        assert bcost == [float(costs[i]) for i in want_beam]
+        assert n_all == len(reps)
+        if not ties:   # fixed-size windows + histograms, independent of the rep count
+            assert nbytes < 64 * 1024
