@@ -156,6 +156,20 @@ int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
                  double* feats, int32_t* row_key, int32_t* n_rows,
                  uint8_t* verdict, int32_t* row_src, void* stream);
 
+/* gs_featurize with a caller-provided workspace: never allocates and never
+ * synchronizes (CUDA-graph capturable).  Batches of >= 8192 candidates with
+ * features use the two-phase sibling schedule, which saves one warp state
+ * per decision-structure run; `max_runs` (<= 0: min(n/8, 1 GiB of states))
+ * bounds how many runs get a state slot — a batch with more runs, or runs
+ * shorter than 8 on average, takes the one-phase schedule on the device
+ * (same results).  Size the workspace with
+ * gs_featurize_workspace_bytes(p, n, s, max_runs). */
+int64_t gs_featurize_workspace_bytes(gs_pipeline_t p, int64_t n, int s, int64_t max_runs);
+int gs_featurize_ws(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
+                    double* feats, int32_t* row_key, int32_t* n_rows,
+                    uint8_t* verdict, int32_t* row_src, int64_t max_runs,
+                    void* workspace, int64_t ws_bytes, void* stream);
+
 /* K2: basis + two-tower network + g.c + h + in-order stage sum.  Replaces
  * CostEvaluator.cost (search.py:115-124).  row_cost/basis_gh optional
  * (NULL = not written; basis_gh is [c*R + r][31] = g[30], h).  With
@@ -175,6 +189,12 @@ int gs_cost(gs_pipeline_t p, const double* feats, const int32_t* row_key,
  * first use with a larger n (synchronizes `stream` then). */
 int gs_struct_hash(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
                    int depth, uint64_t* out, void* stream);
+/* gs_struct_hash with a caller-provided workspace of
+ * gs_struct_hash_workspace_bytes(n) bytes (never allocates or synchronizes). */
+int64_t gs_struct_hash_workspace_bytes(int64_t n);
+int gs_struct_hash_ws(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
+                      int depth, uint64_t* out, void* workspace, int64_t ws_bytes,
+                      void* stream);
 
 /* K4: bucket by hash + hierarchical-sampling representatives
  * (sampling.py:45-59, search.py:127-165).  `valid[i]` = verdict==0.

@@ -19,7 +19,8 @@ EXPORTS = ("gs_last_error", "gs_version", "gs_launch_count", "gs_pipeline_create
            "gs_pipeline_max_rows", "gs_set_weights", "gs_set_reuse", "gs_featurize", "gs_cost",
            "gs_struct_hash", "gs_select_workspace_bytes", "gs_select_reps",
            "gs_topk_workspace_bytes", "gs_beam_topk", "gs_check", "gs_stats", "gs_debug_phases",
-           "gs_expand_workspace_bytes", "gs_expand_step", "gs_simulate")
+           "gs_expand_workspace_bytes", "gs_expand_step", "gs_simulate", "gs_featurize_workspace_bytes",
+           "gs_featurize_ws", "gs_struct_hash_workspace_bytes", "gs_struct_hash_ws")
 
 
 class GsError(RuntimeError):
@@ -60,6 +61,10 @@ def load(path: str = LIB_PATH):
         "gs_expand_workspace_bytes": (i64, [i64]),
         "gs_expand_step": (i32, [P, V, i64, i32, V, V, V, V, i64, V, V, V]),
         "gs_simulate": (i32, [P, V, i64, i32, V, V, V, V, V]),
+        "gs_featurize_workspace_bytes": (i64, [P, i64, i32, i64]),
+        "gs_featurize_ws": (i32, [P, V, i64, i32, V, V, V, V, V, i64, V, i64, V]),
+        "gs_struct_hash_workspace_bytes": (i64, [i64]),
+        "gs_struct_hash_ws": (i32, [P, V, i64, i32, i32, V, V, i64, V]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -17,7 +17,7 @@
 //     histograms, then counts each distinct residue once per emulated warp
 //     with __match_any_sync / __ballot_sync / __popc on the real lanes.
 #include "gs_internal.cuh"
-#include <cub/cub.cuh>
+#include "scan.cuh"
 #include <cuda/std/cstdint>
 
 namespace gs {
@@ -2015,11 +2015,24 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
                  int64_t n, int S, double* __restrict__ feats, int32_t* __restrict__ row_key,
                  int32_t* __restrict__ n_rows, uint8_t* __restrict__ verdict, int32_t* __restrict__ row_src,
                  Layout L, int* gerr, int reuse, uint8_t* __restrict__ gscratch, const uint8_t* __restrict__ heads,
-                 int mode, const int32_t* __restrict__ run_id, const int32_t* __restrict__ run_head, int64_t nruns,
+                 int mode, const int32_t* __restrict__ run_id, const int32_t* __restrict__ run_head,
+                 const uint32_t* __restrict__ nruns_dev, int64_t max_runs,
                  uint8_t* __restrict__ slots, int64_t slot_bytes, int32_t* __restrict__ row_kernel) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar;
   const int warp = threadIdx.x >> 5, lane = lane_id(), nw = blockDim.x >> 5;
+  // Two-phase launches read the run count the preparation kernels left on
+  // the device.  Too many runs for the slots, or runs shorter than 8 on
+  // average: the run-head launch does the one-phase (run-aligned unit)
+  // schedule instead and the sibling launch has nothing to do.
+  int64_t nruns = 0;
+  if (mode != 0) {
+    nruns = (int64_t)*nruns_dev;
+    if (nruns > max_runs || nruns * 8 > n) {
+      if (mode == 2) return;
+      mode = 0;
+    }
+  }
   if (threadIdx.x == 0) bulk_stage(sm + L.blob, blob, P->blob_bytes, &bar);
   uint8_t* ws = sm + L.warps + (size_t)warp * L.warp_bytes;   // this warp's slice
   // capacity-sized structure arrays live in the slice, or — for pipelines
@@ -2281,36 +2294,37 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
 // Decision-structure run heads for the K1 work units: candidate c starts a
 // run when any record's (func, consumer, kind) differs from candidate c-1's
 // (the K1 sibling test); one warp per candidate, coalesced record loads.
-__global__ void k1_heads_kernel(const GsDecision* __restrict__ dec, int64_t n, int S, uint8_t* __restrict__ head) {
+// `hflag` (optional) receives the same flag as a u32 for the run scan.
+__global__ void k1_heads_kernel(const GsDecision* __restrict__ dec, int64_t n, int S, uint8_t* __restrict__ head,
+                                uint32_t* __restrict__ hflag) {
   const int lane = threadIdx.x & 31;
   const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (c >= n) return;
-  if (c == 0) { if (lane == 0) head[0] = 1; return; }
-  const uint2* a = reinterpret_cast<const uint2*>(dec + c * S);
-  const uint2* b = reinterpret_cast<const uint2*>(dec + (c - 1) * S);
-  bool diff = false;
-  for (int i = lane; i < S; i += 32) {
-    const uint2 x = __ldg(a + 2 * i), y = __ldg(b + 2 * i);
-    diff |= x.x != y.x || ((x.y ^ y.y) & 0xFFu) != 0u;
+  bool diff = c == 0;
+  if (c > 0) {
+    const uint2* a = reinterpret_cast<const uint2*>(dec + c * S);
+    const uint2* b = reinterpret_cast<const uint2*>(dec + (c - 1) * S);
+    for (int i = lane; i < S; i += 32) {
+      const uint2 x = __ldg(a + 2 * i), y = __ldg(b + 2 * i);
+      diff |= x.x != y.x || ((x.y ^ y.y) & 0xFFu) != 0u;
+    }
+    diff = __any_sync(0xffffffffu, diff);
   }
-  diff = __any_sync(0xffffffffu, diff);
-  if (lane == 0) head[c] = diff;
+  if (lane == 0) {
+    head[c] = diff;
+    if (hflag) hflag[c] = diff ? 1u : 0u;
+  }
 }
 
-struct HeadToInt {
-  __host__ __device__ int operator()(const uint8_t& h) const { return (int)h; }
-};
-
-// run_head[r] = first candidate of run r (run_id = inclusive scan of heads - 1)
-__global__ void k1_run_heads_kernel(const uint8_t* __restrict__ head, const int32_t* __restrict__ run_id, int64_t n,
+// run_id = inclusive scan of the head flags - 1; run_head[r] = first
+// candidate of run r
+__global__ void k1_run_heads_kernel(const uint8_t* __restrict__ head, int32_t* __restrict__ run_id, int64_t n,
                                     int32_t* __restrict__ run_head) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < n && head[c]) run_head[run_id[c]] = (int32_t)c;
-}
-
-__global__ void k1_run_ids_kernel(int32_t* __restrict__ run_id, int64_t n) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < n) run_id[c] -= 1;
+  if (c >= n) return;
+  const int32_t r = run_id[c] - 1;
+  run_id[c] = r;
+  if (head[c]) run_head[r] = (int32_t)c;
 }
 
 }  // namespace gs
@@ -2400,41 +2414,28 @@ int featurize_warps(const Layout& L1, int max_smem) {
 }
 
 // Run heads of a batch (K1 sibling structure) and, for the two-phase
-// schedule, each candidate's run index and each run's head.  Returns the
-// number of runs (synchronizes `st` to read it) or -1.
-int64_t k1_prepare_runs(const GsDecision* dec, int64_t n, int S, uint8_t* heads, int32_t* run_id,
-                        int32_t* run_head, void* tmp, size_t tmp_bytes, cudaStream_t st) {
-  k1_heads_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(dec, n, S, heads);
-  g_launch_count++;
-  cub::TransformInputIterator<int, HeadToInt, const uint8_t*> it(heads, HeadToInt());
-  size_t need = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, need, it, run_id, (int)n, st);
-  if (need > tmp_bytes) return -1;
-  cub::DeviceScan::InclusiveSum(tmp, need, it, run_id, (int)n, st);
-  k1_run_ids_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(run_id, n);
+// schedule, each candidate's run index, each run's head and the run count
+// (`nruns`, left on the device: no host synchronization).
+void k1_prepare_runs(const GsDecision* dec, int64_t n, int S, uint8_t* heads, int32_t* run_id, int32_t* run_head,
+                     uint32_t* sums, uint32_t* nruns, cudaStream_t st) {
+  uint32_t* flag = reinterpret_cast<uint32_t*>(run_id);
+  k1_heads_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(dec, n, S, heads, flag);
+  scan_u32(flag, flag, n, nullptr, true, sums, nruns, st);
   k1_run_heads_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(heads, run_id, n, run_head);
   g_launch_count += 2;
-  int32_t last = 0;
-  if (cudaMemcpyAsync(&last, run_id + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess) return -1;
-  if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
-  return (int64_t)last + 1;
 }
 
-size_t k1_runs_tmp_bytes(int64_t n) {
-  cub::TransformInputIterator<int, HeadToInt, const uint8_t*> it(nullptr, HeadToInt());
-  size_t need = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, need, it, (int32_t*)nullptr, (int)(n > 0 ? n : 1));
-  return need;
-}
+size_t k1_runs_sums_bytes(int64_t n) { return align256(4 * (scan_tiles_of(n) + 1)); }
 
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
                      const Layout& L, int nwarps, int grid, int* gerr, int reuse, uint8_t* gscratch,
-                     uint8_t* heads, int mode, const int32_t* run_id, const int32_t* run_head, int64_t nruns,
-                     uint8_t* slots, int64_t slot_bytes, int32_t* row_kernel, cudaStream_t st) {
+                     uint8_t* heads, int mode, const int32_t* run_id, const int32_t* run_head,
+                     const uint32_t* nruns, int64_t max_runs, uint8_t* slots, int64_t slot_bytes,
+                     int32_t* row_kernel, cudaStream_t st) {
   dim3 b(nwarps * 32);
   if (heads && reuse && mode == 0) {
-    k1_heads_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(dec, n, S, heads);
+    k1_heads_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(dec, n, S, heads, nullptr);
     g_launch_count++;
   }
   cudaMemsetAsync(gerr + 14, 0, sizeof(unsigned), st);   // work-unit counter
@@ -2442,7 +2443,7 @@ int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDeci
 #define GS_CASE(D)                                                                                  \
   case D:                                                                                           \
     cudaFuncSetAttribute(featurize_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total); \
-    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, gerr, reuse, gscratch, reuse ? heads : nullptr, mode, run_id, run_head, nruns, slots, slot_bytes, row_kernel); \
+    featurize_kernel<D><<<grid, b, L.total, st>>>(P, blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, L, gerr, reuse, gscratch, reuse ? heads : nullptr, mode, run_id, run_head, nruns, max_runs, slots, slot_bytes, row_kernel); \
     g_launch_count++;                                                                               \
     break;
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4)
