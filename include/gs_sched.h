@@ -225,6 +225,17 @@ int gs_beam_topk(const double* costs, const uint64_t* pass_hash, int64_t n,
                  double temperature, uint64_t phase_seed, int64_t k, double tie_band,
                  void* workspace, int64_t ws_bytes, int64_t* out_pos,
                  int64_t* n_out, uint8_t* bottom, void* stream);
+/* gs_beam_topk over the representatives as K4 left them: costs and
+ * pass_hash are per CANDIDATE, rep_idx[i] (i < *n_reps, a device count,
+ * at most n_max) the candidate of rep i.  Positions, the count and the
+ * bottom flags refer to rep order, as in gs_beam_topk.  No host-side count:
+ * a whole phase cut (K3 -> K1 -> K2 -> K4 -> K5) is CUDA-graph capturable.
+ * Workspace: gs_topk_workspace_bytes(n_max). */
+int gs_beam_topk_reps(const double* costs, const uint64_t* pass_hash, const int64_t* rep_idx,
+                      int64_t n_max, const int64_t* n_reps, const uint64_t* flagged,
+                      int64_t n_flagged, double penalty, double temperature, uint64_t phase_seed,
+                      int64_t k, double tie_band, void* workspace, int64_t ws_bytes,
+                      int64_t* out_pos, int64_t* n_out, uint8_t* bottom, void* stream);
 
 /* K1 work counters accumulated since the last call (then reset);
  * synchronizes `stream`.  out[0] candidates, [1] candidates resolved
@@ -257,16 +268,18 @@ typedef struct {
  * step[p]: index of the step root's (compute_root) record in parent p.
  * Writes offsets[0..n] (device int64: candidate range of each parent; the
  * total is offsets[n]) and, when out != NULL, the expanded records
- * out[offsets[n]][S] and (nullable) owner[] = parent index.  Call once with
- * out == NULL to size `out`.  Workspace: gs_expand_workspace_bytes(n).
- * More than 4096 tilings for one parent, or a step record that is not a
- * compute_root decision, raise GS_ERR_CAPACITY / GS_ERR_SCHEDULE at
- * gs_check. */
+ * out[offsets[n]][S] and (nullable) owner[] = parent index; out/owner hold
+ * out_cap candidates and nothing is written past them.  Call once with
+ * out == NULL to size `out`.  Workspace: gs_expand_workspace_bytes(n);
+ * at most 2^20 parents per call.  More than 4096 tilings for one parent, a
+ * step larger than out_cap (those parents are skipped), or a step record
+ * that is not a compute_root decision raise GS_ERR_CAPACITY /
+ * GS_ERR_SCHEDULE at gs_check. */
 int64_t gs_expand_workspace_bytes(int64_t n_parents);
 int gs_expand_step(gs_pipeline_t p, const GsDecision* parents, int64_t n_parents, int s,
                    const int32_t* step, const GsTilingMenus* menus, int64_t* offsets,
-                   void* workspace, int64_t ws_bytes, GsDecision* out, int32_t* owner,
-                   void* stream);
+                   void* workspace, int64_t ws_bytes, GsDecision* out, int64_t out_cap,
+                   int32_t* owner, void* stream);
 
 /* ---- machine oracle ------------------------------
  * The throughput knobs of reference machine.py:26-31 (not hardware limits). */

@@ -1,5 +1,6 @@
 // extern "C" entry points of libgs_sched.so (declared in include/gs_sched.h).
 #include "gs_internal.cuh"
+#include <nvtx3/nvToolsExt.h>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -39,10 +40,11 @@ int64_t topk_workspace_bytes(int64_t n);
 int64_t expand_workspace_bytes(int64_t n);
 int launch_expand(const GsFunc* funcs, const GsDecision* parents, int64_t n, int S, const int32_t* step,
                   const GsTilingMenus& m, int64_t* offsets, void* ws, int64_t ws_bytes, GsDecision* out,
-                  int32_t* owner, int* gerr, int num_sms, cudaStream_t st);
-int beam_topk(const double* costs, const uint64_t* ph, int64_t n, const uint64_t* flagged, int64_t nflag,
-              double penalty, double temperature, uint64_t phase_seed, int64_t k, double band, void* ws,
-              int64_t ws_bytes, int64_t* out_pos, int64_t* n_out, uint8_t* bottom, cudaStream_t st);
+                  int64_t out_cap, int32_t* owner, int* gerr, int num_sms, cudaStream_t st);
+int beam_topk(const double* costs, const uint64_t* ph, const int64_t* rep, int64_t n, const int64_t* ndev,
+              const uint64_t* flagged, int64_t nflag, double penalty, double temperature, uint64_t phase_seed,
+              int64_t k, double band, void* ws, int64_t ws_bytes, int64_t* out_pos, int64_t* n_out, uint8_t* bottom,
+              cudaStream_t st);
 }  // namespace gs
 
 using namespace gs;
@@ -89,6 +91,14 @@ struct GsPipeline {
   uint8_t* simbuf = nullptr;     // K6: features, row keys / kernels, n_rows, verdicts (grow-only)
   int64_t simcap = 0;
 };
+
+// NVTX range per C-ABI entry point (header-only NVTX3; free when no tool
+// is attached): profiles show each library call around its kernels.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define GS_NVTX(name) NvtxRange gs_nvtx_range_(name)
 
 extern "C" {
 
@@ -378,6 +388,7 @@ extern "C" {
 
 int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, double* feats, int32_t* row_key,
                  int32_t* n_rows, uint8_t* verdict, int32_t* row_src, void* stream) {
+  GS_NVTX("gs_featurize");
   if (!p || S < 1 || n < 0) return fail(GS_ERR_ARG, "bad featurize arguments");
   if (p->reuse == 2 && feats && !row_src) return fail(GS_ERR_ARG, "reuse mode 2 (computed rows only) needs row_src");
   return featurize_owned(p, dec, n, S, feats, row_key, n_rows, verdict, row_src, nullptr, p->reuse, stream);
@@ -394,6 +405,7 @@ int64_t gs_featurize_workspace_bytes(gs_pipeline_t p, int64_t n, int s, int64_t 
 int gs_featurize_ws(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, double* feats, int32_t* row_key,
                     int32_t* n_rows, uint8_t* verdict, int32_t* row_src, int64_t max_runs, void* workspace,
                     int64_t ws_bytes, void* stream) {
+  GS_NVTX("gs_featurize_ws");
   if (!p || S < 1 || n < 0) return fail(GS_ERR_ARG, "bad featurize arguments");
   if (p->reuse == 2 && feats && !row_src) return fail(GS_ERR_ARG, "reuse mode 2 (computed rows only) needs row_src");
   if (n == 0) return GS_OK;
@@ -410,6 +422,7 @@ int gs_featurize_ws(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, do
 
 int gs_simulate(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, const GsOracleParams* op,
                 double* runtime, int64_t* spill_bytes, uint8_t* status, void* stream) {
+  GS_NVTX("gs_simulate");
   if (!p || !op || S < 1 || n < 0 || (n > 0 && (!dec || !runtime || !spill_bytes || !status)))
     return fail(GS_ERR_ARG, "bad simulate arguments");
   if (op->registers_per_thread_budget <= 0) return fail(GS_ERR_ARG, "registers_per_thread_budget must be positive");
@@ -453,6 +466,7 @@ int gs_check(gs_pipeline_t p, void* stream) {
 
 int gs_cost(gs_pipeline_t p, const double* feats, const int32_t* row_key, const int32_t* n_rows,
             const int32_t* row_src, int64_t n, double* total, double* row_cost, double* basis_gh, void* stream) {
+  GS_NVTX("gs_cost");
   if (!p || !p->net.sched_w) return fail(GS_ERR_ARG, "weights not set (gs_set_weights)");
   if (row_src && !row_cost) return fail(GS_ERR_ARG, "row reuse (row_src) needs the row_cost buffer");
   int rc = launch_cost(p->net, p->stage_of_func, feats, row_key, n_rows, row_src, n, std::max(1, p->host.max_rows),
@@ -467,6 +481,7 @@ int64_t gs_struct_hash_workspace_bytes(int64_t n) { return (std::max<int64_t>(1,
 
 int gs_struct_hash_ws(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, int depth, uint64_t* out,
                       void* workspace, int64_t ws_bytes, void* stream) {
+  GS_NVTX("gs_struct_hash_ws");
   if (!p || depth < 0) return fail(GS_ERR_ARG, "depth must be >= 0");
   if (ws_bytes < gs_struct_hash_workspace_bytes(n) || !workspace)
     return fail(GS_ERR_ARG, "hash workspace too small (gs_struct_hash_workspace_bytes)");
@@ -479,6 +494,7 @@ int gs_struct_hash_ws(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, 
 
 int gs_struct_hash(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, int depth, uint64_t* out,
                    void* stream) {
+  GS_NVTX("gs_struct_hash");
   if (!p || depth < 0) return fail(GS_ERR_ARG, "depth must be >= 0");
   if (n > p->hcap) {   // one-time growth of the run-head scratch
     CK(cudaStreamSynchronize((cudaStream_t)stream));
@@ -516,6 +532,7 @@ int64_t gs_select_workspace_bytes(int64_t n) { return select_workspace_bytes(n);
 int gs_select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, uint64_t phase_seed, void* ws,
                    int64_t ws_bytes, int64_t* rep_idx, int64_t* n_reps, int64_t* rej_idx, int64_t* n_rejects,
                    void* stream) {
+  GS_NVTX("gs_select_reps");
   int rc = select_reps(hashes, verdict, n, phase_seed, ws, ws_bytes, rep_idx, n_reps, n_rejects, rej_idx,
                        (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "select_reps: workspace too small or n too large");
@@ -529,7 +546,8 @@ int64_t gs_expand_workspace_bytes(int64_t n_parents) { return expand_workspace_b
 
 int gs_expand_step(gs_pipeline_t p, const GsDecision* parents, int64_t n_parents, int s, const int32_t* step,
                    const GsTilingMenus* menus, int64_t* offsets, void* workspace, int64_t ws_bytes, GsDecision* out,
-                   int32_t* owner, void* stream) {
+                   int64_t out_cap, int32_t* owner, void* stream) {
+  GS_NVTX("gs_expand_step");
   if (!p || !menus || !offsets || s < 1 || n_parents < 0) return fail(GS_ERR_ARG, "bad expand arguments");
   const GsTilingMenus& m = *menus;
   if (m.n_serial_powers < 0 || m.n_serial_powers > 8 || m.n_odd_serial < 0 || m.n_odd_serial > 8 ||
@@ -544,8 +562,8 @@ int gs_expand_step(gs_pipeline_t p, const GsDecision* parents, int64_t n_parents
   for (int i = 0; i < m.n_outer; ++i)
     if (m.outer_thread[i] < 1 || m.outer_thread[i] > 255) return fail(GS_ERR_ARG, "thread menu value out of range");
   int rc = launch_expand(reinterpret_cast<const GsFunc*>(p->blob), parents, n_parents, s, step, m, offsets, workspace,
-                         ws_bytes, out, owner, p->err, p->num_sms, (cudaStream_t)stream);
-  if (rc) return fail(GS_ERR_ARG, "expand: workspace too small or too many parents");
+                         ws_bytes, out, out_cap, owner, p->err, p->num_sms, (cudaStream_t)stream);
+  if (rc) return fail(GS_ERR_ARG, "expand: workspace too small or more than 2^20 parents");
   CK(cudaGetLastError());
   return GS_OK;
 }
@@ -553,8 +571,22 @@ int gs_expand_step(gs_pipeline_t p, const GsDecision* parents, int64_t n_parents
 int gs_beam_topk(const double* costs, const uint64_t* pass_hash, int64_t n, const uint64_t* flagged,
                  int64_t n_flagged, double penalty, double temperature, uint64_t phase_seed, int64_t k, double tie_band, void* ws,
                  int64_t ws_bytes, int64_t* out_pos, int64_t* n_out, uint8_t* bottom, void* stream) {
-  int rc = beam_topk(costs, pass_hash, n, flagged, n_flagged, penalty, temperature, phase_seed, k, tie_band, ws, ws_bytes,
-                     out_pos, n_out, bottom, (cudaStream_t)stream);
+  GS_NVTX("gs_beam_topk");
+  int rc = beam_topk(costs, pass_hash, nullptr, n, nullptr, flagged, n_flagged, penalty, temperature, phase_seed, k,
+                     tie_band, ws, ws_bytes, out_pos, n_out, bottom, (cudaStream_t)stream);
+  if (rc) return fail(GS_ERR_ARG, "beam_topk: workspace too small, k out of 1..16384 or negative tie band");
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
+int gs_beam_topk_reps(const double* costs, const uint64_t* pass_hash, const int64_t* rep_idx, int64_t n_max,
+                      const int64_t* n_reps, const uint64_t* flagged, int64_t n_flagged, double penalty,
+                      double temperature, uint64_t phase_seed, int64_t k, double tie_band, void* ws, int64_t ws_bytes,
+                      int64_t* out_pos, int64_t* n_out, uint8_t* bottom, void* stream) {
+  GS_NVTX("gs_beam_topk_reps");
+  if (!rep_idx || !n_reps) return fail(GS_ERR_ARG, "beam_topk_reps: rep_idx and n_reps are required");
+  int rc = beam_topk(costs, pass_hash, rep_idx, n_max, n_reps, flagged, n_flagged, penalty, temperature, phase_seed, k,
+                     tie_band, ws, ws_bytes, out_pos, n_out, bottom, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "beam_topk: workspace too small, k out of 1..16384 or negative tie band");
   CK(cudaGetLastError());
   return GS_OK;

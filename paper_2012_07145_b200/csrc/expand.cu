@@ -5,7 +5,7 @@
 // dim 0 varying slowest).  The host then uploads only the beam (parents),
 // not the expanded candidate records.
 #include "gs_internal.cuh"
-#include <cub/cub.cuh>
+#include "scan.cuh"
 
 namespace gs {
 
@@ -88,7 +88,7 @@ __device__ int64_t enum_tilings(const GsTilingMenus& m, const GsFunc& fn, F&& em
 
 __global__ void expand_count_kernel(const GsFunc* __restrict__ funcs, const GsDecision* __restrict__ parents,
                                     int64_t n, int S, const int32_t* __restrict__ step, GsTilingMenus m,
-                                    int64_t* __restrict__ counts, int* __restrict__ gerr) {
+                                    uint32_t* __restrict__ counts, int* __restrict__ gerr) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int s = step[p];
@@ -96,13 +96,13 @@ __global__ void expand_count_kernel(const GsFunc* __restrict__ funcs, const GsDe
   if (f == 0xFFFF || parents[p * S + s].kind != GS_ROOT) { counts[p] = 0; atomicOr(gerr, 32); return; }
   const int64_t c = enum_tilings(m, funcs[f], [](const int*, const int*) {});
   if (c > kMaxTilings) atomicOr(gerr, 16);
-  counts[p] = c;
+  counts[p] = (uint32_t)(c > kMaxTilings ? 0 : c);   // over-long lists are skipped (and reported)
 }
 
 __global__ void __launch_bounds__(kExpandWarps * 32) expand_write_kernel(
     const GsFunc* __restrict__ funcs, const GsDecision* __restrict__ parents, int64_t n, int S,
     const int32_t* __restrict__ step, GsTilingMenus m, const int64_t* __restrict__ offsets,
-    GsDecision* __restrict__ out, int32_t* __restrict__ owner) {
+    GsDecision* __restrict__ out, int64_t out_cap, int32_t* __restrict__ owner, int* __restrict__ gerr) {
   extern __shared__ __align__(16) uint8_t smx[];
   uint8_t (*til)[kMaxTilings][8] = reinterpret_cast<uint8_t (*)[kMaxTilings][8]>(smx);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -110,6 +110,10 @@ __global__ void __launch_bounds__(kExpandWarps * 32) expand_write_kernel(
   for (int64_t p = (int64_t)blockIdx.x * kExpandWarps + wib; p < n; p += nwarps) {
     const int64_t base = offsets[p], cnt = offsets[p + 1] - base;
     if (cnt <= 0 || cnt > kMaxTilings) continue;
+    if (base + cnt > out_cap) {   // the caller's buffer is smaller than the step: write nothing past it
+      if (lane == 0) atomicOr(gerr, 16);
+      continue;
+    }
     const int s = step[p];
     const GsDecision* par = parents + p * S;
     if (lane == 0) {
@@ -140,32 +144,40 @@ __global__ void __launch_bounds__(kExpandWarps * 32) expand_write_kernel(
   }
 }
 
+// offsets[0] = 0, offsets[p + 1] = inclusive prefix of the (u32) counts
+__global__ void expand_offsets_kernel(const uint32_t* __restrict__ incl, int64_t n, int64_t* __restrict__ offsets) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p == 0) offsets[0] = 0;
+  if (p < n) offsets[p + 1] = (int64_t)incl[p];
+}
+
+// counts | inclusive scan | scan tile sums
 int64_t expand_workspace_bytes(int64_t n) {
-  size_t tb = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, tb, (const int64_t*)nullptr, (int64_t*)nullptr, (int)(n > 0 ? n : 1));
-  return (int64_t)(((tb + 255) & ~(size_t)255) + 256 + 8 * (n + 1));
+  if (n < 1) n = 1;
+  return (int64_t)(2 * align256(4 * n) + align256(4 * (scan_tiles_of(n) + 1)));
 }
 
 int launch_expand(const GsFunc* funcs, const GsDecision* parents, int64_t n, int S, const int32_t* step,
                   const GsTilingMenus& m, int64_t* offsets, void* ws, int64_t ws_bytes, GsDecision* out,
-                  int32_t* owner, int* gerr, int num_sms, cudaStream_t st) {
-  if (n <= 0) return 0;
-  if (n > 0x7FFFFFFF) return -1;
-  size_t tb = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, tb, (const int64_t*)nullptr, (int64_t*)nullptr, (int)n);
-  const size_t tba = (tb + 255) & ~(size_t)255;
-  if ((int64_t)(tba + 256 + 8 * (n + 1)) > ws_bytes) return -2;
-  int64_t* counts = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(ws) + tba + 256);
+                  int64_t out_cap, int32_t* owner, int* gerr, int num_sms, cudaStream_t st) {
+  if (n <= 0) { cudaMemsetAsync(offsets, 0, sizeof(int64_t), st); return 0; }
+  if (n > (int64_t)1 << 20) return -1;   // keeps the u32 scan exact: n * kMaxTilings < 2^32
+  if (expand_workspace_bytes(n) > ws_bytes) return -2;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  uint32_t* counts = reinterpret_cast<uint32_t*>(w);
+  uint32_t* incl = reinterpret_cast<uint32_t*>(w + align256(4 * n));
+  uint32_t* sums = reinterpret_cast<uint32_t*>(w + 2 * align256(4 * n));
   expand_count_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(funcs, parents, n, S, step, m, counts, gerr);
-  g_launch_count++;
-  cudaMemsetAsync(offsets, 0, sizeof(int64_t), st);
-  cub::DeviceScan::InclusiveSum(ws, tb, counts, offsets + 1, (int)n, st);
+  scan_u32(counts, incl, n, nullptr, true, sums, nullptr, st);
+  expand_offsets_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(incl, n, offsets);
+  g_launch_count += 2;
   if (out) {
     const int64_t want = (n + kExpandWarps - 1) / kExpandWarps;
     const int grid = (int)(want < (int64_t)num_sms * 16 ? want : (int64_t)num_sms * 16);
     const int smem = kExpandWarps * kMaxTilings * 8;
     cudaFuncSetAttribute(expand_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    expand_write_kernel<<<grid, kExpandWarps * 32, smem, st>>>(funcs, parents, n, S, step, m, offsets, out, owner);
+    expand_write_kernel<<<grid, kExpandWarps * 32, smem, st>>>(funcs, parents, n, S, step, m, offsets, out, out_cap,
+                                                               owner, gerr);
     g_launch_count++;
   }
   return 0;

@@ -1,21 +1,28 @@
-// K1 — per-candidate resolve + 56 schedule features per stage row + prune.
+// K1 — per-candidate resolve + 56 schedule features per stage row + prune
+// (reference featurize.py:275-617, resolve.py:207-425, options.py:200-255).
 //
-// One CTA scores one candidate at a time (persistent grid over candidates):
+// One CTA per SM; every warp is an independent scorer with its own slice of
+// shared memory, taking work units from a global counter:
 //   * the candidate-independent pipeline descriptor is staged ONCE per CTA
-//     from global memory into shared memory with a bulk async copy (TMA
-//     `cp.async.bulk`, SASS UBLKCP) completing on an mbarrier;
-//   * warp 0 loads the 16-byte decision records with 128-bit loads and
-//     resolves the padded-tile geometry of every func into shared memory
-//     (reference resolve.py:229-376), then the prune verdict
-//     (options.py:200-255);
-//   * all warps then take stage rows round-robin and compute the 56
-//     features of each row (featurize.py:415-617).  Warp-instruction
-//     transaction counts (featurize.py:173-196, 508-571) use the fact that a
-//     count only depends on the per-instruction address residue mod the
-//     transaction size (global) or bank period (shared): the warp builds the
-//     residue histogram of all emitted loads by cyclic convolution of per-dim
-//     histograms, then counts each distinct residue once per emulated warp
-//     with __match_any_sync / __ballot_sync / __popc on the real lanes.
+//     into shared memory with a bulk async copy (TMA `cp.async.bulk`, SASS
+//     UBLKCP) completing on an mbarrier — the only CTA-wide barrier;
+//   * per candidate the warp loads its 16-byte decision records with 128-bit
+//     loads, diffs them against the previous candidate it scored (siblings
+//     of a beam step share their decision structure), re-resolves only the
+//     funcs whose dependency mask meets the changed records, computes the
+//     prune verdict warp-parallel, and recomputes only the feature rows whose
+//     own / host / kernel / producer-layout records changed (the rest are
+//     bit-identical copies, or — reuse mode 2 — not written at all);
+//   * large batches of long sibling runs use a two-phase schedule: run heads
+//     first (each saves its warp state to its run's slot in HBM), then
+//     16-candidate sibling slices that resume from their head's state, so a
+//     run splits across warps without re-resolving;
+//   * warp-instruction transaction counts (featurize.py:173-196, 508-571)
+//     use the residue invariance of the counts (global: address constant mod
+//     32 B; shared: mod the 4 B bank width): residue histograms in registers,
+//     interval sums over one prefix scan for monotonic warps, and
+//     __match_any_sync / __ballot_sync for the rest.
+// See DESIGN.md "K1 featurize" for the roofline reading.
 #include "gs_internal.cuh"
 #include "scan.cuh"
 #include <cuda/std/cstdint>
@@ -1983,12 +1990,18 @@ __device__ __forceinline__ void row_features(K1<ND>& k, WarpScr& W, int func, in
 // ---------------------------------------------------------------------------
 // kernel
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void bulk_stage(void* dst_smem, const void* src, int bytes, uint64_t* bar) {
-  // TMA bulk copy global -> shared, completion on an mbarrier (single thread)
-  unsigned dst = (unsigned)__cvta_generic_to_shared(dst_smem);
+// TMA bulk copy global -> shared completing on an mbarrier.  Thread 0
+// initialises the barrier; the CTA barrier that follows makes the
+// initialisation visible before anyone waits on it; thread 0 then posts the
+// expected bytes and issues the copy.
+__device__ __forceinline__ void bulk_init(uint64_t* bar) {
   unsigned b = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
   asm volatile("fence.mbarrier_init.release.cluster;");
+}
+__device__ __forceinline__ void bulk_stage(void* dst_smem, const void* src, int bytes, uint64_t* bar) {
+  unsigned dst = (unsigned)__cvta_generic_to_shared(dst_smem);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes));
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(dst), "l"(src), "r"(bytes), "r"(b) : "memory");
@@ -2033,6 +2046,8 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
       mode = 0;
     }
   }
+  if (threadIdx.x == 0) bulk_init(&bar);
+  __syncthreads();
   if (threadIdx.x == 0) bulk_stage(sm + L.blob, blob, P->blob_bytes, &bar);
   uint8_t* ws = sm + L.warps + (size_t)warp * L.warp_bytes;   // this warp's slice
   // capacity-sized structure arrays live in the slice, or — for pipelines

@@ -428,6 +428,13 @@ int select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, uint6
 }
 
 // ------------------------------------------------------------ K5 kernels ---
+// element count given on the host (nmax) or, when ndev is set, on the device
+__device__ __forceinline__ int64_t count64(int64_t nmax, const int64_t* ndev) {
+  if (!ndev) return nmax;
+  const int64_t c = *ndev;
+  return c < nmax ? (c < 0 ? 0 : c) : nmax;
+}
+
 __device__ __forceinline__ uint64_t sortable(double x) {
   if (x == 0.0) x = 0.0;   // -0.0 == 0.0 in the reference's sort
   uint64_t b = (uint64_t)__double_as_longlong(x);
@@ -438,16 +445,18 @@ __device__ __forceinline__ double unsortable(uint64_t k) {
   return __longlong_as_double((long long)b);
 }
 
-__global__ void keys_kernel(const double* __restrict__ costs, const uint64_t* __restrict__ ph, int64_t n,
+__global__ void keys_kernel(const double* __restrict__ costs, const uint64_t* __restrict__ ph,
+                            const int64_t* __restrict__ rep, int64_t nmax, const int64_t* __restrict__ ndev,
                             const uint64_t* __restrict__ flagged, int64_t nflag, double penalty,
                             uint64_t* __restrict__ key, uint64_t* __restrict__ ckey, double* __restrict__ kval) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double c = costs[i];
+  if (i >= count64(nmax, ndev)) return;
+  const int64_t src = rep ? rep[i] : i;   // rep: the representatives' candidate indices
+  double c = costs[src];
   bool f = false;
   if (nflag > 0) {
     int64_t lo = 0, hi = nflag;
-    const uint64_t h = ph[i];
+    const uint64_t h = ph[src];
     while (lo < hi) { int64_t mid = (lo + hi) >> 1; if (flagged[mid] < h) lo = mid + 1; else hi = mid; }
     f = lo < nflag && flagged[lo] == h;
   }
@@ -468,8 +477,10 @@ __device__ __forceinline__ double gumbel_key(double kv, double gum, double tempe
   return log(k) + gum * temperature;
 }
 
-__global__ void gumbel_parallel(double* __restrict__ kval, uint64_t* __restrict__ key, int64_t n,
-                                double temperature, uint64_t phase_seed, uint32_t* __restrict__ redo) {
+__global__ void gumbel_parallel(double* __restrict__ kval, uint64_t* __restrict__ key, int64_t nmax,
+                                const int64_t* __restrict__ ndev, double temperature, uint64_t phase_seed,
+                                uint32_t* __restrict__ redo) {
+  const int64_t n = count64(nmax, ndev);
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i0 = c * kGumbelChunk;
   if (i0 >= n) return;
@@ -485,9 +496,11 @@ __global__ void gumbel_parallel(double* __restrict__ kval, uint64_t* __restrict_
   }
 }
 
-__global__ void gumbel_serial(const double* __restrict__ kval, uint64_t* __restrict__ key, int64_t n,
-                              double temperature, uint64_t phase_seed, const uint32_t* __restrict__ redo) {
+__global__ void gumbel_serial(const double* __restrict__ kval, uint64_t* __restrict__ key, int64_t nmax,
+                              const int64_t* __restrict__ ndev, double temperature, uint64_t phase_seed,
+                              const uint32_t* __restrict__ redo) {
   if (threadIdx.x != 0 || blockIdx.x != 0 || *redo == 0) return;
+  const int64_t n = count64(nmax, ndev);
   Pcg64 g;
   seed_pair(g, phase_seed, 0x657870ULL);
   for (int64_t i = 0; i < n; ++i) {
@@ -535,6 +548,7 @@ __device__ void radix_select(const uint64_t* __restrict__ key, int64_t n, int64_
       const int64_t excl = (int64_t)(incl - tot);
       const bool mine = excl <= r && r < (int64_t)incl;
       const unsigned who = __ballot_sync(0xffffffffu, mine);
+      __syncwarp();   // every lane has read s_rank before the owner rewrites it
       if (lane == __ffs(who) - 1) {
         int64_t acc = excl;
         int d = lane * 8;
@@ -598,9 +612,12 @@ constexpr int kWinCap = 16384;
 constexpr int kWinSmem = kWinCap * (8 + 4);
 
 __global__ void __launch_bounds__(kWinNT) cut_kernel(const uint64_t* __restrict__ key, const uint64_t* __restrict__ ckey,
-                                                     int64_t n, int64_t k, double band, int64_t* __restrict__ out_pos,
+                                                     int64_t nmax, const int64_t* __restrict__ ndev, int64_t k,
+                                                     double band, int64_t* __restrict__ out_pos,
                                                      int64_t* __restrict__ n_out, uint8_t* __restrict__ bottom,
                                                      uint32_t* __restrict__ status) {
+  const int64_t n = count64(nmax, ndev);
+  if (k > n) k = n;
   extern __shared__ __align__(16) unsigned char win_smem[];
   uint64_t* wk = (uint64_t*)win_smem;
   uint32_t* wp = (uint32_t*)(wk + kWinCap);
@@ -610,6 +627,10 @@ __global__ void __launch_bounds__(kWinNT) cut_kernel(const uint64_t* __restrict_
   __shared__ uint32_t tot;
   const bool top = blockIdx.x == 0;
   if (!top && !bottom) return;
+  if (top && k < 1) {   // empty representative set (device count 0)
+    if (threadIdx.x == 0) *n_out = 0;
+    return;
+  }
   const uint64_t* kk = top ? key : ckey;
   if (!top && n <= 1) {
     for (int64_t i = threadIdx.x; i < n; i += kWinNT) bottom[i] = 0;
@@ -717,9 +738,10 @@ int64_t topk_workspace_bytes(int64_t n) {
   return (int64_t)(align256(8 * n) * 3 + align256(16));
 }
 
-int beam_topk(const double* costs, const uint64_t* ph, int64_t n, const uint64_t* flagged, int64_t nflag,
-              double penalty, double temperature, uint64_t phase_seed, int64_t k, double band, void* ws,
-              int64_t ws_bytes, int64_t* out_pos, int64_t* n_out, uint8_t* bottom, cudaStream_t st) {
+int beam_topk(const double* costs, const uint64_t* ph, const int64_t* rep, int64_t n, const int64_t* ndev,
+              const uint64_t* flagged, int64_t nflag, double penalty, double temperature, uint64_t phase_seed,
+              int64_t k, double band, void* ws, int64_t ws_bytes, int64_t* out_pos, int64_t* n_out, uint8_t* bottom,
+              cudaStream_t st) {
   if (n <= 0) { cudaMemsetAsync(n_out, 0, 8, st); return 0; }
   if (topk_workspace_bytes(n) > ws_bytes) return -2;
   if (n >= (int64_t)0xFFFFFFFF) return -3;
@@ -738,15 +760,15 @@ int beam_topk(const double* costs, const uint64_t* ph, int64_t n, const uint64_t
   uint32_t* status = (uint32_t*)p;
   cudaMemsetAsync(status, 0, 8, st);
   const unsigned G = (unsigned)((n + 255) / 256);
-  keys_kernel<<<G, 256, 0, st>>>(costs, ph, n, flagged, nflag, penalty, key, ckey, kval); g_launch_count++;
+  keys_kernel<<<G, 256, 0, st>>>(costs, ph, rep, n, ndev, flagged, nflag, penalty, key, ckey, kval); g_launch_count++;
   if (temperature > 0) {
     const int64_t chunks = (n + kGumbelChunk - 1) / kGumbelChunk;
-    gumbel_parallel<<<(unsigned)((chunks + 127) / 128), 128, 0, st>>>(kval, key, n, temperature, phase_seed,
+    gumbel_parallel<<<(unsigned)((chunks + 127) / 128), 128, 0, st>>>(kval, key, n, ndev, temperature, phase_seed,
                                                                        status + 1);
-    gumbel_serial<<<1, 32, 0, st>>>(kval, key, n, temperature, phase_seed, status + 1);
+    gumbel_serial<<<1, 32, 0, st>>>(kval, key, n, ndev, temperature, phase_seed, status + 1);
     g_launch_count += 2;
   }
-  cut_kernel<<<bottom ? 2 : 1, kWinNT, kWinSmem, st>>>(key, ckey, n, k, band, out_pos, n_out, bottom, status);
+  cut_kernel<<<bottom ? 2 : 1, kWinNT, kWinSmem, st>>>(key, ckey, n, ndev, k, band, out_pos, n_out, bottom, status);
   cut_status<<<1, 32, 0, st>>>(status, n_out);
   g_launch_count += 2;
   return 0;

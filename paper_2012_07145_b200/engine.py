@@ -226,13 +226,14 @@ class Scorer:
         offsets = torch.empty((P + 1,), dtype=torch.int64, device=self.device)
         if total is None:
             _lib.check(self.lib.gs_expand_step(self.handle, _ptr(parents), P, S, _ptr(steps), C.byref(m),
-                                               _ptr(offsets), _ptr(ws), wsb, C.c_void_p(0), C.c_void_p(0),
+                                               _ptr(offsets), _ptr(ws), wsb, C.c_void_p(0), 0, C.c_void_p(0),
                                                _stream()))
             total = int(offsets[-1].item())
         out = torch.empty((total, S * 16), dtype=torch.uint8, device=self.device)
         owner = torch.empty((max(1, total),), dtype=torch.int32, device=self.device)
         _lib.check(self.lib.gs_expand_step(self.handle, _ptr(parents), P, S, _ptr(steps), C.byref(m),
-                                           _ptr(offsets), _ptr(ws), wsb, _ptr(out), _ptr(owner), _stream()))
+                                           _ptr(offsets), _ptr(ws), wsb, _ptr(out), total, _ptr(owner),
+                                           _stream()))
         return out, owner[:total], offsets
 
     # -- K4 -------------------------------------------------------------------

@@ -1,40 +1,45 @@
 """The host beam-step enumeration (gen.root_tilings / expand_step), which the
-device expansion is checked against, equals the reference menus
-(options.py:144-183 enumerate_serial_tilings / enumerate_thread_tilings in
-`_phase2_candidates` order, search.py:223-235), restated here from the
-reference source as plain loops."""
+device expansion is checked against, equals the reference's own menus:
+`gpusched.options.enumerate_serial_tilings` / `enumerate_thread_tilings`
+(options.py:144-183) in `_phase2_candidates` order (search.py:223-235),
+called from the unmodified reference (importable in the build container;
+skipped where it is absent)."""
 
-import itertools
 import math
+import os
+import sys
 
 import pytest
 
 from paper_2012_07145_b200 import gen
 
-
-def _ref_serial(extents, m=gen.Menus):
-    per = []
-    for e in extents:
-        opts = sorted({s for s in m.serial_powers if s <= e})
-        for o in m.odd_serial:
-            if o <= e and e % o == 0 and (e // o) % m.warp_size == 0:
-                opts.append(o)
-        per.append(sorted(set(opts)) or [1])
-    return [v for v in itertools.product(*per) if math.prod(v) <= m.unroll_budget]
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+for _p in ("/root/reference/pkg/src", os.path.join(ROOT, "baseline", "_ref")):
+    if os.path.isdir(os.path.join(_p, "gpusched")) and _p not in sys.path:
+        sys.path.append(_p)
+options = pytest.importorskip("gpusched.options")
 
 
-def _ref_thread(extents, m=gen.Menus):
-    inner = next((i for i, e in enumerate(extents) if e >= 16), 0)
-    per = [sorted({min(t, e) for t in (m.innermost_thread if i == inner else m.outer_thread)})
-           for i, e in enumerate(extents)]
-    return list(itertools.product(*per))
+def _reference_phase2_order(extents):
+    cfg = options.DEFAULT_TILING
+    out = []
+    for serial in options.enumerate_serial_tilings(extents, config=cfg):
+        post = tuple(math.ceil(e / s) for e, s in zip(extents, serial))
+        for thread in options.enumerate_thread_tilings(post, config=cfg):
+            out.append((tuple(serial), tuple(thread)))
+    return out
 
 
-@pytest.mark.parametrize("extents", [(1024, 1024), (1536, 2560, 3), (56, 56, 256), (7, 3), (96, 1), (1280, 960)])
+@pytest.mark.parametrize("extents", [(1024, 1024), (1536, 2560, 3), (56, 56, 256), (7, 3), (96, 1), (1280, 960),
+                                     (1024,), (33, 17, 5), (2, 2, 2, 2)])
 def test_root_tilings_follow_reference_order(extents):
-    want = []
-    for s in _ref_serial(extents):
-        post = tuple(math.ceil(e / x) for e, x in zip(extents, s))
-        for t in _ref_thread(post):
-            want.append((s, t))
-    assert gen.root_tilings(extents) == want
+    assert [(tuple(s), tuple(t)) for s, t in gen.root_tilings(extents)] == _reference_phase2_order(extents)
+
+
+def test_menus_match_reference_config():
+    cfg = options.DEFAULT_TILING
+    for name in ("serial_powers", "odd_serial", "innermost_thread", "outer_thread", "unroll_budget", "warp_size"):
+        mine, ref = getattr(gen.Menus, name), getattr(cfg, name)
+        if isinstance(ref, (tuple, list)):
+            mine, ref = tuple(mine), tuple(ref)
+        assert mine == ref, name
