@@ -300,6 +300,42 @@ typedef struct {
 int gs_simulate(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s, const GsOracleParams* op,
                 double* runtime, int64_t* spill_bytes, uint8_t* status, void* stream);
 
+/* ---- the cost model off the beam step ------
+ * Weights are ONE packed fp64 device array in the reference tensor order
+ * (costmodel.py:183-193): algo_w[10][E] algo_b[E] sched_w[56][E] sched_b[E]
+ * head_w[2E][H] head_b[H] out_w[H][30] out_b[30]; gs_model_params(E, H)
+ * doubles. */
+int gs_model_params(int embed_dim, int hidden_dim);
+
+/* predict_coefficients (costmodel.py:316-324) and stage_cost /
+ * CostBreakdown (costmodel.py:34-115) for n rows: algo [n][10], sched
+ * [n][56] (raw schedule features).  coeffs_in (nullable) [n][30]: use these
+ * coefficients instead of the network (stage_cost with given c; the caller
+ * validates c > 0).  Outputs (nullable): coeffs_out [n][30]; breakdown
+ * [n][7] = compute, load, store, malloc, parallelism, working_set, total —
+ * the reference's term order and rounding (bit-exact for given c). */
+int gs_predict(const double* weights, int embed_dim, int hidden_dim, const double* algo,
+               const double* sched, const double* coeffs_in, int64_t n, double* coeffs_out,
+               double* breakdown, void* stream);
+
+/* train (costmodel.py:391-432): SGD with momentum on (log predicted total -
+ * log runtime)^2, gradients through the network only (basis g, h fixed),
+ * one persistent CTA running every epoch.  Samples: rows row_off[s] ..
+ * row_off[s+1]-1 of algo [rows][10], sched [rows][56], g [rows][30], h
+ * [rows]; runtime[s] > 0; order [epochs][n_samples] = each epoch's sample
+ * permutation (the reference's default_rng(seed).permutation stream).
+ * `weights` (device, packed) is updated in place; loss_hist[epoch] = mean
+ * squared error of the epoch; *status (device int) = 0, or s + 1 when
+ * sample s predicted a non-finite or non-positive total (training stops
+ * there; the reference raises ValueError).  At most 1024 rows per sample.
+ * Workspace: gs_train_workspace_bytes(E, H, max_rows). */
+int64_t gs_train_workspace_bytes(int embed_dim, int hidden_dim, int max_rows);
+int gs_train(double* weights, int embed_dim, int hidden_dim, const double* algo, const double* sched,
+             const double* g, const double* h, const int64_t* row_off, const double* runtime,
+             const int32_t* order, int n_samples, int epochs, double learning_rate, double momentum,
+             int max_rows, void* workspace, int64_t ws_bytes, double* loss_hist, int* status,
+             void* stream);
+
 /* Device-side error word of the last K1 launch (capacity overflow etc.);
  * synchronizes `stream`. */
 int gs_check(gs_pipeline_t p, void* stream);

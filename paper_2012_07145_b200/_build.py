@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgs_sched.so")
-SOURCES = ("featurize.cu", "cost.cu", "hash.cu", "select.cu", "expand.cu", "simulate.cu", "api.cu")
+SOURCES = ("featurize.cu", "cost.cu", "hash.cu", "select.cu", "expand.cu", "simulate.cu", "model.cu", "api.cu")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v"]

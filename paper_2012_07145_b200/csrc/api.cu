@@ -41,6 +41,13 @@ int64_t expand_workspace_bytes(int64_t n);
 int launch_expand(const GsFunc* funcs, const GsDecision* parents, int64_t n, int S, const int32_t* step,
                   const GsTilingMenus& m, int64_t* offsets, void* ws, int64_t ws_bytes, GsDecision* out,
                   int64_t out_cap, int32_t* owner, int* gerr, int num_sms, cudaStream_t st);
+int64_t train_cache_bytes(int E, int H, int max_rows);
+int model_params(int E, int H);
+int launch_predict(const double* w, int E, int H, const double* algo, const double* sched, const double* cin,
+                   int64_t n, double* cout, double* breakdown, cudaStream_t st);
+int launch_train(double* w, int E, int H, const double* algo, const double* sched, const double* g, const double* h,
+                 const int64_t* row_off, const double* runtime, const int32_t* order, int n_samples, int epochs,
+                 double lr, double momentum, double* cache, double* loss_hist, int* status, cudaStream_t st);
 int beam_topk(const double* costs, const uint64_t* ph, const int64_t* rep, int64_t n, const int64_t* ndev,
               const uint64_t* flagged, int64_t nflag, double penalty, double temperature, uint64_t phase_seed,
               int64_t k, double band, void* ws, int64_t ws_bytes, int64_t* out_pos, int64_t* n_out, uint8_t* bottom,
@@ -588,6 +595,41 @@ int gs_beam_topk_reps(const double* costs, const uint64_t* pass_hash, const int6
   int rc = beam_topk(costs, pass_hash, rep_idx, n_max, n_reps, flagged, n_flagged, penalty, temperature, phase_seed, k,
                      tie_band, ws, ws_bytes, out_pos, n_out, bottom, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "beam_topk: workspace too small, k out of 1..16384 or negative tie band");
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
+int gs_model_params(int E, int H) { return (E < 1 || H < 1) ? -1 : model_params(E, H); }
+
+int gs_predict(const double* weights, int E, int H, const double* algo, const double* sched, const double* coeffs_in,
+               int64_t n, double* coeffs_out, double* breakdown, void* stream) {
+  GS_NVTX("gs_predict");
+  if (!weights && !coeffs_in) return fail(GS_ERR_ARG, "predict: weights or coefficients required");
+  if (!sched && breakdown) return fail(GS_ERR_ARG, "predict: the breakdown needs the schedule features");
+  if (!coeffs_in && (!algo || !sched)) return fail(GS_ERR_ARG, "predict: the network needs algo and schedule rows");
+  if (launch_predict(weights, E, H, algo, sched, coeffs_in, n, coeffs_out, breakdown, (cudaStream_t)stream))
+    return fail(GS_ERR_ARG, "predict: unsupported network dims (2*embed <= 128)");
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
+int64_t gs_train_workspace_bytes(int E, int H, int max_rows) {
+  if (E < 1 || H < 1 || max_rows < 0) return -1;
+  return train_cache_bytes(E, H, max_rows);
+}
+
+int gs_train(double* weights, int E, int H, const double* algo, const double* sched, const double* g, const double* h,
+             const int64_t* row_off, const double* runtime, const int32_t* order, int n_samples, int epochs,
+             double learning_rate, double momentum, int max_rows, void* workspace, int64_t ws_bytes, double* loss_hist,
+             int* status, void* stream) {
+  GS_NVTX("gs_train");
+  if (!weights || n_samples < 1 || epochs < 0 || max_rows < 1 || max_rows > 1024)
+    return fail(GS_ERR_ARG, "train: bad arguments (1..1024 stage rows per sample)");
+  if (ws_bytes < train_cache_bytes(E, H, max_rows) || !workspace)
+    return fail(GS_ERR_ARG, "train: workspace too small (gs_train_workspace_bytes)");
+  int rc = launch_train(weights, E, H, algo, sched, g, h, row_off, runtime, order, n_samples, epochs, learning_rate,
+                        momentum, static_cast<double*>(workspace), loss_hist, status, (cudaStream_t)stream);
+  if (rc) return fail(GS_ERR_ARG, "train: unsupported network dims (embed, hidden <= 64)");
   CK(cudaGetLastError());
   return GS_OK;
 }

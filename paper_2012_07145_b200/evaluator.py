@@ -18,6 +18,7 @@ import contextlib
 import numpy as np
 import torch
 
+from . import ops  # noqa: F401  (registers torch.ops.gsched)
 from .cut import beam_cut
 from .engine import Scorer
 from .params import DEFAULT_THRESHOLDS
@@ -65,7 +66,8 @@ def scorer_for(graph, params, thresholds, weights) -> Scorer:
     if sc is None or sc.packed.graph is not graph:
         sc = Scorer(graph, params, thresholds)
         _SCORERS[key] = sc
-    sc.set_weights(weights)
+    if weights is not None:
+        sc.set_weights(weights)
     return sc
 
 
@@ -98,13 +100,16 @@ class GpuCostEvaluator(_Base):
         self.thresholds = thresholds or DEFAULT_THRESHOLDS
 
     def _run(self, state, graph):
+        # through the registered custom ops (ops.py): K1 then K2 with the basis
         sc = scorer_for(graph, self.params, self.thresholds, self.weights)
         dec = sc.upload([state])
-        f = sc.featurize(dec)
-        total, rows, gh = sc.cost(f, rows=True, basis=True)
+        h = sc.handle.value
+        feats, row_key, n_rows, verdict, row_src = torch.ops.gsched.featurize(h, dec, sc.R, 1)
+        total, rows, gh = torch.ops.gsched.cost(h, feats, row_key, n_rows, None, True)
         sc.check()
-        n = int(f["n_rows"][0].item())
-        keys = sc.packed.row_keys(f["row_key"][0, :n].cpu().numpy())
+        f = {"feats": feats, "row_key": row_key, "n_rows": n_rows, "verdict": verdict, "row_src": row_src}
+        n = int(n_rows[0].item())
+        keys = sc.packed.row_keys(row_key[0, :n].cpu().numpy())
         return sc, f, n, keys, float(total[0].item()), rows[0, :n].cpu().numpy(), gh[0, :n].cpu().numpy()
 
     def _fill_cache(self, sc, f, n, keys, gh, state, graph):
@@ -137,10 +142,11 @@ class GpuCostEvaluator(_Base):
         """Totals (np.float64[N]) and prune verdicts for a list of states."""
         sc = scorer_for(graph, self.params, self.thresholds, self.weights)
         dec = sc.upload(states)
-        f = sc.featurize(dec)
-        total, _, _ = sc.cost(f)
+        h = sc.handle.value
+        feats, row_key, n_rows, verdict, row_src = torch.ops.gsched.featurize(h, dec, sc.R, 1)
+        total, _, _ = torch.ops.gsched.cost(h, feats, row_key, n_rows, row_src, False)
         sc.check()
-        return total.cpu().numpy(), f["verdict"].cpu().numpy()
+        return total.cpu().numpy(), verdict.cpu().numpy()
 
 
 def gpu_cut(candidates, evaluator, graph, config, pass_index, memo, phase_seed, validate):

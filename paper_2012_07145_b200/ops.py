@@ -92,23 +92,26 @@ def _(handle, dec, R, reuse):
 
 # --------------------------------------------------------------------- cost --
 @torch.library.custom_op("gsched::cost", mutates_args=(), device_types="cuda")
-def cost(handle: int, feats: Tensor, row_key: Tensor, n_rows: Tensor, row_src: Tensor | None) -> tuple[Tensor, Tensor]:
-    """K2: (total f64 [N], row_cost f64 [N, R]).  With row_src the network
-    runs once per distinct row (every row's cost is still returned)."""
+def cost(handle: int, feats: Tensor, row_key: Tensor, n_rows: Tensor, row_src: Tensor | None,
+         basis: bool = False) -> tuple[Tensor, Tensor, Tensor]:
+    """K2: (total f64 [N], row_cost f64 [N, R], basis f64 [N, R, 31] = g[30], h
+    when `basis`, else an empty [0, R, 31]).  With row_src (and no basis) the
+    network runs once per distinct row; every row's cost is still returned."""
     _need_cuda(feats, row_key, n_rows, row_src)
     lib = _lib.load()
     n, R = feats.shape[0], feats.shape[1]
     total = torch.empty((n,), dtype=torch.float64, device=feats.device)
     rc = torch.zeros((n, R), dtype=torch.float64, device=feats.device)   # rows past n_rows stay 0
-    _lib.check(lib.gs_cost(_h(handle), _p(feats), _p(row_key), _p(n_rows), _p(row_src), n, _p(total), _p(rc),
-                           C.c_void_p(0), _st()))
-    return total, rc
+    gh = torch.zeros((n if basis else 0, R, 31), dtype=torch.float64, device=feats.device)
+    _lib.check(lib.gs_cost(_h(handle), _p(feats), _p(row_key), _p(n_rows), None if basis else _p(row_src), n,
+                           _p(total), _p(rc), _p(gh) if basis else C.c_void_p(0), _st()))
+    return total, rc, gh
 
 
 @cost.register_fake
-def _(handle, feats, row_key, n_rows, row_src):
+def _(handle, feats, row_key, n_rows, row_src, basis=False):
     n, R = feats.shape[0], feats.shape[1]
-    return feats.new_empty((n,)), feats.new_empty((n, R))
+    return feats.new_empty((n,)), feats.new_empty((n, R)), feats.new_empty((n if basis else 0, R, 31))
 
 
 # -------------------------------------------------------------- struct_hash --

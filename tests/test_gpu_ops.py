@@ -39,11 +39,12 @@ def test_opcheck_all_ops(small):
     h = sc.handle.value
     feats, row_key, n_rows, verdict, row_src = torch.ops.gsched.featurize(h, dec, sc.R, 1)
     hashes = torch.ops.gsched.struct_hash(h, dec, 2)
-    total, _ = torch.ops.gsched.cost(h, feats, row_key, n_rows, row_src)
+    total, _, _ = torch.ops.gsched.cost(h, feats, row_key, n_rows, row_src)
     rep, _, cnt = torch.ops.gsched.select_reps(hashes, verdict, 11)
     cases = [
         (torch.ops.gsched.featurize.default, (h, dec, sc.R, 1)),
         (torch.ops.gsched.cost.default, (h, feats, row_key, n_rows, row_src)),
+        (torch.ops.gsched.cost.default, (h, feats, row_key, n_rows, None, True)),
         (torch.ops.gsched.struct_hash.default, (h, dec, 3)),
         (torch.ops.gsched.select_reps.default, (hashes, verdict, 11)),
         (torch.ops.gsched.beam_topk.default, (total, hashes, rep, cnt[:1].clone(), None, 2.0, 0.0, 11, 4, 1e-14)),
@@ -69,7 +70,7 @@ def test_ops_equal_direct_calls(small):
     f = sc.featurize(dec)
     t_direct, _, _ = sc.cost(f)
     feats, row_key, n_rows, verdict, row_src = torch.ops.gsched.featurize(h, dec, sc.R, 1)
-    total, _ = torch.ops.gsched.cost(h, feats, row_key, n_rows, row_src)
+    total, _, _ = torch.ops.gsched.cost(h, feats, row_key, n_rows, row_src)
     sc.check()
     assert torch.equal(verdict, f["verdict"]) and torch.equal(n_rows, f["n_rows"])
     for i in range(dec.shape[0]):

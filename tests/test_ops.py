@@ -25,7 +25,10 @@ def test_fake_kernels_infer_shapes():
         assert feats.shape == (1000, 100, 56) and feats.dtype == torch.float64
         assert row_key.shape == row_src.shape == (1000, 100) and row_key.dtype == torch.int32
         assert n_rows.shape == verdict.shape == (1000,) and verdict.dtype == torch.uint8
-        total, rc = torch.ops.gsched.cost(1, feats, row_key, n_rows, row_src)
+        total, rc, gh = torch.ops.gsched.cost(1, feats, row_key, n_rows, row_src)
+        assert gh.shape == (0, 100, 31)
+        _, _, gh = torch.ops.gsched.cost(1, feats, row_key, n_rows, None, True)
+        assert gh.shape == (1000, 100, 31)
         assert total.shape == (1000,) and rc.shape == (1000, 100) and total.dtype == torch.float64
         h = torch.ops.gsched.struct_hash(1, dec, 3)
         assert h.shape == (1000,) and h.dtype == torch.int64
