@@ -281,6 +281,33 @@ int gs_expand_step(gs_pipeline_t p, const GsDecision* parents, int64_t n_parents
                    void* workspace, int64_t ws_bytes, GsDecision* out, int64_t out_cap,
                    int32_t* owner, void* stream);
 
+/* Phase-1 placement menus.  Static per-func facts
+ * the menus need, as the reference defines them (options.py:74-141,
+ * loopnest.py:178-241; pipeline.py:127-134 consumers_of): flags[f] bits
+ * 1 output, 2 single stage, 4 pointwise-called (every consumer reads f
+ * through identity accesses, options.py:74-86), 8 inlinable (not an output,
+ * one stage, no self-read), 16 cheap (ops <= CHEAP_INLINE_OPS); consumers
+ * of f = cons[cons_off[f] .. cons_off[f+1]).  Host pointers; synchronous. */
+int gs_set_placement_info(gs_pipeline_t p, const uint8_t* flags, const int32_t* cons_off,
+                          const int32_t* cons);
+
+/* Every phase-1 candidate of each parent for `func` (search.py:204-220
+ * `_phase1_candidates`): enumerate_compute_locations' menu (compute_root;
+ * fuse_at_block / fuse_at_thread into each scheduled effective consumer in
+ * name order when apply_decision would accept it; inline when cheap, or
+ * alone when single-stage and pointwise-called; compute_root alone for
+ * outputs), restricted to the kinds in restrict_mask (bit per GS_* kind;
+ * 0xF = all; search.py:208-210), fuse_at_block entries crossed with every
+ * serial tiling (options.py:144-162).  The new record is appended after the
+ * parent's last one.  Outputs as gs_expand_step (offsets, out[out_cap][s],
+ * owner).  A parent that already schedules `func` or has no free record
+ * slot raises GS_ERR_SCHEDULE at gs_check.  Workspace:
+ * gs_phase1_workspace_bytes(n). */
+int64_t gs_phase1_workspace_bytes(int64_t n_parents);
+int gs_expand_phase1(gs_pipeline_t p, const GsDecision* parents, int64_t n_parents, int s, int func,
+                     int restrict_mask, const GsTilingMenus* menus, int64_t* offsets, void* workspace,
+                     int64_t ws_bytes, GsDecision* out, int64_t out_cap, int32_t* owner, void* stream);
+
 /* ---- machine oracle ------------------------------
  * The throughput knobs of reference machine.py:26-31 (not hardware limits). */
 typedef struct {

@@ -41,6 +41,12 @@ int64_t expand_workspace_bytes(int64_t n);
 int launch_expand(const GsFunc* funcs, const GsDecision* parents, int64_t n, int S, const int32_t* step,
                   const GsTilingMenus& m, int64_t* offsets, void* ws, int64_t ws_bytes, GsDecision* out,
                   int64_t out_cap, int32_t* owner, int* gerr, int num_sms, cudaStream_t st);
+int serial_count(const GsTilingMenus& m, const GsFunc& fn);
+int64_t phase1_workspace_bytes(int64_t n);
+int launch_phase1(const GsFunc* funcs, int nf, const P1Static& st, const GsDecision* parents, int64_t n, int S,
+                  int func, int restrict_mask, const GsTilingMenus& m, int n_serial, int64_t* offsets, void* ws,
+                  int64_t ws_bytes, GsDecision* out, int64_t out_cap, int32_t* owner, int* gerr, int num_sms,
+                  cudaStream_t st_);
 int64_t train_cache_bytes(int E, int H, int max_rows);
 int model_params(int E, int H);
 int launch_predict(const double* w, int E, int H, const double* algo, const double* sched, const double* cin,
@@ -95,6 +101,10 @@ struct GsPipeline {
   int64_t hcap = 0;
   uint8_t* k1ws = nullptr;       // K1 workspace (see K1Ws)
   int64_t k1cap = 0;
+  uint8_t* p1flags = nullptr;    // phase-1 menus (gs_set_placement_info)
+  int32_t* p1cons_off = nullptr;
+  int16_t* p1cons = nullptr;
+  std::vector<GsFunc> hfuncs;    // host copy of the funcs (menu sizes)
   uint8_t* simbuf = nullptr;     // K6: features, row keys / kernels, n_rows, verdicts (grow-only)
   int64_t simcap = 0;
 };
@@ -188,6 +198,7 @@ int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
   CK(cudaMemcpy(p->dev, &h, sizeof(PipeDev), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&p->blob, h.blob_bytes));
   CK(cudaMemcpy(p->blob, blob.data(), h.blob_bytes, cudaMemcpyHostToDevice));
+  p->hfuncs.assign(d->funcs, d->funcs + h.nf);
   std::vector<int32_t> sof(h.nf);
   for (int f = 0; f < h.nf; ++f) sof[f] = d->funcs[f].stage_begin;
   CK(cudaMalloc(&p->stage_of_func, 4 * h.nf));
@@ -226,6 +237,7 @@ int gs_pipeline_destroy(gs_pipeline_t p) {
   if (!p) return GS_OK;
   cudaFree(p->dev); cudaFree(p->blob); cudaFree(p->stage_of_func); cudaFree(p->algo); cudaFree(p->sorted);
   cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err); cudaFree(p->hscratch); cudaFree(p->k1ws); cudaFree(p->simbuf);
+  cudaFree(p->p1flags); cudaFree(p->p1cons_off); cudaFree(p->p1cons);
   for (double* b : p->wbufs) cudaFree(b);
   delete p;
   return GS_OK;
@@ -630,6 +642,51 @@ int gs_train(double* weights, int E, int H, const double* algo, const double* sc
   int rc = launch_train(weights, E, H, algo, sched, g, h, row_off, runtime, order, n_samples, epochs, learning_rate,
                         momentum, static_cast<double*>(workspace), loss_hist, status, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "train: unsupported network dims (embed, hidden <= 64)");
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
+int gs_set_placement_info(gs_pipeline_t p, const uint8_t* flags, const int32_t* cons_off, const int32_t* cons) {
+  if (!p || !flags || !cons_off) return fail(GS_ERR_ARG, "null argument");
+  const int nf = p->host.nf;
+  const int nc = cons_off[nf];
+  if (cons_off[0] != 0 || nc < 0 || (nc > 0 && !cons)) return fail(GS_ERR_ARG, "bad consumer CSR");
+  std::vector<int16_t> c16(std::max(1, nc));
+  for (int i = 0; i < nc; ++i) {
+    if (cons[i] < 0 || cons[i] >= nf) return fail(GS_ERR_ARG, "consumer index out of range");
+    c16[i] = (int16_t)cons[i];
+  }
+  cudaFree(p->p1flags); cudaFree(p->p1cons_off); cudaFree(p->p1cons);
+  p->p1flags = nullptr; p->p1cons_off = nullptr; p->p1cons = nullptr;
+  CK(cudaMalloc(&p->p1flags, std::max(1, nf)));
+  CK(cudaMemcpy(p->p1flags, flags, nf, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&p->p1cons_off, 4 * (nf + 1)));
+  CK(cudaMemcpy(p->p1cons_off, cons_off, 4 * (nf + 1), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&p->p1cons, 2 * c16.size()));
+  CK(cudaMemcpy(p->p1cons, c16.data(), 2 * c16.size(), cudaMemcpyHostToDevice));
+  return GS_OK;
+}
+
+int64_t gs_phase1_workspace_bytes(int64_t n_parents) { return phase1_workspace_bytes(n_parents); }
+
+int gs_expand_phase1(gs_pipeline_t p, const GsDecision* parents, int64_t n_parents, int s, int func,
+                     int restrict_mask, const GsTilingMenus* menus, int64_t* offsets, void* workspace,
+                     int64_t ws_bytes, GsDecision* out, int64_t out_cap, int32_t* owner, void* stream) {
+  GS_NVTX("gs_expand_phase1");
+  if (!p || !menus || !offsets || s < 1 || n_parents < 0) return fail(GS_ERR_ARG, "bad phase-1 arguments");
+  if (!p->p1flags) return fail(GS_ERR_ARG, "placement info not set (gs_set_placement_info)");
+  if (func < 0 || func >= p->host.nf || p->hfuncs[func].is_external)
+    return fail(GS_ERR_ARG, "func out of range or an external input");
+  const GsTilingMenus& m = *menus;
+  if (m.n_serial_powers < 0 || m.n_serial_powers > 8 || m.n_odd_serial < 0 || m.n_odd_serial > 8 || m.warp_size < 1)
+    return fail(GS_ERR_ARG, "tiling menus out of range");
+  const int nser = serial_count(m, p->hfuncs[func]);
+  P1Static st{p->p1flags, p->p1cons_off, p->p1cons, p->sorted};
+  int rc = launch_phase1(reinterpret_cast<const GsFunc*>(p->blob), p->host.nf, st, parents, n_parents, s, func,
+                         restrict_mask & 0xF, m, nser, offsets, workspace, ws_bytes, out, out_cap, owner, p->err,
+                         p->num_sms, (cudaStream_t)stream);
+  if (rc == -1) return fail(GS_ERR_ARG, "phase 1: more than 2^20 parents or 1024 funcs");
+  if (rc) return fail(GS_ERR_ARG, "phase 1: workspace too small (gs_phase1_workspace_bytes)");
   CK(cudaGetLastError());
   return GS_OK;
 }

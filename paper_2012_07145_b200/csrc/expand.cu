@@ -13,7 +13,7 @@ constexpr int kExpandWarps = 2;
 constexpr int kMaxTilings = 4096;   // per parent (one warp's list in shared memory)
 
 // sorted, de-duplicated serial options of one extent; returns count
-__device__ int serial_opts(const GsTilingMenus& m, int e, int* o) {
+__host__ __device__ int serial_opts(const GsTilingMenus& m, int e, int* o) {
   int n = 0;
   auto add = [&](int v) {
     for (int i = 0; i < n; ++i) if (o[i] == v) return;
@@ -144,6 +144,186 @@ __global__ void __launch_bounds__(kExpandWarps * 32) expand_write_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Phase-1 expansion (search.py:204-220 `_phase1_candidates`): the placement
+// menu of `func` in each parent (options.py:103-141
+// `enumerate_compute_locations`, legality as loopnest.py:178-241
+// `apply_decision`), fuse_at_block entries crossed with every serial tiling
+// (options.py:144-162), parents in order, menus in reference order.
+// Static per-func facts (output, inlinable, pointwise-called, cheap, the
+// consumer lists) are packed at pipeline creation (P1Static).
+// ---------------------------------------------------------------------------
+constexpr int kP1MaxFuncs = 1024;   // dmap capacity per parent (local memory)
+constexpr int kP1MaxMenu = 64;      // menu entries per parent
+
+__device__ int p1_kernel_of(const int8_t* kind, const int16_t* cons, int c, int nf) {
+  for (int it = 0; it <= nf; ++it) {
+    if (c < 0 || kind[c] < 0 || kind[c] == GS_INLINE) return -1;
+    if (kind[c] == GS_ROOT) return c;
+    c = cons[c];
+  }
+  return -1;
+}
+
+// one thread per parent: its menu (kind | consumer << 8 per entry) and
+// candidate count; ndec[p] = the parent's decision count (the new record's slot)
+__global__ void p1_menu_kernel(const GsFunc* __restrict__ funcs, int nf, const P1Static st,
+                               const GsDecision* __restrict__ parents, int64_t n, int S, int func, int restrict_mask,
+                               int n_serial, int32_t* __restrict__ menu, uint8_t* __restrict__ nmenu,
+                               int32_t* __restrict__ ndec, uint32_t* __restrict__ counts, int* __restrict__ gerr) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  int8_t kind[kP1MaxFuncs];
+  int16_t cons[kP1MaxFuncs];
+  for (int f = 0; f < nf; ++f) kind[f] = -1;
+  int nd = 0;
+  const GsDecision* par = parents + p * S;
+  for (; nd < S && par[nd].func != 0xFFFF; ++nd) {
+    const int f = par[nd].func;
+    if (f >= nf) { atomicOr(gerr, 32); counts[p] = 0; nmenu[p] = 0; return; }
+    kind[f] = (int8_t)par[nd].kind;
+    cons[f] = par[nd].consumer == 0xFFFF ? (int16_t)-1 : (int16_t)par[nd].consumer;
+  }
+  ndec[p] = nd;
+  // the new record needs a free slot, and func must be unscheduled (apply_decision)
+  if (nd >= S || kind[func] >= 0) { atomicOr(gerr, 32); counts[p] = 0; nmenu[p] = 0; return; }
+  int32_t* mp = menu + p * kP1MaxMenu;
+  int m = 0;
+  auto add = [&](int k, int c) {
+    if (m < kP1MaxMenu) mp[m] = k | ((c & 0xFFFF) << 8);
+    ++m;
+  };
+  const uint8_t fl = st.flags[func];
+  if (fl & P1_OUTPUT) {
+    add(GS_ROOT, 0xFFFF);
+  } else if ((fl & P1_SINGLE_STAGE) && (fl & P1_POINTWISE_CALLED) && (fl & P1_INLINE_OK)) {
+    add(GS_INLINE, 0xFFFF);
+  } else {
+    add(GS_ROOT, 0xFFFF);
+    // effective consumers: non-inlined funcs reading func, through inlined ones
+    uint32_t eff[kP1MaxFuncs / 32], seen[kP1MaxFuncs / 32];
+    for (int w = 0; w < (nf + 31) / 32; ++w) { eff[w] = 0u; seen[w] = 0u; }
+    int16_t stack[kP1MaxFuncs];
+    int sp = 0;
+    stack[sp++] = (int16_t)func;
+    while (sp > 0) {
+      const int g = stack[--sp];
+      for (int q = st.cons_off[g]; q < st.cons_off[g + 1]; ++q) {
+        const int c = st.cons[q];
+        if (kind[c] == GS_INLINE) {
+          if (!(seen[c >> 5] & (1u << (c & 31)))) { seen[c >> 5] |= 1u << (c & 31); stack[sp++] = (int16_t)c; }
+        } else {
+          eff[c >> 5] |= 1u << (c & 31);
+        }
+      }
+    }
+    int neff = 0;
+    for (int w = 0; w < (nf + 31) / 32; ++w) neff += __popc(eff[w]);
+    for (int r = 0; r < nf; ++r) {   // sorted(effective_consumers) = name order
+      const int c = st.sorted[r];
+      if (!(eff[c >> 5] & (1u << (c & 31)))) continue;
+      if (kind[c] < 0) continue;   // not scheduled yet
+      // fuse_at_block: target scheduled, not inlined, and every effective
+      // consumer in the target's kernel; fuse_at_thread: the only consumer
+      const bool target_ok = kind[c] != GS_INLINE;
+      bool block_ok = target_ok;
+      if (block_ok) {
+        const int kern = p1_kernel_of(kind, cons, c, nf);
+        for (int w = 0; w < (nf + 31) / 32 && block_ok; ++w) {
+          uint32_t bits = eff[w];
+          while (bits && block_ok) {
+            const int o = 32 * w + __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (p1_kernel_of(kind, cons, o, nf) != kern) block_ok = false;
+          }
+        }
+      }
+      if (block_ok) add(GS_FUSE_BLOCK, c);
+      if (target_ok && neff == 1) add(GS_FUSE_THREAD, c);
+    }
+    if ((fl & P1_CHEAP) && (fl & P1_INLINE_OK)) add(GS_INLINE, 0xFFFF);
+  }
+  if (m > kP1MaxMenu) { atomicOr(gerr, 16); counts[p] = 0; nmenu[p] = 0; return; }
+  // restrict_placements (search.py:208-210): keep the allowed kinds, or
+  // compute_root alone when none is allowed
+  if (restrict_mask != 0xF) {
+    int k = 0;
+    for (int i = 0; i < m; ++i) if (restrict_mask & (1 << (mp[i] & 0xFF))) mp[k++] = mp[i];
+    if (k == 0) {
+      for (int i = 0; i < m; ++i) if ((mp[i] & 0xFF) == GS_ROOT) mp[k++] = mp[i];
+    }
+    m = k;
+  }
+  uint32_t cnt = 0;
+  for (int i = 0; i < m; ++i) cnt += (mp[i] & 0xFF) == GS_FUSE_BLOCK ? (uint32_t)n_serial : 1u;
+  nmenu[p] = (uint8_t)m;
+  counts[p] = cnt;
+}
+
+// one warp per parent: each candidate = the parent's records + the new one
+__global__ void __launch_bounds__(kExpandWarps * 32) p1_write_kernel(
+    const GsFunc* __restrict__ funcs, const GsDecision* __restrict__ parents, int64_t n, int S, int func,
+    GsTilingMenus m, const int32_t* __restrict__ menu, const uint8_t* __restrict__ nmenu,
+    const int32_t* __restrict__ ndec, const int64_t* __restrict__ offsets, GsDecision* __restrict__ out,
+    int64_t out_cap, int32_t* __restrict__ owner, int* __restrict__ gerr) {
+  __shared__ uint8_t ser[kExpandWarps][kMaxTilings][4];
+  __shared__ int nser_s[kExpandWarps];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const GsFunc& fn = funcs[func];
+  if (lane == 0) {   // serial tilings of func (enumerate_serial_tilings order)
+    const int nd = fn.ndim;
+    int so[GS_MAX_NDIM][16], sn[GS_MAX_NDIM];
+    for (int d = 0; d < nd; ++d) sn[d] = serial_opts(m, fn.extent[d], so[d]);
+    int idx[GS_MAX_NDIM] = {0, 0, 0, 0}, k = 0;
+    for (;;) {
+      int64_t prod = 1;
+      for (int d = 0; d < nd; ++d) prod *= so[d][idx[d]];
+      if (prod <= m.unroll_budget && k < kMaxTilings) {
+        for (int d = 0; d < GS_MAX_NDIM; ++d) ser[wib][k][d] = (uint8_t)(d < nd ? so[d][idx[d]] : 0);
+        ++k;
+      }
+      int d = nd - 1;
+      while (d >= 0 && ++idx[d] == sn[d]) { idx[d] = 0; --d; }
+      if (d < 0) break;
+    }
+    nser_s[wib] = k;
+  }
+  __syncwarp();
+  const int nser = nser_s[wib];
+  const int64_t nwarps = (int64_t)gridDim.x * kExpandWarps;
+  for (int64_t p = (int64_t)blockIdx.x * kExpandWarps + wib; p < n; p += nwarps) {
+    const int64_t base = offsets[p], cnt = offsets[p + 1] - base;
+    if (cnt <= 0) continue;
+    if (base + cnt > out_cap) { if (lane == 0) atomicOr(gerr, 16); continue; }
+    const uint4* src = reinterpret_cast<const uint4*>(parents + p * S);
+    const int slot = ndec[p];
+    int64_t t = 0;
+    for (int e = 0; e < nmenu[p]; ++e) {
+      const int ent = menu[p * kP1MaxMenu + e];
+      const int k = ent & 0xFF, c = (ent >> 8) & 0xFFFF;
+      const int reps = k == GS_FUSE_BLOCK ? nser : 1;
+      for (int r = 0; r < reps; ++r, ++t) {
+        uint4* dst = reinterpret_cast<uint4*>(out + (base + t) * S);
+        for (int i = lane; i < S; i += 32) {
+          uint4 v = __ldg(src + i);
+          if (i == slot) {
+            GsDecision d;
+            d.func = (uint16_t)func;
+            d.consumer = (uint16_t)c;
+            d.kind = (uint8_t)k;
+            d.flags = k == GS_FUSE_BLOCK ? 1 : 0;
+            for (int q = 0; q < GS_MAX_NDIM; ++q) { d.serial[q] = k == GS_FUSE_BLOCK ? ser[wib][r][q] : 0; d.thread[q] = 0; }
+            d.pad = 0;
+            v = *reinterpret_cast<const uint4*>(&d);
+          }
+          dst[i] = v;
+        }
+        if (owner && lane == 0) owner[base + t] = (int32_t)p;
+      }
+    }
+  }
+}
+
 // offsets[0] = 0, offsets[p + 1] = inclusive prefix of the (u32) counts
 __global__ void expand_offsets_kernel(const uint32_t* __restrict__ incl, int64_t n, int64_t* __restrict__ offsets) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -178,6 +358,58 @@ int launch_expand(const GsFunc* funcs, const GsDecision* parents, int64_t n, int
     cudaFuncSetAttribute(expand_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     expand_write_kernel<<<grid, kExpandWarps * 32, smem, st>>>(funcs, parents, n, S, step, m, offsets, out, out_cap,
                                                                owner, gerr);
+    g_launch_count++;
+  }
+  return 0;
+}
+
+// number of serial tilings of a func (enumerate_serial_tilings), host side
+int serial_count(const GsTilingMenus& m, const GsFunc& fn) {
+  const int nd = fn.ndim;
+  int so[GS_MAX_NDIM][16], sn[GS_MAX_NDIM];
+  for (int d = 0; d < nd; ++d) sn[d] = serial_opts(m, fn.extent[d], so[d]);
+  int idx[GS_MAX_NDIM] = {0, 0, 0, 0}, k = 0;
+  for (;;) {
+    int64_t prod = 1;
+    for (int d = 0; d < nd; ++d) prod *= so[d][idx[d]];
+    if (prod <= m.unroll_budget) ++k;
+    int d = nd - 1;
+    while (d >= 0 && ++idx[d] == sn[d]) { idx[d] = 0; --d; }
+    if (d < 0) break;
+  }
+  return k;
+}
+
+int64_t phase1_workspace_bytes(int64_t n) {
+  if (n < 1) n = 1;
+  return expand_workspace_bytes(n) + (int64_t)(align256(4 * n * kP1MaxMenu) + align256(n) + align256(4 * n));
+}
+
+int launch_phase1(const GsFunc* funcs, int nf, const P1Static& st, const GsDecision* parents, int64_t n, int S,
+                  int func, int restrict_mask, const GsTilingMenus& m, int n_serial, int64_t* offsets, void* ws,
+                  int64_t ws_bytes, GsDecision* out, int64_t out_cap, int32_t* owner, int* gerr, int num_sms,
+                  cudaStream_t st_) {
+  if (n <= 0) { cudaMemsetAsync(offsets, 0, sizeof(int64_t), st_); return 0; }
+  if (n > (int64_t)1 << 20 || nf > kP1MaxFuncs) return -1;
+  if (phase1_workspace_bytes(n) > ws_bytes) return -2;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  uint32_t* counts = reinterpret_cast<uint32_t*>(w);
+  uint32_t* incl = reinterpret_cast<uint32_t*>(w + align256(4 * n));
+  uint32_t* sums = reinterpret_cast<uint32_t*>(w + 2 * align256(4 * n));
+  uint8_t* rest = w + expand_workspace_bytes(n);
+  int32_t* menu = reinterpret_cast<int32_t*>(rest);
+  uint8_t* nmenu = rest + align256(4 * n * kP1MaxMenu);
+  int32_t* ndec = reinterpret_cast<int32_t*>(nmenu + align256(n));
+  p1_menu_kernel<<<(unsigned)((n + 63) / 64), 64, 0, st_>>>(funcs, nf, st, parents, n, S, func, restrict_mask,
+                                                            n_serial, menu, nmenu, ndec, counts, gerr);
+  scan_u32(counts, incl, n, nullptr, true, sums, nullptr, st_);
+  expand_offsets_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st_>>>(incl, n, offsets);
+  g_launch_count += 2;
+  if (out) {
+    const int64_t want = (n + kExpandWarps - 1) / kExpandWarps;
+    const int grid = (int)(want < (int64_t)num_sms * 16 ? want : (int64_t)num_sms * 16);
+    p1_write_kernel<<<grid, kExpandWarps * 32, 0, st_>>>(funcs, parents, n, S, func, m, menu, nmenu, ndec, offsets,
+                                                          out, out_cap, owner, gerr);
     g_launch_count++;
   }
   return 0;

@@ -77,6 +77,17 @@ struct Layout {                 // byte offsets inside dynamic shared memory (K1
   int rcap, pcap, S, R;
 };
 
+// Phase-1 menus (options.py:103-141): static per-func facts, packed by the
+// host from the pipeline (gs_set_placement_info) — the same definitions the
+// reference evaluates per call.
+enum : uint8_t { P1_OUTPUT = 1, P1_SINGLE_STAGE = 2, P1_POINTWISE_CALLED = 4, P1_INLINE_OK = 8, P1_CHEAP = 16 };
+struct P1Static {
+  const uint8_t* flags;      // [nf]
+  const int32_t* cons_off;   // [nf + 1] consumers_of CSR (self-reads excluded)
+  const int16_t* cons;
+  const int32_t* sorted;     // funcs in Python str (name) order
+};
+
 struct NetDev {                 // device copies of the coefficient network (K2)
   int E, H;                     // embed / hidden dims
   const double *algo_w, *algo_b, *sched_w, *sched_b, *head_w, *head_b, *out_w, *out_b;

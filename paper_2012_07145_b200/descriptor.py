@@ -199,6 +199,36 @@ class PackedPipeline:
         d.thresholds.thread_alloc_bytes = int(t.thread_alloc_bytes)
         self.stage_index = {k: i for i, k in enumerate(self.stage_of)}
 
+    def placement_info(self):
+        """Static per-func facts of the phase-1 menus (gs_set_placement_info),
+        with the reference's definitions: consumers_of (pipeline.py:127-134),
+        _is_pointwise_called (options.py:74-86), apply_decision's inline rules
+        (loopnest.py:199-205) and CHEAP_INLINE_OPS = 8 (options.py:22)."""
+        g = self.graph
+        funcs = list(g.funcs)
+        flags = np.zeros(len(funcs), dtype=np.uint8)
+        off, cons = [0], []
+        for fi, f in enumerate(funcs):
+            cs = g.consumers_of(f.name)
+            cons.extend(self.index[c] for c in cs)
+            off.append(len(cons))
+            single = len(f.stages) == 1
+            self_read = any(a.producer == f.name for st in f.stages for a in st.accesses)
+            is_out = f.name in g.outputs
+            found, pointwise = False, True
+            for c in cs:
+                for st in g.func(c).stages:
+                    for a in st.accesses:
+                        if a.producer == f.name:
+                            found = True
+                            if not a.is_pointwise():
+                                pointwise = False
+            ops = sum(sum(st.op_histogram.values()) for st in f.stages)
+            flags[fi] = ((1 if is_out else 0) | (2 if single else 0) | (4 if found and pointwise else 0)
+                         | (8 if (not is_out and single and not self_read and not f.is_external_input) else 0)
+                         | (16 if ops <= 8 else 0))
+        return flags, np.array(off, dtype=np.int32), np.array(cons or [0], dtype=np.int32)
+
     def max_decisions(self) -> int:
         return sum(1 for f in self.graph.funcs if not f.is_external_input)
 

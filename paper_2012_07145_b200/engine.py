@@ -49,6 +49,9 @@ class Scorer:
         with torch.cuda.device(self.device):
             _lib.check(self.lib.gs_pipeline_create(C.byref(self.packed.desc), C.byref(self.handle)))
         self.R = max(1, self.lib.gs_pipeline_max_rows(self.handle))
+        pf, po, pc = self._placement = self.packed.placement_info()
+        _lib.check(self.lib.gs_set_placement_info(self.handle, C.c_void_p(pf.ctypes.data),
+                                                  C.c_void_p(po.ctypes.data), C.c_void_p(pc.ctypes.data)))
         self.S = max(1, self.packed.max_decisions())
         self._weights_key = None
         self.reuse_mode = 1   # gs_set_reuse default
@@ -234,6 +237,31 @@ class Scorer:
         _lib.check(self.lib.gs_expand_step(self.handle, _ptr(parents), P, S, _ptr(steps), C.byref(m),
                                            _ptr(offsets), _ptr(ws), wsb, _ptr(out), total, _ptr(owner),
                                            _stream()))
+        return out, owner[:total], offsets
+
+    def expand_phase1(self, parents: torch.Tensor, func: str, restrict=None, menus=None, total=None):
+        """Every phase-1 candidate of each parent for `func` on the device
+        (search.py:204-220 `_phase1_candidates`): parents uint8 [P, S*16];
+        restrict: the SearchConfig.restrict_placements kinds (None = all).
+        Returns (records [N, S*16], owner int32 [N], offsets int64 [P+1])."""
+        from .descriptor import KIND_CODE, tiling_menus
+        from .gen import Menus
+        P, S = parents.shape[0], parents.shape[1] // 16
+        fi = self.packed.index[func]
+        mask = 0xF if restrict is None else sum(1 << KIND_CODE[k] for k in set(restrict))
+        m = tiling_menus(menus or Menus)
+        wsb = self.lib.gs_phase1_workspace_bytes(P)
+        ws = torch.empty((max(1, wsb),), dtype=torch.uint8, device=self.device)
+        offsets = torch.empty((P + 1,), dtype=torch.int64, device=self.device)
+        if total is None:
+            _lib.check(self.lib.gs_expand_phase1(self.handle, _ptr(parents), P, S, fi, mask, C.byref(m),
+                                                 _ptr(offsets), _ptr(ws), wsb, C.c_void_p(0), 0, C.c_void_p(0),
+                                                 _stream()))
+            total = int(offsets[-1].item())
+        out = torch.empty((total, S * 16), dtype=torch.uint8, device=self.device)
+        owner = torch.empty((max(1, total),), dtype=torch.int32, device=self.device)
+        _lib.check(self.lib.gs_expand_phase1(self.handle, _ptr(parents), P, S, fi, mask, C.byref(m), _ptr(offsets),
+                                             _ptr(ws), wsb, _ptr(out), total, _ptr(owner), _stream()))
         return out, owner[:total], offsets
 
     # -- K4 -------------------------------------------------------------------
