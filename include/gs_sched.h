@@ -289,7 +289,18 @@ int gs_expand_step(gs_pipeline_t p, const GsDecision* parents, int64_t n_parents
  * one stage, no self-read), 16 cheap (ops <= CHEAP_INLINE_OPS); consumers
  * of f = cons[cons_off[f] .. cons_off[f+1]).  Host pointers; synchronous. */
 int gs_set_placement_info(gs_pipeline_t p, const uint8_t* flags, const int32_t* cons_off,
-                          const int32_t* cons);
+                          const int32_t* cons, const int32_t* sched_order, int n_sched);
+
+/* n complete random schedules, candidate i drawn by
+ * default_rng((seed, first + i)) exactly as the reference test suite's
+ * `_random_schedule` (tests/test_acceptance.py:136-160) draws: one menu
+ * entry per func in scheduling order (sched_order of gs_set_placement_info),
+ * a serial tiling for fuse_at_block, then a serial and a thread tiling per
+ * compute_root func.  out: [n][s] records (s >= the schedulable funcs).
+ * This is the §8(d) stress workload generator: independent candidates with
+ * no shared decision structure, generated on the device. */
+int gs_random_schedules(gs_pipeline_t p, uint64_t seed, int64_t first, int64_t n, int s,
+                        const GsTilingMenus* menus, GsDecision* out, void* stream);
 
 /* Every phase-1 candidate of each parent for `func` (search.py:204-220
  * `_phase1_candidates`): enumerate_compute_locations' menu (compute_root;

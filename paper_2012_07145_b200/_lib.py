@@ -22,7 +22,8 @@ EXPORTS = ("gs_last_error", "gs_version", "gs_launch_count", "gs_pipeline_create
            "gs_expand_workspace_bytes", "gs_expand_step", "gs_simulate", "gs_featurize_workspace_bytes",
            "gs_featurize_ws", "gs_struct_hash_workspace_bytes", "gs_struct_hash_ws", "gs_beam_topk_reps",
            "gs_model_params", "gs_predict", "gs_train_workspace_bytes", "gs_train",
-           "gs_set_placement_info", "gs_phase1_workspace_bytes", "gs_expand_phase1")
+           "gs_set_placement_info", "gs_phase1_workspace_bytes", "gs_expand_phase1",
+           "gs_random_schedules")
 
 
 class GsError(RuntimeError):
@@ -67,7 +68,8 @@ def load(path: str = LIB_PATH):
         "gs_featurize_ws": (i32, [P, V, i64, i32, V, V, V, V, V, i64, V, i64, V]),
         "gs_struct_hash_workspace_bytes": (i64, [i64]),
         "gs_model_params": (i32, [i32, i32]),
-        "gs_set_placement_info": (i32, [P, V, V, V]),
+        "gs_set_placement_info": (i32, [P, V, V, V, V, i32]),
+        "gs_random_schedules": (i32, [P, u64, i64, i64, i32, V, V, V]),
         "gs_phase1_workspace_bytes": (i64, [i64]),
         "gs_expand_phase1": (i32, [P, V, i64, i32, i32, i32, V, V, V, i64, V, i64, V, V]),
         "gs_predict": (i32, [V, i32, i32, V, V, V, i64, V, V, V]),

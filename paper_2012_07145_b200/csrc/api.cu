@@ -43,6 +43,9 @@ int launch_expand(const GsFunc* funcs, const GsDecision* parents, int64_t n, int
                   int64_t out_cap, int32_t* owner, int* gerr, int num_sms, cudaStream_t st);
 int serial_count(const GsTilingMenus& m, const GsFunc& fn);
 int64_t phase1_workspace_bytes(int64_t n);
+int launch_random_schedules(const GsFunc* funcs, int nf, const P1Static& st, const int32_t* order, int n_order,
+                            const GsTilingMenus& m, uint64_t seed, int64_t first, int64_t n, int S, GsDecision* out,
+                            int* gerr, cudaStream_t st_);
 int launch_phase1(const GsFunc* funcs, int nf, const P1Static& st, const GsDecision* parents, int64_t n, int S,
                   int func, int restrict_mask, const GsTilingMenus& m, int n_serial, int64_t* offsets, void* ws,
                   int64_t ws_bytes, GsDecision* out, int64_t out_cap, int32_t* owner, int* gerr, int num_sms,
@@ -104,6 +107,8 @@ struct GsPipeline {
   uint8_t* p1flags = nullptr;    // phase-1 menus (gs_set_placement_info)
   int32_t* p1cons_off = nullptr;
   int16_t* p1cons = nullptr;
+  int32_t* p1order = nullptr;    // schedulable funcs, scheduling order
+  int p1norder = 0;
   std::vector<GsFunc> hfuncs;    // host copy of the funcs (menu sizes)
   uint8_t* simbuf = nullptr;     // K6: features, row keys / kernels, n_rows, verdicts (grow-only)
   int64_t simcap = 0;
@@ -237,7 +242,7 @@ int gs_pipeline_destroy(gs_pipeline_t p) {
   if (!p) return GS_OK;
   cudaFree(p->dev); cudaFree(p->blob); cudaFree(p->stage_of_func); cudaFree(p->algo); cudaFree(p->sorted);
   cudaFree(p->names); cudaFree(p->name_off); cudaFree(p->err); cudaFree(p->hscratch); cudaFree(p->k1ws); cudaFree(p->simbuf);
-  cudaFree(p->p1flags); cudaFree(p->p1cons_off); cudaFree(p->p1cons);
+  cudaFree(p->p1flags); cudaFree(p->p1cons_off); cudaFree(p->p1cons); cudaFree(p->p1order);
   for (double* b : p->wbufs) cudaFree(b);
   delete p;
   return GS_OK;
@@ -646,8 +651,11 @@ int gs_train(double* weights, int E, int H, const double* algo, const double* sc
   return GS_OK;
 }
 
-int gs_set_placement_info(gs_pipeline_t p, const uint8_t* flags, const int32_t* cons_off, const int32_t* cons) {
-  if (!p || !flags || !cons_off) return fail(GS_ERR_ARG, "null argument");
+int gs_set_placement_info(gs_pipeline_t p, const uint8_t* flags, const int32_t* cons_off, const int32_t* cons,
+                          const int32_t* sched_order, int n_sched) {
+  if (!p || !flags || !cons_off || (n_sched > 0 && !sched_order) || n_sched < 0) return fail(GS_ERR_ARG, "null argument");
+  for (int i = 0; i < n_sched; ++i)
+    if (sched_order[i] < 0 || sched_order[i] >= p->host.nf) return fail(GS_ERR_ARG, "schedule order out of range");
   const int nf = p->host.nf;
   const int nc = cons_off[nf];
   if (cons_off[0] != 0 || nc < 0 || (nc > 0 && !cons)) return fail(GS_ERR_ARG, "bad consumer CSR");
@@ -664,6 +672,26 @@ int gs_set_placement_info(gs_pipeline_t p, const uint8_t* flags, const int32_t* 
   CK(cudaMemcpy(p->p1cons_off, cons_off, 4 * (nf + 1), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&p->p1cons, 2 * c16.size()));
   CK(cudaMemcpy(p->p1cons, c16.data(), 2 * c16.size(), cudaMemcpyHostToDevice));
+  cudaFree(p->p1order);
+  p->p1order = nullptr;
+  CK(cudaMalloc(&p->p1order, 4 * std::max(1, n_sched)));
+  if (n_sched) CK(cudaMemcpy(p->p1order, sched_order, 4 * n_sched, cudaMemcpyHostToDevice));
+  p->p1norder = n_sched;
+  return GS_OK;
+}
+
+int gs_random_schedules(gs_pipeline_t p, uint64_t seed, int64_t first, int64_t n, int s, const GsTilingMenus* menus,
+                        GsDecision* out, void* stream) {
+  GS_NVTX("gs_random_schedules");
+  if (!p || !menus || !out || s < 1 || n < 0 || first < 0) return fail(GS_ERR_ARG, "bad random-schedule arguments");
+  if (!p->p1flags) return fail(GS_ERR_ARG, "placement info not set (gs_set_placement_info)");
+  if (s < p->p1norder) return fail(GS_ERR_ARG, "record stride below the number of schedulable funcs");
+  P1Static st{p->p1flags, p->p1cons_off, p->p1cons, p->sorted};
+  const int rc = launch_random_schedules(reinterpret_cast<const GsFunc*>(p->blob), p->host.nf, st, p->p1order,
+                                        p->p1norder, *menus, seed, first, n, s, out, p->err, (cudaStream_t)stream);
+  if (rc == -3) return fail(GS_ERR_CUDA, "random schedules: could not raise the per-thread stack limit");
+  if (rc) return fail(GS_ERR_ARG, "random schedules: more than 512 funcs");
+  CK(cudaGetLastError());
   return GS_OK;
 }
 
@@ -685,7 +713,8 @@ int gs_expand_phase1(gs_pipeline_t p, const GsDecision* parents, int64_t n_paren
   int rc = launch_phase1(reinterpret_cast<const GsFunc*>(p->blob), p->host.nf, st, parents, n_parents, s, func,
                          restrict_mask & 0xF, m, nser, offsets, workspace, ws_bytes, out, out_cap, owner, p->err,
                          p->num_sms, (cudaStream_t)stream);
-  if (rc == -1) return fail(GS_ERR_ARG, "phase 1: more than 2^20 parents or 1024 funcs");
+  if (rc == -1) return fail(GS_ERR_ARG, "phase 1: more than 2^20 parents or 512 funcs");
+  if (rc == -3) return fail(GS_ERR_CUDA, "phase 1: could not raise the per-thread stack limit");
   if (rc) return fail(GS_ERR_ARG, "phase 1: workspace too small (gs_phase1_workspace_bytes)");
   CK(cudaGetLastError());
   return GS_OK;

@@ -6,6 +6,7 @@
 // not the expanded candidate records.
 #include "gs_internal.cuh"
 #include "scan.cuh"
+#include "rng.cuh"
 
 namespace gs {
 
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(kExpandWarps * 32) expand_write_kernel(
 // Static per-func facts (output, inlinable, pointwise-called, cheap, the
 // consumer lists) are packed at pipeline creation (P1Static).
 // ---------------------------------------------------------------------------
-constexpr int kP1MaxFuncs = 1024;   // dmap capacity per parent (local memory)
+constexpr int kP1MaxFuncs = 512;    // funcs per pipeline for the menus (per-thread local arrays)
 constexpr int kP1MaxMenu = 64;      // menu entries per parent
 
 __device__ int p1_kernel_of(const int8_t* kind, const int16_t* cons, int c, int nf) {
@@ -165,29 +166,15 @@ __device__ int p1_kernel_of(const int8_t* kind, const int16_t* cons, int c, int 
   return -1;
 }
 
-// one thread per parent: its menu (kind | consumer << 8 per entry) and
-// candidate count; ndec[p] = the parent's decision count (the new record's slot)
-__global__ void p1_menu_kernel(const GsFunc* __restrict__ funcs, int nf, const P1Static st,
-                               const GsDecision* __restrict__ parents, int64_t n, int S, int func, int restrict_mask,
-                               int n_serial, int32_t* __restrict__ menu, uint8_t* __restrict__ nmenu,
-                               int32_t* __restrict__ ndec, uint32_t* __restrict__ counts, int* __restrict__ gerr) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  int8_t kind[kP1MaxFuncs];
-  int16_t cons[kP1MaxFuncs];
-  for (int f = 0; f < nf; ++f) kind[f] = -1;
-  int nd = 0;
-  const GsDecision* par = parents + p * S;
-  for (; nd < S && par[nd].func != 0xFFFF; ++nd) {
-    const int f = par[nd].func;
-    if (f >= nf) { atomicOr(gerr, 32); counts[p] = 0; nmenu[p] = 0; return; }
-    kind[f] = (int8_t)par[nd].kind;
-    cons[f] = par[nd].consumer == 0xFFFF ? (int16_t)-1 : (int16_t)par[nd].consumer;
-  }
-  ndec[p] = nd;
-  // the new record needs a free slot, and func must be unscheduled (apply_decision)
-  if (nd >= S || kind[func] >= 0) { atomicOr(gerr, 32); counts[p] = 0; nmenu[p] = 0; return; }
-  int32_t* mp = menu + p * kP1MaxMenu;
+// The placement menu of `func` in a state (kind / consumer per func, -1 =
+// unscheduled): entries kind | consumer << 8 in reference order, restricted
+// to restrict_mask (search.py:208-210).  Returns the entry count, or -1 when
+// it exceeds kP1MaxMenu.  Kept out of line: inlined into rand_sched_kernel,
+// its bitmask arrays were given the caller's menu-array stack slots (the
+// menu's first entry came back overwritten; memcheck saw local accesses out
+// of bounds) with nvcc 12.9 -O3.
+__device__ __noinline__ int p1_menu(const P1Static& st, int nf, int func, const int8_t* kind, const int16_t* cons,
+                       int restrict_mask, int32_t* mp) {
   int m = 0;
   auto add = [&](int k, int c) {
     if (m < kP1MaxMenu) mp[m] = k | ((c & 0xFFFF) << 8);
@@ -201,19 +188,32 @@ __global__ void p1_menu_kernel(const GsFunc* __restrict__ funcs, int nf, const P
   } else {
     add(GS_ROOT, 0xFFFF);
     // effective consumers: non-inlined funcs reading func, through inlined ones
-    uint32_t eff[kP1MaxFuncs / 32], seen[kP1MaxFuncs / 32];
-    for (int w = 0; w < (nf + 31) / 32; ++w) { eff[w] = 0u; seen[w] = 0u; }
-    int16_t stack[kP1MaxFuncs];
-    int sp = 0;
-    stack[sp++] = (int16_t)func;
-    while (sp > 0) {
-      const int g = stack[--sp];
-      for (int q = st.cons_off[g]; q < st.cons_off[g + 1]; ++q) {
-        const int c = st.cons[q];
-        if (kind[c] == GS_INLINE) {
-          if (!(seen[c >> 5] & (1u << (c & 31)))) { seen[c >> 5] |= 1u << (c & 31); stack[sp++] = (int16_t)c; }
-        } else {
-          eff[c >> 5] |= 1u << (c & 31);
+    // (breadth-first over bitmask frontiers: no per-thread stack)
+    constexpr int NW = kP1MaxFuncs / 32;
+    uint32_t eff[NW], seen[NW], front[NW];
+    const int nw = (nf + 31) / 32;
+    for (int w = 0; w < nw; ++w) { eff[w] = 0u; seen[w] = 0u; front[w] = 0u; }
+    front[func >> 5] = 1u << (func & 31);
+    for (bool more = true; more;) {
+      more = false;
+      for (int w = 0; w < nw; ++w) {
+        uint32_t bits = front[w];
+        front[w] = 0u;
+        while (bits) {
+          const int g = 32 * w + __ffs(bits) - 1;
+          bits &= bits - 1;
+          for (int q = st.cons_off[g]; q < st.cons_off[g + 1]; ++q) {
+            const int c = st.cons[q];
+            if (kind[c] == GS_INLINE) {
+              if (!(seen[c >> 5] & (1u << (c & 31)))) {
+                seen[c >> 5] |= 1u << (c & 31);
+                front[c >> 5] |= 1u << (c & 31);
+                more = true;
+              }
+            } else {
+              eff[c >> 5] |= 1u << (c & 31);
+            }
+          }
         }
       }
     }
@@ -243,9 +243,7 @@ __global__ void p1_menu_kernel(const GsFunc* __restrict__ funcs, int nf, const P
     }
     if ((fl & P1_CHEAP) && (fl & P1_INLINE_OK)) add(GS_INLINE, 0xFFFF);
   }
-  if (m > kP1MaxMenu) { atomicOr(gerr, 16); counts[p] = 0; nmenu[p] = 0; return; }
-  // restrict_placements (search.py:208-210): keep the allowed kinds, or
-  // compute_root alone when none is allowed
+  if (m > kP1MaxMenu) return -1;
   if (restrict_mask != 0xF) {
     int k = 0;
     for (int i = 0; i < m; ++i) if (restrict_mask & (1 << (mp[i] & 0xFF))) mp[k++] = mp[i];
@@ -254,6 +252,34 @@ __global__ void p1_menu_kernel(const GsFunc* __restrict__ funcs, int nf, const P
     }
     m = k;
   }
+  return m;
+}
+
+// one thread per parent: its menu and candidate count; ndec[p] = the
+// parent's decision count (the new record's slot)
+__global__ void p1_menu_kernel(const GsFunc* __restrict__ funcs, int nf, const P1Static st,
+                               const GsDecision* __restrict__ parents, int64_t n, int S, int func, int restrict_mask,
+                               int n_serial, int32_t* __restrict__ menu, uint8_t* __restrict__ nmenu,
+                               int32_t* __restrict__ ndec, uint32_t* __restrict__ counts, int* __restrict__ gerr) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  int8_t kind[kP1MaxFuncs];
+  int16_t cons[kP1MaxFuncs];
+  for (int f = 0; f < nf; ++f) kind[f] = -1;
+  int nd = 0;
+  const GsDecision* par = parents + p * S;
+  for (; nd < S && par[nd].func != 0xFFFF; ++nd) {
+    const int f = par[nd].func;
+    if (f >= nf) { atomicOr(gerr, 32); counts[p] = 0; nmenu[p] = 0; return; }
+    kind[f] = (int8_t)par[nd].kind;
+    cons[f] = par[nd].consumer == 0xFFFF ? (int16_t)-1 : (int16_t)par[nd].consumer;
+  }
+  ndec[p] = nd;
+  // the new record needs a free slot, and func must be unscheduled (apply_decision)
+  if (nd >= S || kind[func] >= 0) { atomicOr(gerr, 32); counts[p] = 0; nmenu[p] = 0; return; }
+  int32_t* mp = menu + p * kP1MaxMenu;
+  const int m = p1_menu(st, nf, func, kind, cons, restrict_mask, mp);
+  if (m < 0) { atomicOr(gerr, 16); counts[p] = 0; nmenu[p] = 0; return; }
   uint32_t cnt = 0;
   for (int i = 0; i < m; ++i) cnt += (mp[i] & 0xFF) == GS_FUSE_BLOCK ? (uint32_t)n_serial : 1u;
   nmenu[p] = (uint8_t)m;
@@ -324,6 +350,113 @@ __global__ void __launch_bounds__(kExpandWarps * 32) p1_write_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Random complete schedules (the reference test-suite's `_random_schedule`,
+// tests/test_acceptance.py:136-160): candidate i walks the schedulable funcs
+// with its own default_rng((seed, first + i)) — a menu draw per func, a
+// serial draw for fuse_at_block, then a serial and a thread tiling draw per
+// compute_root func — exactly the reference's draw sequence, so each
+// candidate equals `_random_schedule(graph, default_rng((seed, i)))`.
+// ---------------------------------------------------------------------------
+__device__ int nth_serial(const GsTilingMenus& m, const GsFunc& fn, int want, int* sv) {
+  const int nd = fn.ndim;
+  int so[GS_MAX_NDIM][16], sn[GS_MAX_NDIM];
+  for (int d = 0; d < nd; ++d) sn[d] = serial_opts(m, fn.extent[d], so[d]);
+  int idx[GS_MAX_NDIM] = {0, 0, 0, 0}, k = 0;
+  for (;;) {
+    int64_t prod = 1;
+    for (int d = 0; d < nd; ++d) prod *= so[d][idx[d]];
+    if (prod <= m.unroll_budget) {
+      if (k == want && sv) for (int d = 0; d < nd; ++d) sv[d] = so[d][idx[d]];
+      ++k;
+    }
+    int d = nd - 1;
+    while (d >= 0 && ++idx[d] == sn[d]) { idx[d] = 0; --d; }
+    if (d < 0) break;
+  }
+  return k;
+}
+
+// enumerate_thread_tilings(post) (options.py:165-183): count, and the
+// want-th vector (last dim fastest)
+__device__ int nth_thread(const GsTilingMenus& m, const int* post, int nd, int want, int* tv) {
+  int inner = -1;
+  for (int d = 0; d < nd; ++d) if (post[d] >= 16) { inner = d; break; }
+  if (inner < 0) inner = 0;
+  int to[GS_MAX_NDIM][16], tn[GS_MAX_NDIM];
+  int total = 1;
+  for (int d = 0; d < nd; ++d) { tn[d] = thread_opts(m, post[d], d == inner, to[d]); total *= tn[d]; }
+  if (tv && want < total) {
+    int r = want;
+    for (int d = nd - 1; d >= 0; --d) { tv[d] = to[d][r % tn[d]]; r /= tn[d]; }
+  }
+  return total;
+}
+
+__global__ void rand_sched_kernel(const GsFunc* __restrict__ funcs, int nf, const P1Static st,
+                                  const int32_t* __restrict__ order, int n_order, GsTilingMenus m, uint64_t seed,
+                                  int64_t first, int64_t n, int S, GsDecision* __restrict__ out,
+                                  int* __restrict__ gerr) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  Pcg64 g;
+  seed_pair(g, seed, (uint64_t)(first + c));
+  int8_t kind[kP1MaxFuncs];
+  int16_t cons[kP1MaxFuncs];
+  int16_t rec[kP1MaxFuncs];
+  for (int f = 0; f < nf; ++f) kind[f] = -1;
+  GsDecision* o = out + c * S;
+  int32_t mp[kP1MaxMenu];
+  int nd = 0;
+  for (int i = 0; i < n_order; ++i) {
+    const int func = order[i];
+    const int len = p1_menu(st, nf, func, kind, cons, 0xF, mp);
+    if (len <= 0 || nd >= S) { atomicOr(gerr, len < 0 ? 16 : 32); return; }
+    const uint32_t pick = g.integers((uint32_t)len);
+    const int e = mp[pick];
+
+    const int k = e & 0xFF, tgt = (e >> 8) & 0xFFFF;
+    GsDecision d;
+    d.func = (uint16_t)func;
+    d.kind = (uint8_t)k;
+    d.consumer = (k == GS_FUSE_BLOCK || k == GS_FUSE_THREAD) ? (uint16_t)tgt : (uint16_t)0xFFFF;
+    d.flags = 0;
+    d.pad = 0;
+    for (int q = 0; q < GS_MAX_NDIM; ++q) { d.serial[q] = 0; d.thread[q] = 0; }
+    if (k == GS_FUSE_BLOCK) {
+      int sv[GS_MAX_NDIM];
+      const int ns = nth_serial(m, funcs[func], -1, nullptr);
+      nth_serial(m, funcs[func], (int)g.integers((uint32_t)ns), sv);
+      for (int q = 0; q < funcs[func].ndim; ++q) d.serial[q] = (uint8_t)sv[q];
+      d.flags = 1;
+    }
+    o[nd] = d;
+    rec[func] = (int16_t)nd++;
+    kind[func] = (int8_t)k;
+    cons[func] = d.consumer == 0xFFFF ? (int16_t)-1 : (int16_t)d.consumer;
+  }
+  for (int i = 0; i < n_order; ++i) {   // deferred root tilings, scheduling order
+    const int func = order[i];
+    if (kind[func] != GS_ROOT) continue;
+    const GsFunc& fn = funcs[func];
+    int sv[GS_MAX_NDIM], tv[GS_MAX_NDIM], post[GS_MAX_NDIM];
+    const int ns = nth_serial(m, fn, -1, nullptr);
+    nth_serial(m, fn, (int)g.integers((uint32_t)ns), sv);
+    for (int q = 0; q < fn.ndim; ++q) post[q] = (fn.extent[q] + sv[q] - 1) / sv[q];
+    const int nt = nth_thread(m, post, fn.ndim, -1, nullptr);
+    nth_thread(m, post, fn.ndim, (int)g.integers((uint32_t)nt), tv);
+    GsDecision& d = o[rec[func]];
+    for (int q = 0; q < fn.ndim; ++q) { d.serial[q] = (uint8_t)sv[q]; d.thread[q] = (uint8_t)tv[q]; }
+    d.flags = 3;
+  }
+  for (int i = nd; i < S; ++i) {
+    GsDecision d;
+    d.func = 0xFFFF; d.consumer = 0xFFFF; d.kind = 0; d.flags = 0; d.pad = 0;
+    for (int q = 0; q < GS_MAX_NDIM; ++q) { d.serial[q] = 0; d.thread[q] = 0; }
+    o[i] = d;
+  }
+}
+
 // offsets[0] = 0, offsets[p + 1] = inclusive prefix of the (u32) counts
 __global__ void expand_offsets_kernel(const uint32_t* __restrict__ incl, int64_t n, int64_t* __restrict__ offsets) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -380,6 +513,19 @@ int serial_count(const GsTilingMenus& m, const GsFunc& fn) {
   return k;
 }
 
+// The menu kernels keep per-thread state in local arrays (a few KB of stack
+// frame, p1_menu's in an out-of-line call): make sure the per-thread stack
+// limit covers the kernel's local size.  Raised once, before first use.
+static int ensure_stack(const void* kernel) {
+  cudaFuncAttributes a;
+  if (cudaFuncGetAttributes(&a, kernel) != cudaSuccess) return -1;
+  size_t cur = 0;
+  if (cudaDeviceGetLimit(&cur, cudaLimitStackSize) != cudaSuccess) return -1;
+  const size_t need = (a.localSizeBytes + 1023) & ~(size_t)1023;
+  if (cur < need && cudaDeviceSetLimit(cudaLimitStackSize, need) != cudaSuccess) return -1;
+  return 0;
+}
+
 int64_t phase1_workspace_bytes(int64_t n) {
   if (n < 1) n = 1;
   return expand_workspace_bytes(n) + (int64_t)(align256(4 * n * kP1MaxMenu) + align256(n) + align256(4 * n));
@@ -400,6 +546,8 @@ int launch_phase1(const GsFunc* funcs, int nf, const P1Static& st, const GsDecis
   int32_t* menu = reinterpret_cast<int32_t*>(rest);
   uint8_t* nmenu = rest + align256(4 * n * kP1MaxMenu);
   int32_t* ndec = reinterpret_cast<int32_t*>(nmenu + align256(n));
+  static bool stack_ok = false;
+  if (!stack_ok) { if (ensure_stack((const void*)p1_menu_kernel)) return -3; stack_ok = true; }
   p1_menu_kernel<<<(unsigned)((n + 63) / 64), 64, 0, st_>>>(funcs, nf, st, parents, n, S, func, restrict_mask,
                                                             n_serial, menu, nmenu, ndec, counts, gerr);
   scan_u32(counts, incl, n, nullptr, true, sums, nullptr, st_);
@@ -412,6 +560,19 @@ int launch_phase1(const GsFunc* funcs, int nf, const P1Static& st, const GsDecis
                                                           out, out_cap, owner, gerr);
     g_launch_count++;
   }
+  return 0;
+}
+
+int launch_random_schedules(const GsFunc* funcs, int nf, const P1Static& st, const int32_t* order, int n_order,
+                            const GsTilingMenus& m, uint64_t seed, int64_t first, int64_t n, int S, GsDecision* out,
+                            int* gerr, cudaStream_t st_) {
+  if (n <= 0) return 0;
+  if (nf > kP1MaxFuncs) return -1;
+  static bool stack_ok = false;
+  if (!stack_ok) { if (ensure_stack((const void*)rand_sched_kernel)) return -3; stack_ok = true; }
+  rand_sched_kernel<<<(unsigned)((n + 63) / 64), 64, 0, st_>>>(funcs, nf, st, order, n_order, m, seed, first, n, S,
+                                                               out, gerr);
+  g_launch_count++;
   return 0;
 }
 

@@ -227,7 +227,9 @@ class PackedPipeline:
             flags[fi] = ((1 if is_out else 0) | (2 if single else 0) | (4 if found and pointwise else 0)
                          | (8 if (not is_out and single and not self_read and not f.is_external_input) else 0)
                          | (16 if ops <= 8 else 0))
-        return flags, np.array(off, dtype=np.int32), np.array(cons or [0], dtype=np.int32)
+        order = np.array([self.index[f] for f in reversed(g.topo_order)
+                          if not g.func(f).is_external_input], dtype=np.int32)
+        return flags, np.array(off, dtype=np.int32), np.array(cons or [0], dtype=np.int32), order
 
     def max_decisions(self) -> int:
         return sum(1 for f in self.graph.funcs if not f.is_external_input)

@@ -49,9 +49,10 @@ class Scorer:
         with torch.cuda.device(self.device):
             _lib.check(self.lib.gs_pipeline_create(C.byref(self.packed.desc), C.byref(self.handle)))
         self.R = max(1, self.lib.gs_pipeline_max_rows(self.handle))
-        pf, po, pc = self._placement = self.packed.placement_info()
+        pf, po, pc, porder = self._placement = self.packed.placement_info()
         _lib.check(self.lib.gs_set_placement_info(self.handle, C.c_void_p(pf.ctypes.data),
-                                                  C.c_void_p(po.ctypes.data), C.c_void_p(pc.ctypes.data)))
+                                                  C.c_void_p(po.ctypes.data), C.c_void_p(pc.ctypes.data),
+                                                  C.c_void_p(porder.ctypes.data), len(porder)))
         self.S = max(1, self.packed.max_decisions())
         self._weights_key = None
         self.reuse_mode = 1   # gs_set_reuse default
@@ -263,6 +264,19 @@ class Scorer:
         _lib.check(self.lib.gs_expand_phase1(self.handle, _ptr(parents), P, S, fi, mask, C.byref(m), _ptr(offsets),
                                              _ptr(ws), wsb, _ptr(out), total, _ptr(owner), _stream()))
         return out, owner[:total], offsets
+
+    def random_schedules(self, n: int, seed: int, first: int = 0, menus=None) -> torch.Tensor:
+        """n complete random schedules generated on the device; candidate i
+        equals the reference `_random_schedule(graph, default_rng((seed,
+        first + i)))` (tests/test_acceptance.py:136-160).  Returns uint8
+        [n, S*16] decision records."""
+        from .descriptor import tiling_menus
+        from .gen import Menus
+        m = tiling_menus(menus or Menus)
+        out = torch.empty((n, self.S * 16), dtype=torch.uint8, device=self.device)
+        _lib.check(self.lib.gs_random_schedules(self.handle, C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), first, n, self.S,
+                                                C.byref(m), _ptr(out), _stream()))
+        return out
 
     # -- K4 -------------------------------------------------------------------
     def select(self, hashes: torch.Tensor, verdict: torch.Tensor, phase_seed: int, rejects=True):

@@ -7,9 +7,12 @@ func in scheduling order, the reference `_phase1_candidates` (search.py:204-220
 over options.py:103-162 and loopnest.py:178-241) of up to 6 beam states,
 then a random subset of the candidates becomes the next beam.  Two
 configurations: unrestricted, and the freeze pre-pass's
-restrict_placements=("compute_root", "inline") (search.py:329).
+restrict_placements=("compute_root", "inline") (search.py:329).  Plus the
+reference test suite's `_random_schedule(graph, default_rng((1234, i)))`
+(tests/test_acceptance.py:136-160) for i < 48 — what gs_random_schedules
+must reproduce.
 Output: phase1.json.gz — per pipeline: text + phases (func, restrict,
-parents and candidates as schedule_dump lines)."""
+parents and candidates as schedule_dump lines) + random schedules."""
 
 from __future__ import annotations
 
@@ -29,6 +32,7 @@ sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
 from gpusched.loopnest import initial_state, schedule_dump  # noqa: E402
 from gpusched.pipeline import parse_pipeline  # noqa: E402
 from gpusched.search import SearchConfig, _phase1_candidates  # noqa: E402
+from test_acceptance import _random_schedule  # noqa: E402
 
 NAMES = ("diamond", "tiny_fork", "chain3", "stencil_chain", "chain20", "unsharp", "harris", "camera_pipe",
          "local_laplacian", "resnet_small", "blur", "conv")
@@ -59,7 +63,8 @@ def main():
         base = SearchConfig(seed=0)
         phases = walk(graph, base, rng) + walk(graph, replace(base, restrict_placements=("compute_root", "inline")),
                                                rng)
-        out[name] = {"pipeline": text, "phases": phases}
+        rand = [schedule_dump(_random_schedule(graph, np.random.default_rng((1234, i)))) for i in range(48)]
+        out[name] = {"pipeline": text, "phases": phases, "random_seed": 1234, "random": rand}
         print(name, len(phases), "phases,", sum(len(p["candidates"]) for p in phases), "candidates")
     with gzip.open(os.path.join(HERE, "phase1.json.gz"), "wt") as fh:
         json.dump(out, fh)

@@ -71,3 +71,23 @@ def test_phase1_errors(gold):
         sc.check()
     with pytest.raises((GsError, KeyError)):
         sc.expand_phase1(pd, "no_such_func")
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_random_schedules_match_reference(gold, name):
+    """gs_random_schedules(seed, i) == the reference `_random_schedule(graph,
+    default_rng((seed, i)))`, record for record."""
+    from paper_2012_07145_b200.engine import Scorer
+    from paper_2012_07145_b200.pipeline import parse_pipeline
+    from paper_2012_07145_b200.schedule import parse_dump
+    g = gold[name]
+    graph = parse_pipeline(g["pipeline"], name)
+    sc = Scorer(graph, PARAMS)
+    want = sc.packed.pack([parse_dump(t) for t in g["random"]], sc.S)
+    out = sc.random_schedules(len(g["random"]), g["random_seed"])
+    sc.check()
+    got = out.cpu().numpy().view(want.dtype).reshape(want.shape)
+    assert np.array_equal(got, want), name
+    # a later window of the same stream
+    tail = sc.random_schedules(8, g["random_seed"], first=40)
+    assert np.array_equal(tail.cpu().numpy().view(want.dtype).reshape(8, -1), want[40:48])
