@@ -85,20 +85,20 @@ def _ref_import():
 _W = {}
 
 
-def _worker_init(kind, text, rows, barrier):
+def _worker_init(kind, text, rows, barrier, name="chain100"):
     _W["kind"], _W["rows"], _W["barrier"] = kind, rows, barrier
     if kind == "reference":
         import gpusched
         from gpusched.costmodel import init_weights
         from gpusched.loopnest import Decision, apply_decision, initial_state
         from gpusched.machine import MachineParams
-        g = gpusched.parse_pipeline(text, "chain100")
+        g = gpusched.parse_pipeline(text, name)
         _W.update(g=g, w=init_weights(0), p=MachineParams(), D=Decision, ap=apply_decision,
                   init=initial_state)
     else:
         from paper_2012_07145_b200.params import MachineParams, init_weights
         from paper_2012_07145_b200.pipeline import parse_pipeline
-        _W.update(g=parse_pipeline(text, "chain100"), w=init_weights(0).tensors, p=MachineParams())
+        _W.update(g=parse_pipeline(text, name), w=init_weights(0).tensors, p=MachineParams())
 
 
 def _states(recs):
@@ -149,14 +149,15 @@ def _worker_run(chunk):
     return len(cands), time.perf_counter() - t0
 
 
-def cpu_reference(graph, recs, seconds=15.0, cores=None):
+def cpu_reference(graph, recs, seconds=15.0, cores=None, per_sec=9.0):
     """Score a bounded, evenly strided sample of the same candidates with the
     CPU reference on all host cores (fork pool, fresh evaluator per
-    candidate).  Returns (cand/s, cores, kind, sample description)."""
+    candidate).  Returns (cand/s, cores, kind, sample description).
+    per_sec: the expected candidates/s per core (sizes the sample)."""
     from paper_2012_07145_b200.pipeline import graph_to_text
     kind = _ref_import()
     cores = cores or os.cpu_count() or 1
-    per_core = max(4, int(seconds * 9))          # ~10 cand/s/core at R = 100
+    per_core = max(4, int(seconds * per_sec))    # ~10 cand/s/core at R = 100
     n = min(len(recs), per_core * cores)
     idx = np.linspace(0, len(recs) - 1, n).astype(np.int64)
     sample = recs[idx]
@@ -165,7 +166,7 @@ def cpu_reference(graph, recs, seconds=15.0, cores=None):
     ctx = mp.get_context("fork")
     barrier = ctx.Barrier(len(chunks))
     with ctx.Pool(len(chunks), initializer=_worker_init,
-                  initargs=(kind, graph_to_text(graph), sample, barrier)) as pool:
+                  initargs=(kind, graph_to_text(graph), sample, barrier, graph.name)) as pool:
         res = pool.map(_worker_run, chunks, chunksize=1)
     done = sum(r[0] for r in res)
     wall = max(r[1] for r in res)

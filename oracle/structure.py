@@ -221,6 +221,22 @@ class PCG64:
             a[i], a[j] = a[j], a[i]
         return a
 
+    def integers(self, n: int) -> int:
+        """Generator.integers(n) for 1 <= n < 2**32: Lemire's bounded
+        rejection on next_uint32 (numpy distributions.c
+        buffered_bounded_lemire_uint32); no draw when n == 1."""
+        rng = n - 1
+        if rng == 0:
+            return 0
+        m = self.next32() * n
+        lo = m & 0xFFFFFFFF
+        if lo < n:
+            th = (0xFFFFFFFF - rng) % n
+            while lo < th:
+                m = self.next32() * n
+                lo = m & 0xFFFFFFFF
+        return m >> 32
+
     def next_double(self) -> float:
         return (self.next64() >> 11) * (1.0 / 9007199254740992.0)
 

@@ -56,8 +56,9 @@ class StepPlan:
     candidate (search.py:142-150)."""
 
     def __init__(self, scorer, n, world, rank, pass_index, phase_seed, beam, penalty, num_passes,
-                 tie_band, sampling=True, group=None):
+                 tie_band, sampling=True, group=None, reuse=2):
         self.sc, self.n, self.world, self.rank = scorer, n, world, rank
+        self.reuse = reuse   # K1 sibling reuse: 2 (computed rows only, the default), 1, or 0 (every row)
         self.pass_index, self.phase_seed, self.beam = pass_index, phase_seed, beam
         self.penalty, self.num_passes, self.tie_band = penalty, num_passes, tie_band
         self.sampling, self.group = sampling, group
@@ -70,12 +71,12 @@ class StepPlan:
         # the cut consumes features only through K2 with row_src, so K1
         # writes just the computed rows (reuse mode 2)
         prev = self.sc.reuse_mode
-        if prev != 2:
-            self.sc.set_reuse(2)
+        if prev != self.reuse:
+            self.sc.set_reuse(self.reuse)
         try:
             return self._features_into(d)
         finally:
-            if prev != 2:
+            if prev != self.reuse:
                 self.sc.set_reuse(prev)
 
     def _features_into(self, d):
@@ -126,7 +127,7 @@ class StepPlan:
         mark()
         f = self._features(d)
         mark()
-        total, _, _ = sc.cost(f, scratch=self.rcbuf)
+        total, _, _ = sc.cost(f, scratch=self.rcbuf, reuse=self.reuse != 0)
         mark()
         verdict = f["verdict"]
         rej = None

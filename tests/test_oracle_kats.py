@@ -104,3 +104,16 @@ def test_gumbel_replica():
     g = structure.PCG64((71, 0x657870))
     got = [g.gumbel() for _ in range(300)]
     assert np.array_equal(np.asarray(got), want)
+
+
+def test_pcg64_integers_replica():
+    """Generator.integers(n) (the `_random_schedule` draws that
+    gs_random_schedules reproduces on the device), interleaved sizes
+    including 1 (no draw) and sizes near 2**32."""
+    rng = np.random.default_rng(5)
+    for seed in range(40):
+        want_g = np.random.default_rng((1234, seed))
+        got_g = structure.PCG64((1234, seed))
+        for _ in range(60):
+            n = int(rng.choice([1, 2, 3, 4, 7, 15, 240, 1000, 2**31 + 11, 2**32 - 5]))
+            assert int(want_g.integers(n)) == got_g.integers(n)
