@@ -149,17 +149,124 @@ class GpuCostEvaluator(_Base):
         return total.cpu().numpy(), verdict.cpu().numpy()
 
 
+class CandidateGroup:
+    """Every phase-1 (or phase-2) candidate of one beam state, left
+    unexpanded: `gpu_cut` generates them on the device
+    (gs_expand_phase1 / gs_expand_step) and builds host states only for the
+    beam it returns.  Produced by `phase1_candidates` / `phase2_candidates`,
+    the drop-ins for search.py:204-220 / 223-235 that `install(expand=True)`
+    puts into the search module."""
+
+    __slots__ = ("parent", "func", "phase", "config")
+
+    def __init__(self, parent, func, phase, config):
+        self.parent, self.func, self.phase, self.config = parent, func, phase, config
+
+
+def phase1_candidates(state, func, graph, config):
+    """Drop-in for `gpusched.search._phase1_candidates` (search.py:204-220)."""
+    return [CandidateGroup(state, func, 1, config)]
+
+
+def phase2_candidates(state, func, graph, config):
+    """Drop-in for `gpusched.search._phase2_candidates` (search.py:223-235)."""
+    return [CandidateGroup(state, func, 2, config)]
+
+
+def _expand_items(sc, candidates):
+    """Device records of a phase's candidate list, in the list's order, where
+    items are states or CandidateGroups.  Returns (records [N, S*16], where:
+    per item (kind, a, b) — ('state', state, row) or ('group', group, first
+    row, count))."""
+    groups = [c for c in candidates if isinstance(c, CandidateGroup)]
+    plain = [c for c in candidates if not isinstance(c, CandidateGroup)]
+    parts, counts = [], []
+    if groups:
+        g0 = groups[0]
+        if any(g.phase != g0.phase or g.func != g0.func for g in groups):
+            raise ValueError("one phase expands one func")
+        par = sc.upload([g.parent for g in groups])
+        if g0.phase == 1:
+            restrict = g0.config.restrict_placements
+            recs, _, offs = sc.expand_phase1(par, g0.func, restrict=restrict, menus=g0.config.tiling)
+        else:
+            steps = []
+            for g in groups:
+                pos = [i for i, (f, _d) in enumerate(g.parent.decisions) if f == g0.func]
+                steps.append(pos[0])
+            st = torch.tensor(steps, dtype=torch.int32, device=sc.device)
+            recs, _, offs = sc.expand_step(par, st, menus=g0.config.tiling)
+        sc.check()
+        counts = np.diff(offs.cpu().numpy()).tolist()
+        parts.append(recs)
+    n_exp = sum(counts)
+    if plain:
+        parts.append(sc.upload(plain))
+    allr = torch.cat(parts) if len(parts) > 1 else parts[0]
+    order, where = [], []
+    gi = pi = 0
+    first = 0
+    starts = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64) if counts else [0]
+    for c in candidates:
+        if isinstance(c, CandidateGroup):
+            k = counts[gi]
+            start = int(starts[gi])
+            order.extend(range(start, start + k))
+            where.append(("group", c, first, k))
+            first += k
+            gi += 1
+        else:
+            order.append(n_exp + pi)
+            where.append(("state", c, first, 1))
+            first += 1
+            pi += 1
+    idx = torch.tensor(order, dtype=torch.int64, device=sc.device)
+    dec = allr.index_select(0, idx) if order != list(range(len(order))) else allr
+    return dec, where
+
+
+def _materialize(sc, dec, where, i):
+    """The host state of candidate i: the item itself, or — for a group —
+    the reference's own apply_decision of the device record's decision on
+    the parent (what the reference's _phase1/2_candidates would have built)."""
+    import bisect
+    firsts = [w[2] for w in where]
+    k = bisect.bisect_right(firsts, i) - 1
+    kind, item, first, _ = where[k]
+    if kind == "state":
+        return item
+    from gpusched.loopnest import Decision, apply_decision  # type: ignore
+    from .descriptor import DECISION_DTYPE, KIND_NAME
+    rec = dec[i].cpu().numpy().view(DECISION_DTYPE)
+    fi = sc.packed.index[item.func]
+    r = rec[rec["func"] == fi][0]
+    fnode = sc.packed.graph.func(item.func)
+    nd = fnode.ndim
+    d = Decision(KIND_NAME[int(r["kind"])],
+                 consumer=None if r["consumer"] == 0xFFFF else sc.packed.names[int(r["consumer"])],
+                 serial=tuple(int(x) for x in r["serial"][:nd]) if r["flags"] & 1 else None,
+                 thread=tuple(int(x) for x in r["thread"][:nd]) if r["flags"] & 2 else None)
+    return apply_decision(item.parent, item.func, d)
+
+
 def gpu_cut(candidates, evaluator, graph, config, pass_index, memo, phase_seed, validate):
     """Drop-in for `gpusched.search._cut` (search.py:168-201).
 
     `validate` is the reference prune closure over `config.thresholds`
     (search.py:246-247); the same rules run on the GPU with those thresholds.
+    Candidates may be states or CandidateGroups (install(expand=True)): a
+    group's candidates are generated on the device and only the returned
+    beam becomes host states.
     """
     if not candidates:
         return [], []
     weights = getattr(evaluator, "weights", None)
     sc = scorer_for(graph, evaluator.params, config.thresholds, weights)
-    dec = sc.upload(candidates)
+    lazy = any(isinstance(c, CandidateGroup) for c in candidates)
+    if lazy:
+        dec, where = _expand_items(sc, candidates)
+    else:
+        dec, where = sc.upload(candidates), None
     flagged = [h for d, h in memo.flagged if d == pass_index]
     res = beam_cut(sc, dec, pass_index, phase_seed, flagged, config.beam_size,
                    config.penalty_factor, config.explore_temperature, config.num_passes,
@@ -168,29 +275,37 @@ def gpu_cut(candidates, evaluator, graph, config, pass_index, memo, phase_seed, 
                for i, reason in res.rejects]
     for depth, h in res.memo_new:
         memo.record(depth, h)
-    beam = [candidates[i].with_cost(c) for i, c in zip(res.beam, res.costs)]
+    if lazy:
+        beam = [_materialize(sc, dec, where, i).with_cost(c) for i, c in zip(res.beam, res.costs)]
+    else:
+        beam = [candidates[i].with_cost(c) for i, c in zip(res.beam, res.costs)]
     return beam, reports
 
 
-def install(search_module=None):
-    """Route the reference search's phase cuts through the GPU.  Returns the
-    previous `_cut` so callers can restore it."""
+def install(search_module=None, expand=False):
+    """Route the reference search's phase cuts through the GPU; with
+    expand=True also its candidate generation (`_phase1_candidates`,
+    `_phase2_candidates` -> device expansion inside gpu_cut).  Returns the
+    previous functions so callers can restore them."""
     if search_module is None:
         import gpusched.search as search_module  # type: ignore
-    prev = search_module._cut
+    prev = (search_module._cut, search_module._phase1_candidates, search_module._phase2_candidates)
     search_module._cut = gpu_cut
+    if expand:
+        search_module._phase1_candidates = phase1_candidates
+        search_module._phase2_candidates = phase2_candidates
     return prev
 
 
 @contextlib.contextmanager
-def installed(search_module=None):
+def installed(search_module=None, expand=False):
     if search_module is None:
         import gpusched.search as search_module  # type: ignore
-    prev = install(search_module)
+    prev = install(search_module, expand=expand)
     try:
         yield
     finally:
-        search_module._cut = prev
+        search_module._cut, search_module._phase1_candidates, search_module._phase2_candidates = prev
 
 
 def as_numpy(t: torch.Tensor) -> np.ndarray:

@@ -58,10 +58,13 @@ def _reference_on_path():
         return False
 
 
+@pytest.mark.parametrize("expand", [False, True])
 @pytest.mark.parametrize("tag", ["chain2", "diamond", "stencil_chain", "chain16_freeze"])
-def test_reference_search_drives_gpu_path(tag, dev):
+def test_reference_search_drives_gpu_path(tag, expand, dev):
     """The UNCHANGED reference search with the GPU evaluator + `_cut` hook
-    returns the same final beam as the pure-CPU reference run."""
+    returns the same final beam as the pure-CPU reference run — and with
+    expand=True also with its candidate generation on the device (phase-1 /
+    phase-2 groups expanded inside gpu_cut, host states only for beams)."""
     if not _reference_on_path():
         pytest.skip("reference package not installed (baseline/_ref)")
     import importlib
@@ -87,7 +90,7 @@ def test_reference_search_drives_gpu_path(tag, dev):
     w = load_weights(os.path.join(ROOT, "tests", "golden", "weights_seed0.txt"))
     params = MachineParams()
     ev = ev_mod.GpuCostEvaluator(w, params, scfg.thresholds)
-    with ev_mod.installed(gs):
+    with ev_mod.installed(gs, expand=expand):
         if cfg["freeze_enabled"]:
             final = gs.schedule_with_freezing(graph, params, scfg, ev)
         else:
