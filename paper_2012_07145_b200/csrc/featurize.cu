@@ -2102,10 +2102,16 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tph = 0;
 #endif
   unsigned* work = reinterpret_cast<unsigned*>(gerr + 14);
-  const int64_t nunits = (n + kUnit - 1) / kUnit;
+  // Small batches (a search phase of a few hundred candidates) take smaller
+  // units so every scorer warp gets work; below 16 candidates per unit runs
+  // are split (latency over sibling reuse).
+  const int64_t twarps = (int64_t)gridDim.x * nw;
+  const int64_t unit = n >= (int64_t)kUnit * twarps ? kUnit : (n + twarps - 1) / twarps;
+  const int64_t nunits = (n + unit - 1) / unit;
+  const bool snapping = unit >= 16;
   auto snap = [&](int64_t x) -> int64_t {
     if (x >= n) return n;
-    if (!heads) return x;
+    if (!heads || !snapping) return x;
     for (int64_t i = x; i < n; i += 32) {
       const bool h = i + lane < n && heads[i + lane];
       const unsigned b = __ballot_sync(0xffffffffu, h);
@@ -2147,7 +2153,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   int64_t c0, c1;
   if (mode == 0) {
     if (j >= nunits) break;
-    c0 = snap(j * kUnit); c1 = snap((j + 1) * kUnit);
+    c0 = snap(j * unit); c1 = snap((j + 1) * unit);
   } else if (mode == 1) {
     if (j >= nruns) break;
     c0 = run_head[j]; c1 = c0 + 1;
