@@ -56,6 +56,16 @@ except Exception:  # pragma: no cover - standalone use
 
 
 _SCORERS: dict = {}
+_SHARDING = {"on": False, "group": None}
+
+
+def configure_sharding(enable: bool = True, group=None):
+    """Shard every phase cut's buckets across the ranks of `group` (default:
+    the initialised torch.distributed world; one process per GPU, NCCL), as
+    SURVEY §8(e) splits a beam step.  Every rank runs the same search; each
+    featurizes and costs only its buckets' candidates, and the ranks agree on
+    the beam through the top-k / memo-window exchange (exchange.py)."""
+    _SHARDING["on"], _SHARDING["group"] = enable, group
 
 
 def scorer_for(graph, params, thresholds, weights) -> Scorer:
@@ -268,9 +278,15 @@ def gpu_cut(candidates, evaluator, graph, config, pass_index, memo, phase_seed, 
     else:
         dec, where = sc.upload(candidates), None
     flagged = [h for d, h in memo.flagged if d == pass_index]
+    world, rank, group = 1, 0, None
+    if _SHARDING["on"]:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            group = _SHARDING["group"]
+            world, rank = dist.get_world_size(group), dist.get_rank(group)
     res = beam_cut(sc, dec, pass_index, phase_seed, flagged, config.beam_size,
                    config.penalty_factor, config.explore_temperature, config.num_passes,
-                   sampling=config.sampling)
+                   sampling=config.sampling, world=world, rank=rank, group=group)
     reports = [_PruneReport(reason, f"GPU prune verdict for candidate {i} of this phase")
                for i, reason in res.rejects]
     for depth, h in res.memo_new:

@@ -194,6 +194,8 @@ class StepPlan:
             nrej = int(nrej_t.item())
             ridx = rej[:nrej]
             codes = verdict.index_select(0, ridx).cpu().numpy()
+            if mine is not None:   # pass-depth hashes: ranks merge their rejects in bucket order
+                out["reject_hashes"] = [int(x) for x in hl.index_select(0, ridx).cpu().numpy().view(np.uint64)]
             ridx = (ridx if mine is None else mine.index_select(0, ridx)).cpu().numpy()
             out["rejects"] = [(int(i), PRUNE_REASONS[int(c) - 1]) for i, c in zip(ridx, codes)]
         return out
