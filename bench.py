@@ -403,15 +403,30 @@ def run_gpu(args):
         bytes_k1 = n_local * (R * (16 + 448 + 4) + 5)
         peak, peak_kind = _peaks()
         achieved = bytes_k1 / (k1 / 1e3) / 1e9 if k1 else None
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "r01_k1_dram_bytes.json")
+        traffic, inst_per_cand = None, None
+        prof = os.path.join(ROOT, "profiles", "r02_k1_counters.json")
         if os.path.exists(prof):
             try:
                 with open(prof) as fh:
-                    traffic = json.load(fh).get("dram_bytes_per_launch_per_candidate")
-                    traffic = traffic * n_local if traffic else None
+                    kc = json.load(fh)
+                traffic = kc.get("dram_bytes_per_launch_per_candidate")
+                traffic = traffic * n_local if traffic else None
+                inst_per_cand = kc.get("warp_instructions_per_candidate")
             except Exception:
                 traffic = None
+        clk_summary = clk.summary()
+        f_clk = (clk_summary.get("sm_mhz") or 1965.0) * 1e6
+        import torch as _t
+        n_sm = _t.cuda.get_device_properties(local).multi_processor_count
+        issue = None
+        if inst_per_cand and k1:
+            # instruction-issue roofline of K1: warp-instructions it must issue
+            # (ncu count per candidate) at the measured rate, over 4 issue
+            # slots per SM per clock
+            ach = inst_per_cand * n_local / (k1 / 1e3)
+            issue = {"achieved": ach, "peak": n_sm * 4 * f_clk, "unit": "warp-instructions/s",
+                     "frac": ach / (n_sm * 4 * f_clk), "warp_instructions_per_candidate": inst_per_cand,
+                     "source": "profiles/r02_k1_counters.json (ncu smsp__inst_executed.sum / candidates)"}
         cpu = None
         if world == 1 and not args.no_cpu:
             v, cores, kind, desc = cpu_reference(graph, recs, seconds=args.cpu_seconds)
@@ -434,14 +449,15 @@ def run_gpu(args):
                          "algorithmic_bytes_per_launch": bytes_k1,
                          "note": "K1 is integer-ALU / instruction-latency bound (resolve + warp transaction "
                                  "emulation); achieved = SURVEY 8(d) algorithmic bytes / K1 time as the north "
-                                 "star asks; K1 writes only computed rows (reuse mode 2), traffic = ncu DRAM bytes"},
+                                 "star asks; K1 writes only computed rows (reuse mode 2), traffic = ncu DRAM bytes",
+                         "issue": issue},
             "cpu_baseline": cpu,
             "e2e": {"value": N / (e / 1e3), "unit": UNIT, "ms_per_step": e,
                     "path": "StepPlan.run_beam_host: H2D beam, gs_expand_step on device, step, D2H results",
                     "h2d_bytes_per_step": int(out["h2d_bytes"]), "d2h_bytes_per_step": int(out["d2h_bytes"])},
             "step_breakdown_ms": breakdown,
             "gpu_launches": int(launches),
-            "clocks": clk.summary(),
+            "clocks": clk_summary,
             "beam": res["beam"][:8],
             "parity": parity,
         }

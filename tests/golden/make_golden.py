@@ -176,8 +176,46 @@ def record_search(tag, graph, cfg, params, weights, freeze=False):
     return len(calls), sum(len(c["candidates"]) for c in calls)
 
 
+def record_search_beams(tag, graph, cfg, params, weights):
+    """Trace a search too large to store its candidates (C3 at SURVEY §8(d)'s
+    beam 32 x 5 passes): per `_cut` call the candidate count, the returned
+    beam and costs and the memo size; plus the final beam and the wall time."""
+    import time
+    calls = []
+    orig_cut = gsearch._cut
+
+    def traced(candidates, evaluator, graph_, config, pass_index, memo, phase_seed, validate):
+        beam, reports = orig_cut(candidates, evaluator, graph_, config, pass_index, memo,
+                                 phase_seed, validate)
+        calls.append({"pass_index": pass_index, "phase_seed": phase_seed, "n_candidates": len(candidates),
+                      "beam": [schedule_dump(s) for s in beam], "beam_costs": [s.cost for s in beam],
+                      "memo_size": len(memo.flagged), "n_reports": len(reports)})
+        return beam, reports
+
+    gsearch._cut = traced
+    t = time.perf_counter()
+    try:
+        final = gsearch.schedule_with_freezing(graph, params, cfg, CostEvaluator(weights, params))
+    finally:
+        gsearch._cut = orig_cut
+    wall = time.perf_counter() - t
+    out = {"pipeline": graph_to_text(graph), "config": {
+        "beam_size": cfg.beam_size, "num_passes": cfg.num_passes, "seed": cfg.seed,
+        "freeze_enabled": cfg.freeze_enabled}, "calls": calls,
+        "final": [schedule_dump(s) for s in final], "final_costs": [s.cost for s in final],
+        "reference_wall_s": wall, "reference_cores": 1}
+    with gzip.open(os.path.join(HERE, f"search_{tag}.json.gz"), "wt") as fh:
+        json.dump(out, fh)
+    return len(calls), sum(c["n_candidates"] for c in calls), wall
+
+
 def main():
     params = MachineParams()
+    if "--c3-full" in sys.argv:   # C3 at beam 32 x 5 passes (beams only; candidates regenerate on the GPU)
+        print(record_search_beams("local_laplacian_b32p5", authored("local_laplacian"),
+                                  SearchConfig(beam_size=32, num_passes=5, seed=0, freeze_enabled=True),
+                                  params, init_weights(seed=0)), flush=True)
+        return
     w0 = init_weights(seed=0)
     save_weights(w0, os.path.join(HERE, "weights_seed0.txt"))
     w1 = init_weights(seed=3, embed_dim=16, hidden_dim=48)
