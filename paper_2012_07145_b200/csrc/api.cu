@@ -9,7 +9,7 @@
 
 namespace gs {
 Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rcap, int pcap, int nwarps,
-                   bool spill);
+                   bool spill, bool generic);
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
                      const Layout& L, int nwarps, int grid, int* gerr, int reuse, uint8_t* gscratch,
@@ -275,8 +275,12 @@ int gs_set_weights(gs_pipeline_t p, int E, int H, const double* aw, const double
 }
 
 static Layout layout_for(gs_pipeline_t p, int S, int nwarps, bool spill) {
+  // machines other than the default (32 B transactions, 32 x 4 B banks) run
+  // the generic counters and need their residue tables in the warp slice
+  const GsMachine& m = p->host.m;
+  const bool generic = !(m.global_transaction_bytes == 32 && m.shared_banks == 32 && m.bank_width_bytes == 4);
   return make_layout(p->host.nd, p->host.nf, p->host.ns, p->host.blob_bytes, S, std::max(1, p->host.max_rows),
-                     p->rcap, p->pcap, nwarps, spill);
+                     p->rcap, p->pcap, nwarps, spill, generic);
 }
 
 int gs_set_reuse(gs_pipeline_t p, int enable) {

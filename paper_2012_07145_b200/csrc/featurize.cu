@@ -25,6 +25,7 @@
 // See DESIGN.md "K1 featurize" for the roofline reading.
 #include "gs_internal.cuh"
 #include "scan.cuh"
+#include <cstddef>
 #include <cuda/std/cstdint>
 
 namespace gs {
@@ -33,10 +34,13 @@ struct Frame { int16_t owner, root; int32_t cur, end; int16_t plen, pad; int64_t
 
 struct ICall { int16_t root, iname, stage, pad; int64_t vol; };   // per (root stage, inline func)
 
+// Per-warp row scratch.  The generic counters (machines other than 32 B
+// transactions / 32 x 4 B banks) need residue tables of up to kMaxM entries;
+// they sit at the end and are allocated only for such machines, which keeps
+// the default machine's warp slice small enough for ten scorer warps.
 struct WarpScr {
   double feat[GS_NUM_FEATURES];
-  unsigned long long H[kMaxM], S[kMaxM], T[kMaxM];
-  int16_t nz[kMaxM];
+  unsigned long long H[32], S[32];      // residue_hist scratch (Q <= 32)
   unsigned long long acc[4][3][2];      // box x tier x (bytes, lines)
   int16_t rl[kRowReads];
   int8_t grp[kRowReads];
@@ -44,7 +48,11 @@ struct WarpScr {
   int16_t gprod[kRowReads];
   int ngroups;
   int nr;
+  // generic machines only
+  unsigned long long GH[kMaxM], GS[kMaxM], T[kMaxM];
+  int16_t nz[kMaxM];
 };
+constexpr int kScrDefaultBytes = (int)offsetof(WarpScr, GH);
 
 struct Misc {
   int ndec, nreads, npath, nrows, nicall, err, verdict, same_struct, prev_valid, ndirty, ngeo, incr;
@@ -1363,42 +1371,42 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
       const int e = h.ext[d];
       // per-dim histogram of relative coordinates (mod M) into H
       if (identity || !h.unrolled) {
-        for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.H[r] = mm.count_in(0, e - 1, r); }
+        for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.GH[r] = mm.count_in(0, e - 1, r); }
         __syncwarp();
         if (!identity) {
           for (int q = 0; q < plen; ++q) {
             const GsAccess& x = A[path[q]];
             const int64_t s = x.s[d], wl = x.lo[d], wh = x.hi[d];
             // S[k] = sum_r H[r] * #{w in [wl,wh] : r*s + w = k (mod M)}
-            for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.S[r] = 0; }
+            for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.GS[r] = 0; }
             __syncwarp();
             if (wh - wl + 1 < M) {       // short window: scatter each residue's taps
               for (int j = 0; j < per; ++j) {
                 const int r = lane + 32 * j;
                 if (r >= M) continue;
-                const unsigned long long hv = W.H[r];
+                const unsigned long long hv = W.GH[r];
                 if (!hv) continue;
                 const int64_t base = (int64_t)r * s;
                 #pragma unroll 1
-                for (int64_t w = wl; w <= wh; ++w) atomicAdd(&W.S[mm.pmod(base + w)], hv);
+                for (int64_t w = wl; w <= wh; ++w) atomicAdd(&W.GS[mm.pmod(base + w)], hv);
               }
             } else {
               for (int c = 0; c < per; ++c) {
-                unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < M && W.H[c * 32 + lane] != 0);
+                unsigned nz = __ballot_sync(0xffffffffu, (c * 32 + lane) < M && W.GH[c * 32 + lane] != 0);
                 while (nz) {
                   const int b = __ffs(nz) - 1; nz &= nz - 1;
                   const int r = c * 32 + b;
-                  const unsigned long long hv = W.H[r];
+                  const unsigned long long hv = W.GH[r];
                   const int64_t sh = mm.pmod((int64_t)r * s);
                   for (int j = 0; j < per; ++j) {
                     const int k = lane + 32 * j;
-                    if (k < M) W.S[k] += hv * mm.count_in(wl, wh, mm.pmod(k - sh));
+                    if (k < M) W.GS[k] += hv * mm.count_in(wl, wh, mm.pmod(k - sh));
                   }
                 }
               }
             }
             __syncwarp();
-            for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.H[r] = W.S[r]; }
+            for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.GH[r] = W.GS[r]; }
             __syncwarp();
           }
         }
@@ -1412,17 +1420,17 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
           unsigned long long c = 0;
           #pragma unroll 1
           for (int i = 0; i < n; ++i) c += mm.count_in(buf[i].lo, buf[i].hi, r);
-          W.H[r] = c;
+          W.GH[r] = c;
         }
         __syncwarp();
       }
       // scale by the byte stride of dim d, then convolve into T
       const int64_t bm = mm.pmod(bs[d]);
-      for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.S[r] = 0; }
+      for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.GS[r] = 0; }
       __syncwarp();
       for (int j = 0; j < per; ++j) {
         int r = lane + 32 * j;
-        if (r < M && W.H[r]) atomicAdd(&W.S[mm.pmod((int64_t)r * bm)], W.H[r]);
+        if (r < M && W.GH[r]) atomicAdd(&W.GS[mm.pmod((int64_t)r * bm)], W.GH[r]);
       }
       // nonzero residues of T, then H[k] = sum_r T[r] S[k - r] (lane per k)
       int nnz = 0;
@@ -1441,12 +1449,12 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
         #pragma unroll 1
         for (int i = 0; i < nnz; ++i) {
           const int r = W.nz[i];
-          acc += W.T[r] * W.S[mm.pmod(k - r)];
+          acc += W.T[r] * W.GS[mm.pmod(k - r)];
         }
-        W.H[k] = acc;
+        W.GH[k] = acc;
       }
       __syncwarp();
-      for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.T[r] = W.H[r]; }
+      for (int j = 0; j < per; ++j) { int r = lane + 32 * j; if (r < M) W.T[r] = W.GH[r]; }
       __syncwarp();
     }
   }
@@ -1545,7 +1553,7 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
   }
   // two classes: weights in H (class 0) and S (class 1); registers are
   // named, not indexed, so they stay out of local memory
-  for (int j = 0; j < pp; ++j) { int r = lane + 32 * j; if (r < P) { W.H[r] = 0; W.S[r] = 0; } }
+  for (int j = 0; j < pp; ++j) { int r = lane + 32 * j; if (r < P) { W.GH[r] = 0; W.GS[r] = 0; } }
   __syncwarp();
   int ncls = 0;
   int64_t rel0 = 0, rel1 = 0, o00 = 0, o01 = 0;
@@ -1594,7 +1602,7 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
       if (fold) acc += cd * __shfl_sync(0xffffffffu, tb, (lane - d) & (P - 1));
       else acc += cd * W.T[(lane - d) & (P - 1)];
     }
-    if (lane < P) W.H[lane] = acc;
+    if (lane < P) W.GH[lane] = acc;
     __syncwarp();
   }
   for (int w = 0; w < nwarps && !regular; ++w, walk.next()) {
@@ -1610,7 +1618,7 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
     else if (ncls == 1) { cls = 1; ncls = 2; rel1 = rw; am1 = amask; o01 = ow; }
     if (cls >= 0) {
       const int64_t dlt = ow - (cls ? o01 : o00);
-      unsigned long long* wv = cls ? W.S : W.H;
+      unsigned long long* wv = cls ? W.GS : W.GH;
       if (fold) {
         const int src = (int)((lane - dlt) & (int64_t)(bw - 1));
         const unsigned long long add = __shfl_sync(0xffffffffu, tb, src);
@@ -1664,7 +1672,7 @@ __device__ __noinline__ unsigned long long warp_tx(const GsAccess* A, const int1
   for (int j = 0; j < ncls; ++j) {
     const bool active = ((j ? am1 : am0) >> lane) & 1u;
     const int64_t org = j ? o01 + rel1 : o00 + rel0;
-    const unsigned long long* wv = j ? W.S : W.H;
+    const unsigned long long* wv = j ? W.GS : W.GH;
     if (MC == 32 && tier == T_GLOBAL) {
       // lanes = residues.  When the representative's lane addresses are
       // non-decreasing (row-major thread tiles), the segments of one
@@ -2067,9 +2075,9 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   k.path = reinterpret_cast<int16_t*>(wg + L.paths);
   k.rdb = reinterpret_cast<int32_t*>(ws + L.rdb);
   k.rows = reinterpret_cast<int32_t*>(ws + L.rows);
-  k.stack = reinterpret_cast<Frame*>(ws + L.stack);
-  k.volacc = reinterpret_cast<int64_t*>(ws + L.volacc);
-  k.touched = reinterpret_cast<int16_t*>(ws + L.touched);
+  k.stack = reinterpret_cast<Frame*>(wgs + L.stack);       // structure-build scratch: global
+  k.volacc = reinterpret_cast<int64_t*>(wgs + L.volacc);
+  k.touched = reinterpret_cast<int16_t*>(wgs + L.touched);
   k.icall = reinterpret_cast<ICall*>(wgs + L.icall);
   k.srcb = reinterpret_cast<int32_t*>(ws + L.srcb);
   k.srcl = reinterpret_cast<int16_t*>(wg + L.srcl);
@@ -2078,7 +2086,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   k.dirty = reinterpret_cast<uint8_t*>(ws + L.dirty);
   k.rowlist = reinterpret_cast<int16_t*>(ws + L.rowlist);
   k.kern = reinterpret_cast<int16_t*>(ws + L.kern);
-  k.dm = reinterpret_cast<uint32_t*>(ws + L.dm);
+  k.dm = reinterpret_cast<uint32_t*>(wgs + L.dm);          // dependency masks: global (L1)
   k.cmask = reinterpret_cast<uint32_t*>(ws + L.cmask);
   k.kmb = reinterpret_cast<int32_t*>(ws + L.kmb);
   k.kml = reinterpret_cast<int16_t*>(ws + L.kml);
@@ -2359,11 +2367,10 @@ template <int ND>
 static int cf_size() { return (int)sizeof(CF<ND>); }
 
 // Shared memory: [pipeline descriptor | warp 0 slice | warp 1 slice | ...];
-// offsets inside a slice are relative to the slice.  The structure-build
-// scratch (DFS stack, volume accumulators, touched list) aliases the row
-// scratch: they are never live at the same time.
+// offsets inside a slice are relative to the slice.  Arrays placed with
+// gplace live in the warp's global scratch instead (offsets relative to it).
 Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rcap, int pcap, int nwarps,
-                   bool spill) {
+                   bool spill, bool generic) {
   auto al = [](int x) { return (x + 15) & ~15; };
   Layout L{};
   L.blob = 0;
@@ -2393,7 +2400,7 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   L.rsrc = o; o += al(R * 4);
   L.mw = nf <= 32 * kMaxMaskWords ? (nf + 31) / 32 : 0;
   L.kern = o; o += al(nf * 2);
-  L.dm = o; o += al(nf * L.mw * 4);
+  L.dm = gplace(nf * L.mw * 4);
   L.cmask = o; o += al(kMaxMaskWords * 4);
   L.kmb = o; o += al((nf + 1) * 4);
   L.kml = o; o += al(nf * 2);
@@ -2403,14 +2410,16 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   L.gdirty = o; o += al(nf);
   L.kdirty = o; o += al(nf);
   L.misc = o; o += al((int)sizeof(Misc));
-  // aliased: row scratch | structure-build scratch
+  // row scratch; the structure-build scratch (DFS stack, volume
+  // accumulators, touched list: used once per decision structure) lives in
+  // the warp's global scratch, as do the dependency masks, so that the
+  // default machine's slice fits ten scorer warps per SM
   L.scr = o;
-  int sa = 0;
-  L.stack = o + sa; sa += al((nf + 2) * (int)sizeof(Frame));
-  L.volacc = o + sa; sa += al(nf * 8);
-  L.touched = o + sa; sa += al(2 * nf * 2 + 4);
-  const int scr = al((int)sizeof(WarpScr)) > sa ? al((int)sizeof(WarpScr)) : sa;
-  o += scr;
+  L.stack = gplace((nf + 2) * (int)sizeof(Frame));
+  L.volacc = gplace(nf * 8);
+  L.touched = gplace(2 * nf * 2 + 4);
+  const int scr_bytes = generic ? (int)sizeof(WarpScr) : kScrDefaultBytes;
+  o += al(scr_bytes);
   L.warp_bytes = al(o);
   L.gl_bytes = g;
   L.spill = spill;
