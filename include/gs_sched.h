@@ -151,6 +151,8 @@ int gs_set_weights(gs_pipeline_t p, int embed_dim, int hidden_dim,
  * gs_cost with row_src (the beam step) — gs_featurize then requires
  * row_src. */
 int gs_set_reuse(gs_pipeline_t p, int enable);
+/* The current reuse mode (-1 for a null handle). */
+int gs_get_reuse(gs_pipeline_t p);
 
 int gs_featurize(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
                  double* feats, int32_t* row_key, int32_t* n_rows,

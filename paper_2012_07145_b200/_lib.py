@@ -23,7 +23,7 @@ EXPORTS = ("gs_last_error", "gs_version", "gs_launch_count", "gs_pipeline_create
            "gs_featurize_ws", "gs_struct_hash_workspace_bytes", "gs_struct_hash_ws", "gs_beam_topk_reps",
            "gs_model_params", "gs_predict", "gs_train_workspace_bytes", "gs_train",
            "gs_set_placement_info", "gs_phase1_workspace_bytes", "gs_expand_phase1",
-           "gs_random_schedules")
+           "gs_random_schedules", "gs_get_reuse")
 
 
 class GsError(RuntimeError):
@@ -51,6 +51,7 @@ def load(path: str = LIB_PATH):
         "gs_pipeline_max_rows": (i32, [P]),
         "gs_set_weights": (i32, [P, i32, i32] + [V] * 8),
         "gs_set_reuse": (i32, [P, i32]),
+        "gs_get_reuse": (i32, [P]),
         "gs_featurize": (i32, [P, V, i64, i32, V, V, V, V, V, V]),
         "gs_cost": (i32, [P, V, V, V, V, i64, V, V, V, V]),
         "gs_struct_hash": (i32, [P, V, i64, i32, i32, V, V]),

@@ -290,6 +290,8 @@ int gs_set_reuse(gs_pipeline_t p, int enable) {
   return GS_OK;
 }
 
+int gs_get_reuse(gs_pipeline_t p) { return p ? p->reuse : -1; }
+
 }  // extern "C"
 
 // K1 launch shape and workspace.  One CTA per SM, as many independent

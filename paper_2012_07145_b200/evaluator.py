@@ -108,6 +108,30 @@ class GpuCostEvaluator(_Base):
     def __init__(self, weights, params, thresholds=None):
         _Base.__init__(self, weights, params)
         self.thresholds = thresholds or DEFAULT_THRESHOLDS
+        self._cost_cache = {}    # (id(graph), decisions) -> (weights key, total, per-stage dict)
+        self._last_beam = None   # (id(graph), states) of the last gpu_cut
+
+    def _batch_costs(self, states, graph):
+        """K1 + K2 (with the basis) for several states in one launch each;
+        fills the cost and basis caches (search.py:103-124 semantics)."""
+        sc = scorer_for(graph, self.params, self.thresholds, self.weights)
+        dec = sc.upload(states)
+        h = sc.handle.value
+        feats, row_key, n_rows, verdict, row_src = torch.ops.gsched.featurize(h, dec, sc.R, 1)
+        total, rows, gh = torch.ops.gsched.cost(h, feats, row_key, n_rows, None, True)
+        sc.check()
+        f_all = feats.cpu().numpy()
+        keys_all, nr = row_key.cpu().numpy(), n_rows.cpu().numpy()
+        tot, rc, g = total.cpu().numpy(), rows.cpu().numpy(), gh.cpu().numpy()
+        algo = sc.packed.algo
+        for i, st in enumerate(states):
+            n = int(nr[i])
+            keys = sc.packed.row_keys(keys_all[i, :n])
+            ck = (id(graph), st.decisions)
+            self._cost_cache[ck] = (sc._weights_key, float(tot[i]), {k: float(c) for k, c in zip(keys, rc[i, :n])})
+            if ck not in self._basis_cache:
+                self._basis_cache[ck] = [(k, algo[sc.packed.stage_index[k]].copy(), f_all[i, r].copy(),
+                                          g[i, r, :30].copy(), float(g[i, r, 30])) for r, k in enumerate(keys)]
 
     def _run(self, state, graph):
         # through the registered custom ops (ops.py): K1 then K2 with the basis
@@ -144,9 +168,25 @@ class GpuCostEvaluator(_Base):
         return hit
 
     def cost(self, state, graph):
+        # The search re-costs its final beam one state at a time
+        # (search.py:312-317, and the freeze pre-pass's best, 335): the first
+        # such call costs the whole last beam in one batch, the rest are hits.
+        ck = (id(graph), state.decisions)
+        wk = scorer_for(graph, self.params, self.thresholds, self.weights)._weights_key
+        hit = self._cost_cache.get(ck)
+        if hit is None and self._last_beam is not None and self._last_beam[0] == id(graph):
+            beam = self._last_beam[1]
+            if any(s.decisions == state.decisions for s in beam):
+                self._batch_costs(beam, graph)
+                self._last_beam = None
+                hit = self._cost_cache.get(ck)
+        if hit is not None and hit[0] == wk:
+            return hit[1], dict(hit[2])
         sc, f, n, keys, total, rows, gh = self._run(state, graph)
         self._fill_cache(sc, f, n, keys, gh, state, graph)
-        return total, {k: float(c) for k, c in zip(keys, rows)}
+        per = {k: float(c) for k, c in zip(keys, rows)}
+        self._cost_cache[ck] = (sc._weights_key, total, per)
+        return total, dict(per)
 
     def cost_batch(self, states, graph):
         """Totals (np.float64[N]) and prune verdicts for a list of states."""
@@ -295,6 +335,8 @@ def gpu_cut(candidates, evaluator, graph, config, pass_index, memo, phase_seed, 
         beam = [_materialize(sc, dec, where, i).with_cost(c) for i, c in zip(res.beam, res.costs)]
     else:
         beam = [candidates[i].with_cost(c) for i, c in zip(res.beam, res.costs)]
+    if isinstance(evaluator, GpuCostEvaluator):
+        evaluator._last_beam = (id(graph), beam)   # batched final re-cost (GpuCostEvaluator.cost)
     return beam, reports
 
 

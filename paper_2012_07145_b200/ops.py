@@ -73,12 +73,13 @@ def featurize(handle: int, dec: Tensor, R: int, reuse: int) -> tuple[Tensor, Ten
     verdict = torch.empty((n,), dtype=torch.uint8, device=dev)
     row_src = torch.zeros((n, R), dtype=torch.int32, device=dev)
     h = _h(handle)
+    prev = lib.gs_get_reuse(h)
     _lib.check(lib.gs_set_reuse(h, reuse))
     try:
         _lib.check(lib.gs_featurize(h, _p(dec), n, S, _p(feats), _p(row_key), _p(n_rows), _p(verdict),
                                     _p(row_src), _st()))
     finally:
-        lib.gs_set_reuse(h, 1)
+        lib.gs_set_reuse(h, prev)   # the handle's mode is the caller's state: restore it
     return feats, row_key, n_rows, verdict, row_src
 
 

@@ -1,0 +1,74 @@
+"""C3 at SURVEY §8(d)'s full size: the unchanged reference `schedule_with_freezing`
+on the 100-func local Laplacian, beam 32 x 5 passes with the freeze pre-pass,
+driven through the seam (GpuCostEvaluator + gpu_cut + device candidate
+generation) — every `_cut` call's beam, beam costs, memo size and candidate
+count, and the final beam, against the unmodified reference's own run of the
+same search (tests/golden/search_local_laplacian_b32p5.json.gz, written by
+`make_golden.py --c3-full`; the candidates are too many to store, so they
+are regenerated on the device and checked through the cut results)."""
+
+import gzip
+import json
+import os
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+FIX = os.path.join(ROOT, "tests", "golden", "search_local_laplacian_b32p5.json.gz")
+
+
+def test_c3_full_search_matches_reference():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    if not os.path.exists(FIX):
+        pytest.skip("fixture not generated (make_golden.py --c3-full)")
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "gpusched")):
+        pytest.skip("reference package not installed (baseline/_ref)")
+    if ref not in sys.path:
+        sys.path.append(ref)
+    import importlib
+    import gpusched.search as gs
+    from gpusched.costmodel import init_weights
+    from gpusched.loopnest import schedule_dump
+    from gpusched.machine import MachineParams
+    from gpusched.pipeline import parse_pipeline
+    ev_mod = importlib.import_module("paper_2012_07145_b200.evaluator")
+    if not ev_mod.HAVE_REFERENCE:
+        ev_mod = importlib.reload(ev_mod)
+    with gzip.open(FIX, "rt") as fh:
+        tr = json.load(fh)
+    cfg = tr["config"]
+    graph = parse_pipeline(tr["pipeline"], "local_laplacian")
+    scfg = gs.SearchConfig(beam_size=cfg["beam_size"], num_passes=cfg["num_passes"], seed=cfg["seed"],
+                           freeze_enabled=cfg["freeze_enabled"])
+    params = MachineParams()
+    ev = ev_mod.GpuCostEvaluator(init_weights(0), params, scfg.thresholds)
+    calls = []
+
+    def traced(candidates, evaluator, graph_, config, pass_index, memo, phase_seed, validate):
+        beam, reports = ev_mod.gpu_cut(candidates, evaluator, graph_, config, pass_index, memo, phase_seed,
+                                       validate)
+        calls.append((pass_index, phase_seed, [schedule_dump(s) for s in beam], [s.cost for s in beam],
+                      len(memo.flagged), len(reports)))
+        return beam, reports
+
+    prev = ev_mod.install(gs, expand=True)
+    gs._cut = traced
+    try:
+        final = gs.schedule_with_freezing(graph, params, scfg, ev)
+    finally:
+        gs._cut, gs._phase1_candidates, gs._phase2_candidates = prev
+    assert len(calls) == len(tr["calls"])
+    for i, (got, want) in enumerate(zip(calls, tr["calls"])):
+        assert (got[0], got[1]) == (want["pass_index"], want["phase_seed"]), i
+        assert got[2] == want["beam"], i
+        assert got[3] == pytest.approx(want["beam_costs"], rel=1e-9), i
+        assert got[4] == want["memo_size"], i
+        assert got[5] == want["n_reports"], i
+    assert [schedule_dump(s) for s in final] == tr["final"]
+    assert [s.cost for s in final] == pytest.approx(tr["final_costs"], rel=1e-9)
