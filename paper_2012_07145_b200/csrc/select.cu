@@ -185,23 +185,22 @@ __global__ void k4_quota(const uint32_t* __restrict__ bstart, const uint32_t* __
   quota[b] = q < 1 ? 1u : (uint32_t)q;
 }
 
-// One thread per bucket: numpy default_rng((phase_seed, h)).permutation(B)
-// (Fisher-Yates with bounded draws), then the draw walk of search.py:151-164
-// until quota valid members are taken.  Member j of a bucket is found in
-// its runs (insertion order) by binary search on the run offsets.
-__global__ void k4_walk(const uint64_t* __restrict__ skey, const uint32_t* __restrict__ sval,
-                        const uint32_t* __restrict__ rstart, const uint32_t* __restrict__ cum,
-                        const uint32_t* __restrict__ bstart, const uint32_t* __restrict__ nb_dev,
-                        const uint32_t* __restrict__ qoff, const uint32_t* __restrict__ quota,
-                        const uint8_t* __restrict__ verdict, uint64_t phase_seed, uint32_t* __restrict__ perm,
-                        int64_t* __restrict__ slot, uint32_t* __restrict__ taken, int64_t* __restrict__ rej,
-                        uint32_t* __restrict__ rejn) {
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= (int64_t)*nb_dev) return;
+// numpy default_rng((phase_seed, h)).permutation(B) (Fisher-Yates with
+// bounded draws), then the draw walk of search.py:151-164 until quota valid
+// members are taken.  Member j of a bucket is found in its runs (insertion
+// order) by binary search on the run offsets.  `p` holds B entries (global
+// or shared memory); one thread.
+__device__ __forceinline__ void walk_bucket(int64_t b, uint32_t* p, const uint64_t* __restrict__ skey,
+                                            const uint32_t* __restrict__ sval, const uint32_t* __restrict__ rstart,
+                                            const uint32_t* __restrict__ cum, const uint32_t* __restrict__ bstart,
+                                            const uint32_t* __restrict__ qoff, const uint32_t* __restrict__ quota,
+                                            const uint8_t* __restrict__ verdict, uint64_t phase_seed, bool filled,
+                                            int64_t* __restrict__ slot, uint32_t* __restrict__ taken,
+                                            int64_t* __restrict__ rej, uint32_t* __restrict__ rejn) {
   const uint32_t r0 = bstart[b], r1 = bstart[b + 1];
   const uint32_t s0 = cum[r0], B = cum[r1] - s0;
-  uint32_t* p = perm + s0;
-  for (uint32_t i = 0; i < B; ++i) p[i] = i;
+  if (!filled)
+    for (uint32_t i = 0; i < B; ++i) p[i] = i;
   Pcg64 g;
   seed_pair(g, phase_seed, skey[r0]);
   for (uint32_t i = B - 1; i >= 1; --i) {   // numpy Generator.permutation (Fisher-Yates)
@@ -228,6 +227,106 @@ __global__ void k4_walk(const uint64_t* __restrict__ skey, const uint32_t* __res
   }
   taken[b] = t;
   rejn[b] = nr;
+}
+
+// Small buckets: one thread each, the permutation in global memory (the
+// bucket's slice of `perm`).
+constexpr uint32_t kBigBucket = 1024;
+constexpr int kWalkSmemEntries = 50 * 1024;   // 200 KB of u32: a big bucket's permutation in shared memory
+
+__global__ void k4_walk(const uint64_t* __restrict__ skey, const uint32_t* __restrict__ sval,
+                        const uint32_t* __restrict__ rstart, const uint32_t* __restrict__ cum,
+                        const uint32_t* __restrict__ bstart, const uint32_t* __restrict__ nb_dev,
+                        const uint32_t* __restrict__ qoff, const uint32_t* __restrict__ quota,
+                        const uint8_t* __restrict__ verdict, uint64_t phase_seed, uint32_t* __restrict__ perm,
+                        int64_t* __restrict__ slot, uint32_t* __restrict__ taken, int64_t* __restrict__ rej,
+                        uint32_t* __restrict__ rejn) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= (int64_t)*nb_dev) return;
+  const uint32_t s0 = cum[bstart[b]], B = cum[bstart[b + 1]] - s0;
+  if (B >= kBigBucket) return;   // k4_walk_big
+  walk_bucket(b, perm + s0, skey, sval, rstart, cum, bstart, qoff, quota, verdict, phase_seed, false, slot, taken,
+              rej, rejn);
+}
+
+// Big buckets (random schedules of a small pipeline share a few structures:
+// C4 has 16 buckets of ~16K): one CTA each.  The Fisher-Yates shuffle is
+// sequential, so one thread runs it on a permutation in shared memory
+// (initialised by the whole CTA).  The walk is then parallel: every thread
+// maps its strided positions to candidates (run lookup: O(1) when every run
+// of the bucket is one candidate, else a binary search) and their verdicts,
+// and one thread scans the validity bitmask in draw order.  Buckets beyond
+// the shared capacity take the one-thread path on their global slice.
+constexpr int kWalkBits = kWalkSmemEntries / 32;
+
+__global__ void __launch_bounds__(256) k4_walk_big(
+    const uint64_t* __restrict__ skey, const uint32_t* __restrict__ sval, const uint32_t* __restrict__ rstart,
+    const uint32_t* __restrict__ cum, const uint32_t* __restrict__ bstart, const uint32_t* __restrict__ nb_dev,
+    const uint32_t* __restrict__ qoff, const uint32_t* __restrict__ quota, const uint8_t* __restrict__ verdict,
+    uint64_t phase_seed, uint32_t* __restrict__ perm, int64_t* __restrict__ slot, uint32_t* __restrict__ taken,
+    int64_t* __restrict__ rej, uint32_t* __restrict__ rejn) {
+  extern __shared__ uint32_t ps[];
+  __shared__ uint32_t vbits[kWalkBits];
+  const int64_t nb = *nb_dev;
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const uint32_t r0 = bstart[b], r1 = bstart[b + 1];
+    const uint32_t s0 = cum[r0], B = cum[r1] - s0;
+    if (B < kBigBucket) continue;   // uniform over the CTA
+    if (B > (uint32_t)kWalkSmemEntries) {
+      if (threadIdx.x == 0)
+        walk_bucket(b, perm + s0, skey, sval, rstart, cum, bstart, qoff, quota, verdict, phase_seed, false, slot,
+                    taken, rej, rejn);
+      __syncthreads();
+      continue;
+    }
+    for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) ps[i] = i;
+    for (uint32_t i = threadIdx.x; i < (B + 31) / 32; i += blockDim.x) vbits[i] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {   // numpy Generator.permutation (Fisher-Yates)
+      Pcg64 g;
+      seed_pair(g, phase_seed, skey[r0]);
+      for (uint32_t i = B - 1; i >= 1; --i) {
+        const uint32_t j = (uint32_t)g.interval(i);
+        const uint32_t t = ps[i]; ps[i] = ps[j]; ps[j] = t;
+      }
+    }
+    __syncthreads();
+    const bool singles = (r1 - r0) == B;   // every run one candidate
+    for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
+      const uint32_t o = s0 + ps[i];
+      uint32_t lo;
+      if (singles) {
+        lo = r0 + ps[i];
+      } else {
+        lo = r0;
+        uint32_t hi = r1 - 1;           // last run with cum[run] <= o
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi + 1) >> 1;
+          if (cum[mid] <= o) lo = mid; else hi = mid - 1;
+        }
+      }
+      const uint32_t m = rstart[sval[lo]] + (o - cum[lo]);
+      ps[i] = m;                         // position -> candidate
+      if (verdict[m] == 0) atomicOr(&vbits[i >> 5], 1u << (i & 31));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {   // search.py:151-164: draw order until quota valid
+      const uint32_t q = quota[b];
+      uint32_t t = 0, nr = 0;
+      for (uint32_t i = 0; i < B; ++i) {
+        if ((vbits[i >> 5] >> (i & 31)) & 1u) {
+          slot[qoff[b] + t] = ps[i];
+          if (++t == q) break;
+        } else {
+          rej[s0 + nr] = ps[i];
+          ++nr;
+        }
+      }
+      taken[b] = t;
+      rejn[b] = nr;
+    }
+    __syncthreads();
+  }
 }
 
 __global__ void k4_gather(const uint32_t* __restrict__ nb_dev, const uint32_t* __restrict__ qoff,
@@ -324,6 +423,21 @@ int select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, uint6
   scan_u32(w.quota, w.qoff, n, nb_dev, false, w.sums, nullptr, st);
   k4_walk<<<G, 64, 0, st>>>(w.rkey, w.rval, w.rstart, w.cum, w.bstart, nb_dev, w.qoff, w.quota, verdict,
                             phase_seed, w.perm, w.slot, w.taken, w.rej, w.rejn); g_launch_count++;
+  if (n >= (int64_t)kBigBucket) {   // a bucket of >= kBigBucket members is possible
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(k4_walk_big, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kWalkSmemEntries) !=
+          cudaSuccess)
+        return -3;
+      attr = true;
+    }
+    const int64_t maxbig = n / kBigBucket;
+    const unsigned gb = (unsigned)(maxbig < 512 ? maxbig : 512);
+    k4_walk_big<<<gb, 256, 4 * kWalkSmemEntries, st>>>(w.rkey, w.rval, w.rstart, w.cum, w.bstart, nb_dev, w.qoff,
+                                                       w.quota, verdict, phase_seed, w.perm, w.slot, w.taken, w.rej,
+                                                       w.rejn);
+    g_launch_count++;
+  }
   scan_u32(w.taken, w.toff, n, nb_dev, false, w.sums, tot_reps, st);
   scan_u32(w.rejn, w.roff, n, nb_dev, false, w.sums, tot_rej, st);
   k4_gather<<<G, T, 0, st>>>(nb_dev, w.qoff, w.taken, w.toff, w.slot, rep_idx, w.bstart, w.cum, w.rejn, w.roff,
