@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) cost_rows_kernel(NetDev ne
                                                         const int32_t* __restrict__ row_key,
                                                         const int32_t* __restrict__ n_rows,
                                                         const int32_t* __restrict__ row_src, int64_t n, int R,
-                                                        double* __restrict__ row_cost, unsigned* __restrict__ work) {
+                                                        double* __restrict__ row_cost, unsigned* __restrict__ work,
+                                                        int64_t kSpan) {
   extern __shared__ __align__(16) double smd[];
   __shared__ int64_t ring[kRowsWarps][kRing];
   const int E = net.E, H = net.H;
@@ -247,7 +248,8 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) cost_rows_kernel(NetDev ne
   // flags of 4 slabs are loaded together (4 loads in flight per lane) into
   // a circular queue; the network is evaluated at ONE call site (its code
   // is large: a second inlined copy would thrash the instruction cache).
-  constexpr int64_t kSpan = 2048;
+  // kSpan: rows per claimed span (a multiple of 32 x kBatch; smaller for
+  // small batches, so every warp gets spans)
   constexpr int kBatch = 4;
   // spans are claimed dynamically (the computed-row density varies along
   // the batch, so a static round-robin leaves SMs idle at the end)
@@ -334,21 +336,26 @@ int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* f
                 double* basis_gh, unsigned* work, int num_sms, cudaStream_t st) {
   if (n == 0) return 0;
   if (row_src && row_cost && !basis_gh) {
-    if (n * (int64_t)R / 2048 >= 0xFFFFFFFFll) return -1;
+    if (n * (int64_t)R / 128 >= 0xFFFFFFFFll) return -1;
     cudaMemsetAsync(work, 0, sizeof(unsigned), st);
     if (net.E > 64) return -1;
     const int smA = (GS_NUM_FEATURES * net.E + net.E * net.H + net.H * GS_NUM_COEFFS + net.E + GS_NUM_COEFFS +
                      GS_NUM_COEFFS * kRowsWarps * 32) * 8;
     const int64_t slabs = (n * (int64_t)R + kRowsWarps * 32 - 1) / (kRowsWarps * 32);
     const int gridA = (int)(slabs < (int64_t)num_sms ? slabs : (int64_t)num_sms);
+    // spans of 2,048 rows, down to 128 when the batch has fewer than four
+    // spans per warp (a 64K-candidate C2 step left most warps idle)
+    const int64_t rows_total = n * (int64_t)R, warps = (int64_t)gridA * kRowsWarps;
+    int64_t span = 2048;
+    while (span > 128 && rows_total / span < 4 * warps) span >>= 1;
     if (net.E <= 32) {
       cudaFuncSetAttribute(cost_rows_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smA);
       cost_rows_kernel<32><<<gridA, kRowsWarps * 32, smA, st>>>(net, stage_of_func, feats, row_key, n_rows, row_src,
-                                                                n, R, row_cost, work);
+                                                                n, R, row_cost, work, span);
     } else {
       cudaFuncSetAttribute(cost_rows_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smA);
       cost_rows_kernel<64><<<gridA, kRowsWarps * 32, smA, st>>>(net, stage_of_func, feats, row_key, n_rows, row_src,
-                                                                n, R, row_cost, work);
+                                                                n, R, row_cost, work, span);
     }
     g_launch_count++;
     int CB = 1024 / (R > 0 ? R : 1);
