@@ -275,28 +275,32 @@ def _expand_items(sc, candidates):
     return dec, where
 
 
-def _materialize(sc, dec, where, i):
-    """The host state of candidate i: the item itself, or — for a group —
-    the reference's own apply_decision of the device record's decision on
-    the parent (what the reference's _phase1/2_candidates would have built)."""
+def _materialize(sc, rows, where, idx):
+    """Host states of candidates `idx` (their device records already read
+    back as `rows`, one per index): the item itself, or — for a group — the
+    reference's own apply_decision of the record's decision on the parent
+    (what the reference's _phase1/2_candidates would have built)."""
     import bisect
-    firsts = [w[2] for w in where]
-    k = bisect.bisect_right(firsts, i) - 1
-    kind, item, first, _ = where[k]
-    if kind == "state":
-        return item
-    from gpusched.loopnest import Decision, apply_decision  # type: ignore
     from .descriptor import DECISION_DTYPE, KIND_NAME
-    rec = dec[i].cpu().numpy().view(DECISION_DTYPE)
-    fi = sc.packed.index[item.func]
-    r = rec[rec["func"] == fi][0]
-    fnode = sc.packed.graph.func(item.func)
-    nd = fnode.ndim
-    d = Decision(KIND_NAME[int(r["kind"])],
-                 consumer=None if r["consumer"] == 0xFFFF else sc.packed.names[int(r["consumer"])],
-                 serial=tuple(int(x) for x in r["serial"][:nd]) if r["flags"] & 1 else None,
-                 thread=tuple(int(x) for x in r["thread"][:nd]) if r["flags"] & 2 else None)
-    return apply_decision(item.parent, item.func, d)
+    firsts = [w[2] for w in where]
+    out = []
+    for i, raw in zip(idx, rows):
+        k = bisect.bisect_right(firsts, i) - 1
+        kind, item, first, _ = where[k]
+        if kind == "state":
+            out.append(item)
+            continue
+        from gpusched.loopnest import Decision, apply_decision  # type: ignore
+        rec = raw.view(DECISION_DTYPE)
+        fi = sc.packed.index[item.func]
+        r = rec[rec["func"] == fi][0]
+        nd = sc.packed.graph.func(item.func).ndim
+        d = Decision(KIND_NAME[int(r["kind"])],
+                     consumer=None if r["consumer"] == 0xFFFF else sc.packed.names[int(r["consumer"])],
+                     serial=tuple(int(x) for x in r["serial"][:nd]) if r["flags"] & 1 else None,
+                     thread=tuple(int(x) for x in r["thread"][:nd]) if r["flags"] & 2 else None)
+        out.append(apply_decision(item.parent, item.func, d))
+    return out
 
 
 def gpu_cut(candidates, evaluator, graph, config, pass_index, memo, phase_seed, validate):
@@ -332,7 +336,10 @@ def gpu_cut(candidates, evaluator, graph, config, pass_index, memo, phase_seed, 
     for depth, h in res.memo_new:
         memo.record(depth, h)
     if lazy:
-        beam = [_materialize(sc, dec, where, i).with_cost(c) for i, c in zip(res.beam, res.costs)]
+        bi = torch.tensor(res.beam, dtype=torch.int64, device=dec.device)
+        rows = dec.index_select(0, bi).cpu().numpy() if res.beam else []   # one read-back for the beam
+        states = _materialize(sc, rows, where, res.beam)
+        beam = [st.with_cost(c) for st, c in zip(states, res.costs)]
     else:
         beam = [candidates[i].with_cost(c) for i, c in zip(res.beam, res.costs)]
     if isinstance(evaluator, GpuCostEvaluator):
