@@ -242,6 +242,10 @@ def train(dataset: list, hyper=None, init=None):
     rng = np.random.default_rng(hyper.seed)
     order = np.stack([rng.permutation(len(dataset)) for _ in range(hyper.epochs)]).astype(np.int32) \
         if hyper.epochs > 0 else np.zeros((0, len(dataset)), dtype=np.int32)
+    for s in dataset:   # a sample without stages predicts 0: the reference raises on it
+        if not s.stages:
+            raise ValueError(f"non-finite or non-positive predicted cost for sample "
+                             f"{getattr(s, 'pipeline_id', '')}/{getattr(s, 'schedule_id', '')}")
     rows = [st for s in dataset for st in s.stages]
     off = np.zeros(len(dataset) + 1, dtype=np.int64)
     off[1:] = np.cumsum([len(s.stages) for s in dataset])
