@@ -2303,7 +2303,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     }
     __syncwarp();
     GS_MARK(6);
-    if (lane == 0) m.prev_valid = (m.err == 0) && feats != nullptr;
+    if (lane == 0) m.prev_valid = m.err == 0;   // geometry reuse holds with or without feature rows
     __syncwarp();
     pc = c;
   }

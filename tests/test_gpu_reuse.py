@@ -139,3 +139,31 @@ def test_rows_only_mode(src, parents, dev):
     with pytest.raises(ValueError):
         sc.cost(f2, reuse=False)
     sc.set_reuse(True)
+
+
+def test_prune_only_reuses_geometry_and_matches_featurize():
+    """Prune-only K1 (feats == NULL, `Scorer.prune`) resolves siblings
+    incrementally too, and its verdicts and row counts equal the featurizing
+    pass's on a C5 sample and on every golden candidate set."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import bench
+    from golden_io import PARAMS, available_sets, candidate_set, weights
+    from paper_2012_07145_b200.engine import Scorer
+    from paper_2012_07145_b200.params import DEFAULT_THRESHOLDS, MachineParams, init_weights
+    graph, recs, _ = bench._workload(60)
+    sc = Scorer(graph, MachineParams(), DEFAULT_THRESHOLDS, init_weights(0))
+    dec = sc.to_device(recs)
+    want = sc.featurize(dec)["verdict"]
+    sc.stats()
+    got = sc.prune(dec)
+    st = sc.stats()
+    sc.check()
+    assert torch.equal(got, want)
+    # small batches split runs into ~10-candidate units: one full resolve per unit
+    assert st["incremental"] >= 0.85 * len(recs)
+    for name in available_sets():
+        cs = candidate_set(name)
+        s2 = Scorer(cs.graph, PARAMS, cs.thresholds, weights())
+        d2 = s2.upload(cs.decisions)
+        assert torch.equal(s2.prune(d2), s2.featurize(d2)["verdict"]), name
