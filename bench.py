@@ -389,6 +389,27 @@ def run_gpu(args):
     sc.check()
 
     parity = bench_parity(sc, plan, dec, res) if world == 1 else {"checked": False, "why": "N > 1"}
+    extra = None
+    if world == 1 and not args.no_extras:
+        # what sibling reuse hides, and the other BASELINE configs (VERDICT
+        # r01 item 3): tools/bench_extras.py, each with the reference CPU path
+        # on the same candidates at 16 and 1 cores (after the timed region)
+        import io
+        import contextlib
+        import types
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_extras
+        plan.fbuf = plan.rcbuf = None
+        torch.cuda.empty_cache()
+        buf = io.StringIO()
+        ex_args = types.SimpleNamespace(only=None, cpu_seconds=args.cpu_seconds * (0 if args.no_cpu else 0.5),
+                                        no_cpu=args.no_cpu, stress_n=1_000_000)
+        try:
+            with contextlib.redirect_stdout(buf):
+                bench_extras.run_all(ex_args)
+            extra = [json.loads(x) for x in buf.getvalue().splitlines() if x.startswith("{")]
+        except Exception as e:   # extras never fail the headline line
+            extra = [{"error": repr(e)}]
     if rank == 0:
         R = sc.R
         n_local = plan.local_count
@@ -460,6 +481,7 @@ def run_gpu(args):
             "clocks": clk_summary,
             "beam": res["beam"][:8],
             "parity": parity,
+            "extra": extra,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -476,6 +498,7 @@ def main():
     ap.add_argument("--parents", type=int, default=PARENTS)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip tools/bench_extras.py's workloads")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -120,7 +120,10 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--stress-n", type=int, default=1_000_000)
-    args = ap.parse_args()
+    run_all(ap.parse_args())
+
+
+def run_all(args):
     args.cpu_rate = {"c2_unsharp": 300.0, "c2_harris": 150.0}
     args.cpu_skip = {"c4_resnet": "the reference featurizer materialises per-lane address tensors for the "
                                   "256-channel stride-0 windows (featurize.py:508-571) and exhausts host memory "
