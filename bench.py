@@ -452,6 +452,12 @@ def run_gpu(args):
         if world == 1 and not args.no_cpu:
             v, cores, kind, desc = cpu_reference(graph, recs, seconds=args.cpu_seconds)
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc}
+            try:
+                out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+                cpu["cpu_model"] = next((ln.split(":", 1)[1].strip() for ln in out.splitlines()
+                                         if ln.startswith("Model name")), None)
+            except Exception:
+                pass
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
