@@ -2027,8 +2027,8 @@ __device__ __forceinline__ void bulk_wait(uint64_t* bar) {
 // candidates (consecutive candidates of a beam step are siblings), keeping
 // its decision structure, geometry and scratch in its own slice of shared
 // memory; the candidate-independent pipeline descriptor is shared by the
-// CTA.  There is no CTA-wide barrier after the descriptor is staged, so the
-// serial parts of one candidate (resolve, prune) overlap other warps' rows.
+// CTA.  The warps take their candidates in lockstep: a CTA barrier separates
+// each candidate's resolve phase from its feature-row phase (see the main loop).
 
 template <int ND>
 __global__ void __launch_bounds__(kK1MaxWarps * 32, 1)
@@ -2153,34 +2153,12 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     __syncwarp();
   };
   bulk_wait(&bar);
-  __syncthreads();   // the only CTA barrier: descriptor staged
-  for (;;) {
-  unsigned uj = 0;
-  if (lane == 0) uj = atomicAdd(work, 1u);
-  const int64_t j = __shfl_sync(0xffffffffu, uj, 0);
-  int64_t c0, c1;
-  if (mode == 0) {
-    if (j >= nunits) break;
-    c0 = snap(j * unit); c1 = snap((j + 1) * unit);
-  } else if (mode == 1) {
-    if (j >= nruns) break;
-    c0 = run_head[j]; c1 = c0 + 1;
-  } else {
-    if (j >= nchunks) break;
-    if (j < nbig) { c0 = j * kChunk2; c1 = c0 + kChunk2; }
-    else { c0 = nbig * kChunk2 + (j - nbig) * kFine; c1 = c0 + kFine < n ? c0 + kFine : n; }
-  }
-  if (c0 >= c1) continue;
-  if (lane == 0) { m.prev_valid = 0; m.same_struct = 0; m.ndec = 0; }
-  __syncwarp();
-  int64_t pc = c0;          // the candidate this warp's state and feature rows follow
-  int64_t cur_run = -1;
-  for (int64_t c = c0; c < c1; ++c) {
-    if (mode == 2) {
-      if (heads[c]) { cur_run = -1; continue; }   // run heads: done in mode 1
-      const int64_t r = run_id[c];
-      if (r != cur_run) { slot_copy(r, false); pc = run_head[r]; cur_run = r; }
-    }
+  __syncthreads();   // descriptor staged
+  // Per-candidate work, in two phases: A (records, diff, resolve, prune,
+  // row flags) and B (rows and outputs).
+  int nr = 0, nd = 0;
+  bool diffable = false;
+  auto phaseA = [&](int64_t c, int64_t pc) {
     if (lane == 0) st_cand++;
 #ifdef GS_PHASES
     tph = clock64();
@@ -2220,7 +2198,11 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
       }
       __syncwarp();
       GS_MARK(0);
-      resolve<ND>(k);
+    }
+  };
+  auto phaseResolve = [&]() { resolve<ND>(k); };
+  auto phaseA2 = [&](int64_t c, int64_t pc) {
+    {
       GS_MARK(1);
       const int v = m.err ? 255 : prune_verdict<ND>(k);
       GS_MARK(2);
@@ -2231,11 +2213,11 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
       }
       __syncwarp();
     }
-    const int nr = feats ? m.nrows : 0;   // feats == NULL: prune verdict only
-    const bool diffable = m.same_struct && !m.err;
+    nr = feats ? m.nrows : 0;   // feats == NULL: prune verdict only
+    diffable = m.same_struct && !m.err;
     // rows to recompute: own func, host, host kernel, read producers and
     // fuse_at_thread children unchanged => features are bit-identical
-    int nd = 0;
+    nd = 0;
     for (int r0 = 0; r0 < nr; r0 += 32) {
       const int r = r0 + lane;
       bool d = false;
@@ -2260,6 +2242,8 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     }
     __syncwarp();
     if (lane == 0) { st_inc += m.same_struct; st_rows += nd; st_emit += nr; st_geo += m.ngeo; }
+  };
+  auto phaseB = [&](int64_t c, int64_t pc) {
     // a sibling starts from the previous candidate's feature block (this
     // warp wrote it: visible after __syncwarp), copied as one contiguous run
     // of 16-byte vectors with four loads in flight per lane; the dirty rows
@@ -2278,12 +2262,14 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
       __syncwarp();
     }
     GS_MARK(4);
-    for (int q = 0; q < nd; ++q) {
-      const int r = k.rowlist[q];
-      const int key = k.rows[r];
-      const int f = key >> 8, si = key & 255;
-      row_features<ND>(k, W, f, si, k.cf[f].kind == K_INLINE, feats + ((int64_t)c * L.R + r) * GS_NUM_FEATURES);
-    }
+  };
+  auto phaseRow = [&](int64_t c, int q) {
+    const int r = k.rowlist[q];
+    const int key = k.rows[r];
+    const int f = key >> 8, si = key & 255;
+    row_features<ND>(k, W, f, si, k.cf[f].kind == K_INLINE, feats + ((int64_t)c * L.R + r) * GS_NUM_FEATURES);
+  };
+  auto phaseB3 = [&](int64_t c) {
     GS_MARK(5);
     for (int r = lane; r < nr; r += 32) {
       row_key[c * L.R + r] = k.rows[r];
@@ -2305,9 +2291,74 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     GS_MARK(6);
     if (lane == 0) m.prev_valid = m.err == 0;   // geometry reuse holds with or without feature rows
     __syncwarp();
-    pc = c;
-  }
-  if (mode == 1) slot_copy(j, true);
+  };
+  // The CTA's warps take their candidates in lockstep: every warp runs
+  // phase A (records, diff, resolve, prune, row flags) for its next
+  // candidate, a CTA barrier, then phase B (feature rows and outputs), and a
+  // barrier again.  K1 is bound by instruction delivery (DESIGN.md §(d)):
+  // with all warps in the same phase the SM streams one phase's code at a
+  // time.  240K C5 candidates: 27.6 ms free-running, 25.1 ms in lockstep;
+  // a barrier around every feature row as well (load imbalance) measured
+  // 27.5 ms, and a separate resolve phase 25.1-25.3 ms.  Lockstep needs
+  // even work per candidate: sibling slices (modes 1, 2) or pipelines with
+  // many rows per candidate.  Random schedules of a small pipeline (C4:
+  // eight rows, some of them 256-channel windows) run free (the same loop
+  // without barriers): lockstep took C4's K1 from 88 to 122 ms.
+  const bool lockstep = mode != 0 || L.R >= 16;
+  {
+    int64_t c = 0, c1 = 0, pc = 0, cur_run = -1, jcur = -1;
+    bool done = false;
+    for (;;) {
+      bool have = false;
+      while (!done) {
+        if (c >= c1) {
+          if (mode == 1 && jcur >= 0) { slot_copy(jcur, true); jcur = -1; }
+          unsigned uj = 0;
+          if (lane == 0) uj = atomicAdd(work, 1u);
+          const int64_t j = __shfl_sync(0xffffffffu, uj, 0);
+          int64_t c0;
+          if (mode == 0) {
+            if (j >= nunits) { done = true; break; }
+            c0 = snap(j * unit); c1 = snap((j + 1) * unit);
+          } else if (mode == 1) {
+            if (j >= nruns) { done = true; break; }
+            c0 = run_head[j]; c1 = c0 + 1;
+          } else {
+            if (j >= nchunks) { done = true; break; }
+            if (j < nbig) { c0 = j * kChunk2; c1 = c0 + kChunk2; }
+            else { c0 = nbig * kChunk2 + (j - nbig) * kFine; c1 = c0 + kFine < n ? c0 + kFine : n; }
+          }
+          if (c0 >= c1) continue;
+          c = c0; pc = c0; cur_run = -1; jcur = j;
+          if (lane == 0) { m.prev_valid = 0; m.same_struct = 0; m.ndec = 0; }
+          __syncwarp();
+        }
+        if (mode == 2 && heads[c]) { cur_run = -1; ++c; continue; }
+        have = true;
+        break;
+      }
+      if (lockstep) {
+        if (!__syncthreads_or(have)) break;
+      } else if (!have) {
+        break;
+      }
+      if (have) {
+        if (mode == 2) {
+          const int64_t r = run_id[c];
+          if (r != cur_run) { slot_copy(r, false); pc = run_head[r]; cur_run = r; }
+        }
+        phaseA(c, pc);
+      }
+      if (have) { phaseResolve(); phaseA2(c, pc); }
+      if (lockstep) __syncthreads();
+      if (have) {
+        phaseB(c, pc);
+        for (int q = 0; q < nd; ++q) phaseRow(c, q);
+        phaseB3(c);
+        pc = c; ++c;
+      }
+      if (lockstep) __syncthreads();
+    }
   }
 #ifdef GS_PHASES
   if (lane == 0)
