@@ -322,12 +322,14 @@ struct K1Ws {
 };
 
 static int k1_plan(gs_pipeline_t p, int64_t n, int S, bool feats, int reuse, K1Plan& kp) {
-  bool spill = false;
-  int nwarps = std::min(p->nwarps, featurize_warps(layout_for(p, S, 1, false), p->max_smem));
-  if (nwarps < 4) {
-    spill = true;
-    nwarps = std::min(p->nwarps, featurize_warps(layout_for(p, S, 1, true), p->max_smem));
-  }
+  // the capacity-sized structure arrays go to the warp's global scratch when
+  // that buys more scorer warps (or when fewer than 4 would fit otherwise);
+  // GS_K1_SPILL=0/1 forces the choice (diagnostics)
+  const int w_smem = std::min(p->nwarps, featurize_warps(layout_for(p, S, 1, false), p->max_smem));
+  const int w_spill = std::min(p->nwarps, featurize_warps(layout_for(p, S, 1, true), p->max_smem));
+  bool spill = w_spill > w_smem;
+  if (const char* e = getenv("GS_K1_SPILL")) spill = atoi(e) != 0;
+  int nwarps = spill ? w_spill : w_smem;
   if (nwarps < 1)
     return fail(GS_ERR_CAPACITY, "pipeline too large for one warp's shared-memory slice (" +
                                      std::to_string(layout_for(p, S, 1, true).total) + " > " +

@@ -2088,11 +2088,11 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   k.kern = reinterpret_cast<int16_t*>(ws + L.kern);
   k.dm = reinterpret_cast<uint32_t*>(wgs + L.dm);          // dependency masks: global (L1)
   k.cmask = reinterpret_cast<uint32_t*>(ws + L.cmask);
-  k.kmb = reinterpret_cast<int32_t*>(ws + L.kmb);
-  k.kml = reinterpret_cast<int16_t*>(ws + L.kml);
-  k.icb = reinterpret_cast<int32_t*>(ws + L.icb);
+  k.kmb = reinterpret_cast<int32_t*>(wg + L.kmb);
+  k.kml = reinterpret_cast<int16_t*>(wg + L.kml);
+  k.icb = reinterpret_cast<int32_t*>(wg + L.icb);
   k.icl = reinterpret_cast<int16_t*>(wgs + L.icl);
-  k.dlist = reinterpret_cast<int16_t*>(ws + L.dlist);
+  k.dlist = reinterpret_cast<int16_t*>(wg + L.dlist);
   k.gdirty = reinterpret_cast<uint8_t*>(ws + L.gdirty);
   k.kdirty = reinterpret_cast<uint8_t*>(ws + L.kdirty);
   k.misc = reinterpret_cast<Misc*>(ws + L.misc);
@@ -2453,11 +2453,11 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   L.kern = o; o += al(nf * 2);
   L.dm = gplace(nf * L.mw * 4);
   L.cmask = o; o += al(kMaxMaskWords * 4);
-  L.kmb = o; o += al((nf + 1) * 4);
-  L.kml = o; o += al(nf * 2);
-  L.icb = o; o += al((nf + 1) * 4);
+  L.kmb = place((nf + 1) * 4);
+  L.kml = place(nf * 2);
+  L.icb = place((nf + 1) * 4);
   L.icl = gplace(pcap * 2);
-  L.dlist = o; o += al(nf * 2);
+  L.dlist = place(nf * 2);
   L.gdirty = o; o += al(nf);
   L.kdirty = o; o += al(nf);
   L.misc = o; o += al((int)sizeof(Misc));

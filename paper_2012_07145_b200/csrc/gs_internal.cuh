@@ -15,7 +15,7 @@ constexpr int kMaxM = 128;          // largest residue modulus (transaction / ba
 constexpr int kRowReads = 64;       // reads attributed to one row
 constexpr int kGroupReads = 16;     // reads in one (tier, producer) group
 constexpr int kLaneIv = 96;         // per-lane interval capacity for unions
-constexpr int kK1MaxWarps = 10;      // K1 warps per CTA (one CTA per SM)
+constexpr int kK1MaxWarps = 12;      // K1 warps per CTA (one CTA per SM)
 constexpr int kUnit = 64;           // K1 work-unit size (candidates, before run-head snapping)
 constexpr int kChunk2 = 16;         // K1 two-phase schedule: sibling slice size
 constexpr int64_t kAddrBias = int64_t(1) << 40;  // featurize.py:256
