@@ -2308,9 +2308,37 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   {
     int64_t c = 0, c1 = 0, pc = 0, cur_run = -1, jcur = -1;
     bool done = false;
+    // sibling slices: the CTA's warps take nw consecutive slices together
+    // (mostly one run: the same decision structure and dirty rows, so the
+    // warps run the same instruction stream), the next block once all are
+    // done.  240K C5 candidates: 24.9 ms claiming per warp, 23.0 ms per CTA.
+    __shared__ int64_t s_base;
+    const bool cta_blocks = mode == 2 && lockstep;
     for (;;) {
       bool have = false;
-      while (!done) {
+      if (cta_blocks) {
+        while (c < c1 && heads[c]) { cur_run = -1; ++c; }
+        if (__syncthreads_and(c >= c1)) {
+          if (threadIdx.x == 0) s_base = (int64_t)atomicAdd(work, (unsigned)nw);
+          __syncthreads();
+          const int64_t base = s_base;
+          __syncthreads();
+          if (base >= nchunks) break;
+          const int64_t j = base + warp;
+          c = c1 = 0;
+          if (j < nchunks) {
+            int64_t c0;
+            if (j < nbig) { c0 = j * kChunk2; c1 = c0 + kChunk2; }
+            else { c0 = nbig * kChunk2 + (j - nbig) * kFine; c1 = c0 + kFine < n ? c0 + kFine : n; }
+            c = c0; pc = c0; cur_run = -1;
+            if (lane == 0) { m.prev_valid = 0; m.same_struct = 0; m.ndec = 0; }
+            __syncwarp();
+            while (c < c1 && heads[c]) { cur_run = -1; ++c; }
+          }
+        }
+        have = c < c1;
+      }
+      while (!done && !cta_blocks) {
         if (c >= c1) {
           if (mode == 1 && jcur >= 0) { slot_copy(jcur, true); jcur = -1; }
           unsigned uj = 0;
@@ -2337,7 +2365,9 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
         have = true;
         break;
       }
-      if (lockstep) {
+      if (cta_blocks) {
+        if (!__syncthreads_or(have)) continue;   // a block of head-only slices: claim the next
+      } else if (lockstep) {
         if (!__syncthreads_or(have)) break;
       } else if (!have) {
         break;
