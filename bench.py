@@ -453,8 +453,8 @@ def run_gpu(args):
             v, cores, kind, desc = cpu_reference(graph, recs, seconds=args.cpu_seconds)
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc}
             try:
-                out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
-                cpu["cpu_model"] = next((ln.split(":", 1)[1].strip() for ln in out.splitlines()
+                lscpu = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+                cpu["cpu_model"] = next((ln.split(":", 1)[1].strip() for ln in lscpu.splitlines()
                                          if ln.startswith("Model name")), None)
             except Exception:
                 pass
