@@ -176,13 +176,20 @@ __global__ void k4_buckets(const uint64_t* __restrict__ skey, const uint32_t* __
   }
 }
 
+constexpr uint32_t kBigBucket = 1024;          // buckets walked by a CTA (k4_walk_big)
+constexpr int kWalkSmemEntries = 50 * 1024;   // 200 KB of u32: a big bucket's permutation in shared memory
+
+// quota = max(1, floor(log2 B)); buckets of >= kBigBucket members are also
+// listed for k4_walk_big (in any order: buckets are independent)
 __global__ void k4_quota(const uint32_t* __restrict__ bstart, const uint32_t* __restrict__ cum,
-                         const uint32_t* __restrict__ nb_dev, uint32_t* __restrict__ quota) {
+                         const uint32_t* __restrict__ nb_dev, uint32_t* __restrict__ quota,
+                         uint32_t* __restrict__ big, uint32_t* __restrict__ big_cnt) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= (int64_t)*nb_dev) return;
   const uint32_t B = cum[bstart[b + 1]] - cum[bstart[b]];
   const int q = 63 - __clzll((unsigned long long)B);   // floor(log2 B)
   quota[b] = q < 1 ? 1u : (uint32_t)q;
+  if (B >= kBigBucket) big[atomicAdd(big_cnt, 1u)] = (uint32_t)b;
 }
 
 // numpy default_rng((phase_seed, h)).permutation(B) (Fisher-Yates with
@@ -231,8 +238,6 @@ __device__ __forceinline__ void walk_bucket(int64_t b, uint32_t* p, const uint64
 
 // Small buckets: one thread each, the permutation in global memory (the
 // bucket's slice of `perm`).
-constexpr uint32_t kBigBucket = 1024;
-constexpr int kWalkSmemEntries = 50 * 1024;   // 200 KB of u32: a big bucket's permutation in shared memory
 
 __global__ void k4_walk(const uint64_t* __restrict__ skey, const uint32_t* __restrict__ sval,
                         const uint32_t* __restrict__ rstart, const uint32_t* __restrict__ cum,
@@ -264,14 +269,15 @@ __global__ void __launch_bounds__(256) k4_walk_big(
     const uint32_t* __restrict__ cum, const uint32_t* __restrict__ bstart, const uint32_t* __restrict__ nb_dev,
     const uint32_t* __restrict__ qoff, const uint32_t* __restrict__ quota, const uint8_t* __restrict__ verdict,
     uint64_t phase_seed, uint32_t* __restrict__ perm, int64_t* __restrict__ slot, uint32_t* __restrict__ taken,
-    int64_t* __restrict__ rej, uint32_t* __restrict__ rejn) {
+    int64_t* __restrict__ rej, uint32_t* __restrict__ rejn, const uint32_t* __restrict__ big,
+    const uint32_t* __restrict__ big_cnt) {
   extern __shared__ uint32_t ps[];
   __shared__ uint32_t vbits[kWalkBits];
-  const int64_t nb = *nb_dev;
-  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+  const int64_t nbig = *big_cnt;
+  for (int64_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+    const int64_t b = big[bi];
     const uint32_t r0 = bstart[b], r1 = bstart[b + 1];
     const uint32_t s0 = cum[r0], B = cum[r1] - s0;
-    if (B < kBigBucket) continue;   // uniform over the CTA
     if (B > (uint32_t)kWalkSmemEntries) {
       if (threadIdx.x == 0)
         walk_bucket(b, perm + s0, skey, sval, rstart, cum, bstart, qoff, quota, verdict, phase_seed, false, slot,
@@ -354,7 +360,7 @@ __global__ void k4_gather(const uint32_t* __restrict__ nb_dev, const uint32_t* _
 // workspace carve-up for K4 (every array sized for the candidate count n)
 struct SelWs {
   uint32_t *head, *runid, *rstart, *len, *cum, *bhead, *bid, *bstart, *quota, *qoff, *taken, *toff, *rejn,
-      *roff, *perm, *sums, *hist, *cnt;   // cnt: m, nb, total reps, total rejects
+      *roff, *perm, *sums, *hist, *cnt, *big;   // cnt: m, nb, total reps, total rejects, big buckets
   uint32_t *rval, *rval2;
   uint64_t *rkey, *rkey2;
   int64_t *slot, *rej;
@@ -388,7 +394,8 @@ static size_t carve(SelWs& w, void* base, int64_t n) {
   w.hist = (uint32_t*)take(rs_hist_bytes(n));
   const size_t sb = std::max(rs_sums_bytes(n), align256(4 * (scan_tiles_of(n) + 1)));
   w.sums = (uint32_t*)take(sb);
-  w.cnt = (uint32_t*)take(16);
+  w.cnt = (uint32_t*)take(32);
+  w.big = (uint32_t*)take(4 * (n / kBigBucket + 1));
   return o;
 }
 
@@ -410,7 +417,7 @@ int select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, uint6
   if ((int64_t)carve(w, ws, n) > ws_bytes) return -2;
   const int T = 256;
   const unsigned G = (unsigned)((n + T - 1) / T);
-  uint32_t *m_dev = w.cnt, *nb_dev = w.cnt + 1, *tot_reps = w.cnt + 2, *tot_rej = w.cnt + 3;
+  uint32_t *m_dev = w.cnt, *nb_dev = w.cnt + 1, *tot_reps = w.cnt + 2, *tot_rej = w.cnt + 3, *big_cnt = w.cnt + 4;
   k4_heads<<<G, T, 0, st>>>(hashes, n, w.head); g_launch_count++;
   scan_u32(w.head, w.runid, n, nullptr, false, w.sums, m_dev, st);
   k4_runs<<<G, T, 0, st>>>(hashes, n, w.runid, w.rkey, w.rval, w.rstart); g_launch_count++;
@@ -419,7 +426,8 @@ int select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, uint6
   scan_u32(w.len, w.cum, n, m_dev, false, w.sums, nullptr, st);
   scan_u32(w.bhead, w.bid, n, m_dev, false, w.sums, nullptr, st);
   k4_buckets<<<G, T, 0, st>>>(w.rkey, w.bid, m_dev, n, w.bstart, w.cum, nb_dev); g_launch_count++;
-  k4_quota<<<G, T, 0, st>>>(w.bstart, w.cum, nb_dev, w.quota); g_launch_count++;
+  cudaMemsetAsync(big_cnt, 0, 4, st);
+  k4_quota<<<G, T, 0, st>>>(w.bstart, w.cum, nb_dev, w.quota, w.big, big_cnt); g_launch_count++;
   scan_u32(w.quota, w.qoff, n, nb_dev, false, w.sums, nullptr, st);
   k4_walk<<<G, 64, 0, st>>>(w.rkey, w.rval, w.rstart, w.cum, w.bstart, nb_dev, w.qoff, w.quota, verdict,
                             phase_seed, w.perm, w.slot, w.taken, w.rej, w.rejn); g_launch_count++;
@@ -432,10 +440,10 @@ int select_reps(const uint64_t* hashes, const uint8_t* verdict, int64_t n, uint6
       attr = true;
     }
     const int64_t maxbig = n / kBigBucket;
-    const unsigned gb = (unsigned)(maxbig < 512 ? maxbig : 512);
+    const unsigned gb = (unsigned)(maxbig < 296 ? maxbig : 296);
     k4_walk_big<<<gb, 256, 4 * kWalkSmemEntries, st>>>(w.rkey, w.rval, w.rstart, w.cum, w.bstart, nb_dev, w.qoff,
                                                        w.quota, verdict, phase_seed, w.perm, w.slot, w.taken, w.rej,
-                                                       w.rejn);
+                                                       w.rejn, w.big, big_cnt);
     g_launch_count++;
   }
   scan_u32(w.taken, w.toff, n, nb_dev, false, w.sums, tot_reps, st);
