@@ -92,6 +92,8 @@ struct GsPipeline {
   std::vector<double*> wbufs;
   int num_sms = 0;
   int max_smem = 0;
+  int sm_smem = 0;       // shared memory per SM
+  int cta_reserved = 0;  // shared memory the runtime reserves per CTA
   int rcap = 0, pcap = 0;
   int reuse = 1;
   int nwarps = getenv("GS_K1_WARPS") ? atoi(getenv("GS_K1_WARPS")) : kK1MaxWarps;   // diagnostics override
@@ -199,6 +201,8 @@ int gs_pipeline_create(const GsPipelineDesc* d, gs_pipeline_t* out) {
   CK(cudaGetDeviceProperties(&prop, dev));
   p->num_sms = prop.multiProcessorCount;
   p->max_smem = (int)prop.sharedMemPerBlockOptin;
+  p->sm_smem = (int)prop.sharedMemPerMultiprocessor;
+  p->cta_reserved = (int)prop.reservedSharedMemPerBlock;
   CK(cudaMalloc(&p->dev, sizeof(PipeDev)));
   CK(cudaMemcpy(p->dev, &h, sizeof(PipeDev), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&p->blob, h.blob_bytes));
@@ -303,9 +307,12 @@ int gs_get_reuse(gs_pipeline_t p) { return p ? p->reuse : -1; }
 // the kernel falls back to the one-phase schedule when the batch has more
 // runs, or runs shorter than 8 on average).
 struct K1Plan {
-  Layout L;
+  Layout L;              // modes 0 / 1 (one CTA per SM, as many warps as fit)
   int nwarps = 0;
   int64_t grid = 0;
+  Layout L2;             // mode 2 (sibling slices): several smaller CTAs per SM
+  int nwarps2 = 0;
+  int64_t grid2 = 0;
   bool two_phase = false;
   int64_t slot_bytes = 0;
 };
@@ -322,22 +329,47 @@ struct K1Ws {
 };
 
 static int k1_plan(gs_pipeline_t p, int64_t n, int S, bool feats, int reuse, K1Plan& kp) {
-  // the capacity-sized structure arrays go to the warp's global scratch when
-  // that buys more scorer warps (or when fewer than 4 would fit otherwise);
-  // GS_K1_SPILL=0/1 forces the choice (diagnostics)
-  const int w_smem = std::min(p->nwarps, featurize_warps(layout_for(p, S, 1, false), p->max_smem));
-  const int w_spill = std::min(p->nwarps, featurize_warps(layout_for(p, S, 1, true), p->max_smem));
-  bool spill = w_spill > w_smem;
+  // Launch shapes (CTAs per SM x scorer warps per CTA).  The warps of a CTA
+  // work in lockstep (featurize_kernel).  Sibling slices (mode 2) run best
+  // as two CTAs per SM, one CTA's warps issuing while the other's wait at a
+  // barrier; 240K C5 candidates: 12 warps x 1 CTA 23.1 ms, 5 x 2 22.1 ms,
+  // 4 x 2 22.8 ms, 2 x 6 23.8 ms.  Whole-candidate work (modes 0 / 1:
+  // random schedules, reuse off, run heads) runs best with the most warps
+  // in one CTA (the 1M stress batch: 2.2 s as 12 x 1, 2.7 s as 5 x 2).
+  // Both launches of the two-phase schedule share one slice layout (the
+  // run-head launch saves warp states the sibling launch restores), so they
+  // share the spill choice: the capacity-sized structure arrays go to the
+  // warp's global scratch when that buys more warps.  GS_K1_CTAS (sibling
+  // launch) / GS_K1_SPILL force the choice (diagnostics).  Registers cap a
+  // SM at kK1MaxWarps warps.
+  auto fit = [&](int ctas, bool spill) {
+    const Layout L1 = layout_for(p, S, 1, spill);
+    const int per_cta = (p->sm_smem / ctas) - p->cta_reserved;
+    const int budget = std::min(per_cta, p->max_smem) - L1.warps;
+    const int w = budget > 0 ? budget / L1.warp_bytes : 0;
+    return std::min({w, p->nwarps, kK1MaxWarps / ctas});
+  };
+  kp.two_phase = reuse && feats && n >= 8192;
+  bool spill = fit(1, true) > fit(1, false);
+  int ctas2 = 1;
+  if (kp.two_phase) {
+    ctas2 = 2;
+    if (const char* e = getenv("GS_K1_CTAS")) ctas2 = std::max(1, atoi(e));
+    spill = fit(ctas2, true) > fit(ctas2, false) || fit(1, true) > fit(1, false);
+    if (fit(ctas2, spill) < 3) ctas2 = 1;   // too big for several CTAs per SM
+  }
   if (const char* e = getenv("GS_K1_SPILL")) spill = atoi(e) != 0;
-  int nwarps = spill ? w_spill : w_smem;
+  const int nwarps = fit(1, spill);
   if (nwarps < 1)
     return fail(GS_ERR_CAPACITY, "pipeline too large for one warp's shared-memory slice (" +
                                      std::to_string(layout_for(p, S, 1, true).total) + " > " +
                                      std::to_string(p->max_smem) + " bytes)");
   kp.L = layout_for(p, S, nwarps, spill);
   kp.nwarps = nwarps;
-  kp.grid = std::max<int64_t>(1, std::min<int64_t>(p->num_sms, (n + nwarps - 1) / nwarps));
-  kp.two_phase = reuse && feats && n >= 8192;
+  kp.grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)p->num_sms, (n + nwarps - 1) / nwarps));
+  kp.nwarps2 = std::max(1, fit(ctas2, spill));
+  kp.L2 = layout_for(p, S, kp.nwarps2, spill);
+  kp.grid2 = std::max<int64_t>(1, std::min<int64_t>((int64_t)p->num_sms * ctas2, (n + kp.nwarps2 - 1) / kp.nwarps2));
   kp.slot_bytes = (int64_t)kp.L.warp_bytes + kp.L.gl_bytes;
   return GS_OK;
 }
@@ -350,7 +382,7 @@ static int64_t k1_default_runs(const K1Plan& kp, int64_t n) {
 static int64_t k1_carve(const K1Plan& kp, int64_t n, int64_t max_runs, uint8_t* base, K1Ws& w) {
   int64_t o = 0;
   auto take = [&](int64_t bytes) { uint8_t* r = base ? base + o : nullptr; o += (bytes + 255) & ~(int64_t)255; return r; };
-  w.gscratch = take(kp.grid * kp.nwarps * (int64_t)kp.L.gl_bytes);
+  w.gscratch = take(std::max(kp.grid * kp.nwarps, kp.grid2 * kp.nwarps2) * (int64_t)kp.L.gl_bytes);
   w.heads = take(std::max<int64_t>(1, n));
   w.max_runs = 0;
   if (kp.two_phase) {
@@ -379,9 +411,10 @@ static int featurize_impl(gs_pipeline_t p, const GsDecision* dec, int64_t n, int
     // across warps without re-resolving
     k1_prepare_runs(dec, n, S, w.heads, w.run_id, w.run_head, w.sums, w.nruns, st);
     for (int mode = 1; mode <= 2 && !rc; ++mode)
-      rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, kp.L,
-                            kp.nwarps, (int)kp.grid, p->err, reuse, w.gscratch, w.heads, mode, w.run_id, w.run_head,
-                            w.nruns, w.max_runs, w.slots, kp.slot_bytes, row_kernel, st);
+      rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src,
+                            mode == 1 ? kp.L : kp.L2, mode == 1 ? kp.nwarps : kp.nwarps2,
+                            (int)(mode == 1 ? kp.grid : kp.grid2), p->err, reuse, w.gscratch, w.heads, mode, w.run_id,
+                            w.run_head, w.nruns, w.max_runs, w.slots, kp.slot_bytes, row_kernel, st);
   } else {
     rc = launch_featurize(p->host.nd, p->dev, p->blob, dec, n, S, feats, row_key, n_rows, verdict, row_src, kp.L,
                           kp.nwarps, (int)kp.grid, p->err, reuse, w.gscratch, w.heads, 0, nullptr, nullptr, nullptr,
