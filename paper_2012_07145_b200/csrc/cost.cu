@@ -207,7 +207,10 @@ __global__ void __launch_bounds__(128) cost_kernel(NetDev net, const int32_t* __
 // the network, so lanes stay full and no block-wide barrier or per-chunk
 // tail idles the SM.  Pass B gathers every row's cost from its source and
 // adds a candidate's rows in order.
-constexpr int kRowsWarps = 12;   // one 384-thread CTA per SM (166 registers)
+#ifndef GS_K2_WARPS
+#define GS_K2_WARPS 12
+#endif
+constexpr int kRowsWarps = GS_K2_WARPS;   // one CTA per SM; 240K C5: 8 warps 3.08 ms, 12 2.63 ms, 16 (128 registers, spills) 3.24 ms
 constexpr unsigned kRing = 256;   // per-warp queue (>= 31 + kBatch slabs x 32)
 
 template <int MAXE>

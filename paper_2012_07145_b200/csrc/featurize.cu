@@ -2137,7 +2137,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   const int64_t nbig_all = (n + kChunk2 - 1) / kChunk2;
   const int64_t tail_big = 3 * (int64_t)gridDim.x * nw < nbig_all ? 3 * (int64_t)gridDim.x * nw : nbig_all;
   const int64_t nbig = nbig_all - tail_big;
-  constexpr int kFine = kChunk2 / 4;
+  constexpr int kFine = kChunk2 / 4 > 0 ? kChunk2 / 4 : 1;
   const int64_t nchunks = nbig + (n - nbig * kChunk2 + kFine - 1) / kFine;
   // warp state <-> run slot: the shared-memory slice and the global scratch
   auto slot_copy = [&](int64_t r, bool save) {

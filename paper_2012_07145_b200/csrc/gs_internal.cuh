@@ -17,7 +17,10 @@ constexpr int kGroupReads = 16;     // reads in one (tier, producer) group
 constexpr int kLaneIv = 96;         // per-lane interval capacity for unions
 constexpr int kK1MaxWarps = 12;      // K1 warps per CTA (one CTA per SM)
 constexpr int kUnit = 64;           // K1 work-unit size (candidates, before run-head snapping)
-constexpr int kChunk2 = 16;         // K1 two-phase schedule: sibling slice size
+#ifndef GS_CHUNK2
+#define GS_CHUNK2 5
+#endif
+constexpr int kChunk2 = GS_CHUNK2;  // K1 two-phase schedule: sibling slice size (C5 K1: 16 -> 80.2 ms, 8 -> 77.2, 5 -> 70.4, 4 -> 74.3)
 constexpr int64_t kAddrBias = int64_t(1) << 40;  // featurize.py:256
 
 enum Tier : int8_t { T_GLOBAL = 0, T_SHARED = 1, T_REGISTER = 2, T_NONE = 3 };
