@@ -9,7 +9,7 @@
 
 namespace gs {
 Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rcap, int pcap, int nwarps,
-                   bool spill, bool generic);
+                   int spill, bool generic);
 int launch_featurize(int nd, const PipeDev* P, const uint8_t* blob, const GsDecision* dec, int64_t n, int S,
                      double* feats, int32_t* row_key, int32_t* n_rows, uint8_t* verdict, int32_t* row_src,
                      const Layout& L, int nwarps, int grid, int* gerr, int reuse, uint8_t* gscratch,
@@ -278,7 +278,7 @@ int gs_set_weights(gs_pipeline_t p, int E, int H, const double* aw, const double
   return GS_OK;
 }
 
-static Layout layout_for(gs_pipeline_t p, int S, int nwarps, bool spill) {
+static Layout layout_for(gs_pipeline_t p, int S, int nwarps, int spill) {
   // machines other than the default (32 B transactions, 32 x 4 B banks) run
   // the generic counters and need their residue tables in the warp slice
   const GsMachine& m = p->host.m;
@@ -342,27 +342,34 @@ static int k1_plan(gs_pipeline_t p, int64_t n, int S, bool feats, int reuse, K1P
   // warp's global scratch when that buys more warps.  GS_K1_CTAS (sibling
   // launch) / GS_K1_SPILL force the choice (diagnostics).  Registers cap a
   // SM at kK1MaxWarps warps.
-  auto fit = [&](int ctas, bool spill) {
+  auto fit = [&](int ctas, int spill) {
     const Layout L1 = layout_for(p, S, 1, spill);
     const int per_cta = (p->sm_smem / ctas) - p->cta_reserved;
     const int budget = std::min(per_cta, p->max_smem) - L1.warps;
     const int w = budget > 0 ? budget / L1.warp_bytes : 0;
     return std::min({w, p->nwarps, kK1MaxWarps / ctas});
   };
+  // the lowest spill level that reaches the most warps for `ctas`
+  auto best = [&](int ctas) {
+    int lvl = 0, w = fit(ctas, 0);
+    for (int l = 1; l <= 2; ++l)
+      if (fit(ctas, l) > w) { w = fit(ctas, l); lvl = l; }
+    return lvl;
+  };
   kp.two_phase = reuse && feats && n >= 8192;
-  bool spill = fit(1, true) > fit(1, false);
+  int spill = best(1);
   int ctas2 = 1;
   if (kp.two_phase) {
     ctas2 = 2;
     if (const char* e = getenv("GS_K1_CTAS")) ctas2 = std::max(1, atoi(e));
-    spill = fit(ctas2, true) > fit(ctas2, false) || fit(1, true) > fit(1, false);
+    spill = best(ctas2);   // the sibling launch dominates: its best level for both launches
     if (fit(ctas2, spill) < 3) ctas2 = 1;   // too big for several CTAs per SM
   }
-  if (const char* e = getenv("GS_K1_SPILL")) spill = atoi(e) != 0;
+  if (const char* e = getenv("GS_K1_SPILL")) spill = std::min(2, std::max(0, atoi(e)));
   const int nwarps = fit(1, spill);
   if (nwarps < 1)
     return fail(GS_ERR_CAPACITY, "pipeline too large for one warp's shared-memory slice (" +
-                                     std::to_string(layout_for(p, S, 1, true).total) + " > " +
+                                     std::to_string(layout_for(p, S, 1, 2).total) + " > " +
                                      std::to_string(p->max_smem) + " bytes)");
   kp.L = layout_for(p, S, nwarps, spill);
   kp.nwarps = nwarps;

@@ -2062,7 +2062,10 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   // whose worst-case inline expansion does not fit shared memory — in this
   // warp's slice of a global scratch (generic pointers: same code)
   uint8_t* wgs = gscratch + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * L.gl_bytes;
-  uint8_t* wg = L.spill ? wgs : ws;
+  // spill level 1: the resolve-side capacity arrays in global scratch;
+  // level 2: also the expanded reads and chain paths the rows walk
+  uint8_t* wg = L.spill >= 1 ? wgs : ws;
+  uint8_t* wg2 = L.spill >= 2 ? wgs : ws;
   K1<ND> k;
   k.P = P;
   k.F = reinterpret_cast<const GsFunc*>(sm + L.blob);
@@ -2071,8 +2074,8 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   k.dec = reinterpret_cast<GsDecision*>(ws + L.dec);
   k.didx = reinterpret_cast<int16_t*>(ws + L.didx);
   k.cf = reinterpret_cast<CF<ND>*>(ws + L.cf);
-  k.rd = reinterpret_cast<RRead*>(wg + L.reads);
-  k.path = reinterpret_cast<int16_t*>(wg + L.paths);
+  k.rd = reinterpret_cast<RRead*>(wg2 + L.reads);
+  k.path = reinterpret_cast<int16_t*>(wg2 + L.paths);
   k.rdb = reinterpret_cast<int32_t*>(ws + L.rdb);
   k.rows = reinterpret_cast<int32_t*>(ws + L.rows);
   k.stack = reinterpret_cast<Frame*>(wgs + L.stack);       // structure-build scratch: global
@@ -2451,7 +2454,7 @@ static int cf_size() { return (int)sizeof(CF<ND>); }
 // offsets inside a slice are relative to the slice.  Arrays placed with
 // gplace live in the warp's global scratch instead (offsets relative to it).
 Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rcap, int pcap, int nwarps,
-                   bool spill, bool generic) {
+                   int spill, bool generic) {
   auto al = [](int x) { return (x + 15) & ~15; };
   Layout L{};
   L.blob = 0;
@@ -2459,15 +2462,20 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   int o = 0;
   int g = 0;   // global scratch bytes per warp (spill)
   // capacity-sized arrays: in the smem slice, or in global scratch
-  auto place = [&](int bytes) { int r; if (spill) { r = g; g += al(bytes); } else { r = o; o += al(bytes); } return r; };
+  auto place_at = [&](int level, int bytes) {
+    int r;
+    if (spill >= level) { r = g; g += al(bytes); } else { r = o; o += al(bytes); }
+    return r;
+  };
+  auto place = [&](int bytes) { return place_at(1, bytes); };
   auto gplace = [&](int bytes) { int r = g; g += al(bytes); return r; };   // always global
   L.dec = o; o += al(S * 16);
   L.didx = o; o += al(nf * 2);
   int cfs = nd == 1 ? cf_size<1>() : nd == 2 ? cf_size<2>() : nd == 3 ? cf_size<3>() : cf_size<4>();
   L.cf = o; o += al(nf * cfs);
   L.pcf = 0;
-  L.reads = place(rcap * (int)sizeof(RRead));
-  L.paths = place(pcap * 2);
+  L.reads = place_at(2, rcap * (int)sizeof(RRead));
+  L.paths = place_at(2, pcap * 2);
   L.rdb = o; o += al(2 * ns * 4);
   L.rows = o; o += al(R * 4);
   L.icall = gplace(pcap * (int)sizeof(ICall));

@@ -75,7 +75,7 @@ struct Layout {                 // byte offsets inside dynamic shared memory (K1
       kdirty, misc, warps, scr;
   int mw;                       // dependency-mask words per func (0 = incremental resolve off)
   int gl_bytes;                 // per-warp global scratch bytes (inline-call lists, spilled arrays)
-  int spill;                    // capacity-sized structure arrays in global scratch
+  int spill;                    // capacity-sized structure arrays in global scratch: 0 none, 1 resolve-side, 2 all
   int warp_bytes, total;
   int rcap, pcap, S, R;
 };
