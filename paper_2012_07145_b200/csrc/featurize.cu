@@ -2085,7 +2085,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   k.srcb = reinterpret_cast<int32_t*>(ws + L.srcb);
   k.srcl = reinterpret_cast<int16_t*>(wg + L.srcl);
   k.rdepb = reinterpret_cast<int32_t*>(ws + L.rdepb);
-  k.rdep = reinterpret_cast<int16_t*>(wg + L.rdep);
+  k.rdep = reinterpret_cast<int16_t*>(wg2 + L.rdep);
   k.dirty = reinterpret_cast<uint8_t*>(ws + L.dirty);
   k.rowlist = reinterpret_cast<int16_t*>(ws + L.rowlist);
   k.kern = reinterpret_cast<int16_t*>(ws + L.kern);
@@ -2482,7 +2482,7 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   L.srcb = o; o += al((nf + 1) * 4);
   L.srcl = place(rcap * 2);
   L.rdepb = o; o += al((R + 1) * 4);
-  L.rdep = place((rcap + nf) * 2);
+  L.rdep = place_at(2, (rcap + nf) * 2);
   L.dirty = o; o += al(nf);
   L.rflag = o; o += al(R);
   L.rowlist = o; o += al(R * 2);
