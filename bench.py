@@ -309,9 +309,16 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU over NCCL; GS_DIST_BACKEND=gloo (and ranks sharing a
+    # device) lets a one-GPU box exercise the N > 1 path (tests, diagnostics)
+    backend = os.environ.get("GS_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     graph, recs, info = _workload(args.parents)
     N = int(recs.shape[0])
     lib = _lib.load()
