@@ -377,7 +377,7 @@ static int k1_plan(gs_pipeline_t p, int64_t n, int S, bool feats, int reuse, K1P
   kp.nwarps2 = std::max(1, fit(ctas2, spill));
   kp.L2 = layout_for(p, S, kp.nwarps2, spill);
   kp.grid2 = std::max<int64_t>(1, std::min<int64_t>((int64_t)p->num_sms * ctas2, (n + kp.nwarps2 - 1) / kp.nwarps2));
-  kp.slot_bytes = (int64_t)kp.L.warp_bytes + kp.L.gl_bytes;
+  kp.slot_bytes = (int64_t)kp.L.keep + kp.L.gkeep;   // persistent prefixes only
   return GS_OK;
 }
 

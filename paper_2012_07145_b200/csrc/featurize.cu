@@ -2147,11 +2147,11 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     uint8_t* sl = slots + r * slot_bytes;
     int4* a = reinterpret_cast<int4*>(sl);
     int4* b = reinterpret_cast<int4*>(ws);
-    const int nw1 = L.warp_bytes / 16;
+    const int nw1 = L.keep / 16;
     for (int i = lane; i < nw1; i += 32) { if (save) a[i] = b[i]; else b[i] = a[i]; }
-    int4* a2 = reinterpret_cast<int4*>(sl + L.warp_bytes);
+    int4* a2 = reinterpret_cast<int4*>(sl + L.keep);
     int4* b2 = reinterpret_cast<int4*>(wgs);
-    const int nw2 = L.gl_bytes / 16;
+    const int nw2 = L.gkeep / 16;
     for (int i = lane; i < nw2; i += 32) { if (save) a2[i] = b2[i]; else b2[i] = a2[i]; }
     __syncwarp();
   };
@@ -2469,7 +2469,6 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   };
   auto place = [&](int bytes) { return place_at(1, bytes); };
   auto gplace = [&](int bytes) { int r = g; g += al(bytes); return r; };   // always global
-  L.dec = o; o += al(S * 16);
   L.didx = o; o += al(nf * 2);
   int cfs = nd == 1 ? cf_size<1>() : nd == 2 ? cf_size<2>() : nd == 3 ? cf_size<3>() : cf_size<4>();
   L.cf = o; o += al(nf * cfs);
@@ -2503,6 +2502,12 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   // accumulators, touched list: used once per decision structure) lives in
   // the warp's global scratch, as do the dependency masks, so that the
   // default machine's slice fits ten scorer warps per SM
+  // Everything from here on is per-candidate scratch (the candidate's own
+  // records, row scratch, structure-build scratch): a run slot keeps only
+  // the prefixes [0, keep) and [0, gkeep) of the slice and global scratch.
+  L.keep = o;
+  L.gkeep = g;
+  L.dec = o; o += al(S * 16);
   L.scr = o;
   L.stack = gplace((nf + 2) * (int)sizeof(Frame));
   L.volacc = gplace(nf * 8);

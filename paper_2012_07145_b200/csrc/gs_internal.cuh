@@ -77,6 +77,7 @@ struct Layout {                 // byte offsets inside dynamic shared memory (K1
   int gl_bytes;                 // per-warp global scratch bytes (inline-call lists, spilled arrays)
   int spill;                    // capacity-sized structure arrays in global scratch: 0 none, 1 resolve-side, 2 all
   int warp_bytes, total;
+  int keep, gkeep;              // slice / global-scratch prefixes a run slot saves (the rest is per-candidate)
   int rcap, pcap, S, R;
 };
 
