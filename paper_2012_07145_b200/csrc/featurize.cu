@@ -1023,7 +1023,7 @@ struct ModM {
 template <int ND>
 struct WarpWalk {
   int cd[ND], inc[ND], ext[ND];
-  int64_t mul[ND], org0;
+  int64_t mul[ND], im[ND], em[ND], o;
   int t, n;
   __device__ WarpWalk(const CF<ND>& h, const int64_t* ts, const int64_t* bs, int64_t cst, int lane) {
     int a = lane, b = 32;
@@ -1036,15 +1036,19 @@ struct WarpWalk {
     }
     cd[ND - 1] += a * ext[ND - 1];   // top digit is unbounded
     inc[ND - 1] += b * ext[ND - 1];
-    org0 = cst;
+    o = cst;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      o += (int64_t)cd[d] * mul[d];
+      im[d] = (int64_t)inc[d] * mul[d];
+      em[d] = (int64_t)ext[d] * mul[d];
+    }
     t = lane;
     n = h.n_threads;
   }
+  // the origin is carried along with the digits: adds only in the loop
   __device__ __forceinline__ int64_t origin(bool& active) const {
     active = t < n;
-    int64_t o = org0;
-#pragma unroll
-    for (int d = 0; d < ND; ++d) o += (int64_t)cd[d] * mul[d];
     return o;
   }
   __device__ __forceinline__ void next() {
@@ -1052,8 +1056,10 @@ struct WarpWalk {
 #pragma unroll
     for (int d = 0; d < ND; ++d) {
       cd[d] += inc[d] + carry;
+      o += im[d];
+      if (carry) o += mul[d];
       carry = 0;
-      if (d < ND - 1 && cd[d] >= ext[d]) { cd[d] -= ext[d]; carry = 1; }
+      if (d < ND - 1 && cd[d] >= ext[d]) { cd[d] -= ext[d]; o -= em[d]; carry = 1; }
     }
     t += 32;
   }
@@ -1236,7 +1242,7 @@ __device__ __forceinline__ unsigned long long tx_global32(const GsAccess* A, con
   const unsigned long long pex = incl - tv;
   const unsigned long long tsum = __shfl_sync(0xffffffffu, incl, 31);
   const ModM<32> mm(32);
-  unsigned long long total = 0;
+  unsigned long long total = 0, part = 0;   // part: per-lane shares, summed once after the walk
   const int nwarps = (h.n_threads + 31) / 32;
   WarpWalk<ND> walk(h, ts, bs, cst, lane);
   for (int w = 0; w < nwarps; ++w, walk.next()) {
@@ -1256,8 +1262,7 @@ __device__ __forceinline__ unsigned long long tx_global32(const GsAccess* A, con
       const unsigned long long plo = __shfl_sync(0xffffffffu, pex, lo);
       const unsigned long long phi = __shfl_sync(0xffffffffu, pex, hi & 31);
       if (hi > lo) c = hi <= 32 ? (hi == 32 ? tsum : phi) - plo : (tsum - plo) + phi;
-      for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-      total += c;
+      part += c;
     } else {
 #pragma unroll 1
       for (int r = 0; r < 32; ++r) {
@@ -1266,7 +1271,8 @@ __device__ __forceinline__ unsigned long long tx_global32(const GsAccess* A, con
       }
     }
   }
-  return total;
+  for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  return total + part;
 }
 
 // shared: register histogram mod the 4-byte bank width, one evaluation
