@@ -1065,6 +1065,50 @@ struct WarpWalk {
   }
 };
 
+// Regular thread tiles — dim-0 rows of a multiple of 32 threads, or whole
+// rows whose length divides 32 stacked without wrapping, and only full
+// warps — give every emulated warp warp 0's lane pattern, shifted by the
+// origin of its first thread.  A warp's transaction count depends on that
+// shift only modulo the counter's period (32 B segments; 128 B of banks).
+template <int ND>
+__device__ __forceinline__ bool regular_tile(const CF<ND>& h) {
+  if ((h.n_threads & 31) != 0) return false;
+  const int cx = h.ctx[0];
+  return (cx % 32 == 0) || (ND >= 2 && 32 % cx == 0 && h.ctx[ND >= 2 ? 1 : 0] % (32 / cx) == 0);
+}
+
+// Histogram of the emulated warps' shifts modulo 32 * NR: register j of
+// lane b counts the warps whose shift = 32 j + b.  A uniform (scalar)
+// mixed-radix walk over the warps' first threads: adds only.
+template <int ND, int NR>
+__device__ __forceinline__ void shift_hist(const WarpWalk<ND>& walk, int nwarps, int lane, unsigned (&cnt)[NR]) {
+  int dg[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) dg[d] = 0;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) cnt[j] = 0;
+  int64_t dlt = 0;
+#pragma unroll 1
+  for (int w = 0; w < nwarps; ++w) {
+    const int key = (int)(dlt & (int64_t)(32 * NR - 1));
+    const bool me = lane == (key & 31);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) cnt[j] += (unsigned)(me && (key >> 5) == j);
+    int carry = 0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      dg[d] += walk.inc[d] + carry;
+      dlt += walk.im[d];
+      if (carry) dlt += walk.mul[d];
+      carry = 0;
+      if (d < ND - 1 && dg[d] >= walk.ext[d]) { dg[d] -= walk.ext[d]; dlt -= walk.em[d]; carry = 1; }
+    }
+  }
+}
+
+// the regular-tile path pays off from this many emulated warps on
+constexpr int kRegularMinWarps = 4;
+
 // transactions of one emulated warp for ONE instruction constant r
 // (featurize.py:173-196): global = distinct segments; shared = max over
 // banks of distinct words; warp-collective, lanes agree on the result
@@ -1245,24 +1289,46 @@ __device__ __forceinline__ unsigned long long tx_global32(const GsAccess* A, con
   unsigned long long total = 0, part = 0;   // part: per-lane shares, summed once after the walk
   const int nwarps = (h.n_threads + 31) / 32;
   WarpWalk<ND> walk(h, ts, bs, cst, lane);
+  // lane share of one emulated warp whose lane addresses are non-decreasing
+  auto mono_share = [&](int64_t org, int64_t up) {
+    unsigned long long c = 0;
+    int lo = 0, hi = 0;
+    if (lane > 0) {
+      const int64_t d = org - up;
+      if (d >= 32) c = tsum;
+      else { lo = (int)((32 - d - (up & 31)) & 31); hi = lo + (int)d; }
+    } else {
+      c = tsum;
+    }
+    const unsigned long long plo = __shfl_sync(0xffffffffu, pex, lo);
+    const unsigned long long phi = __shfl_sync(0xffffffffu, pex, hi & 31);
+    if (hi > lo) c = hi <= 32 ? (hi == 32 ? tsum : phi) - plo : (tsum - plo) + phi;
+    return c;
+  };
+  if (nwarps >= kRegularMinWarps && regular_tile<ND>(h)) {
+    bool active;
+    const int64_t org = walk.origin(active);   // warp 0, all lanes active
+    const int64_t up = __shfl_up_sync(0xffffffffu, org, 1);
+    if (__all_sync(0xffffffffu, lane == 0 || org >= up)) {
+      unsigned cnt[1];
+      shift_hist<ND, 1>(walk, nwarps, lane, cnt);
+      unsigned nz = __ballot_sync(0xffffffffu, cnt[0] != 0);
+      while (nz) {
+        const int r = __ffs(nz) - 1; nz &= nz - 1;
+        const unsigned cr = __shfl_sync(0xffffffffu, cnt[0], r);
+        part += (unsigned long long)cr * mono_share(org + r, up + r);
+      }
+      for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      return part;
+    }
+  }
   for (int w = 0; w < nwarps; ++w, walk.next()) {
     bool active;
     const int64_t org = walk.origin(active);
     const int64_t up = __shfl_up_sync(0xffffffffu, org, 1);
     if (__all_sync(0xffffffffu, lane == 0 || !active || org >= up)) {
-      unsigned long long c = 0;
-      int lo = 0, hi = 0;
-      if (active && lane > 0) {
-        const int64_t d = org - up;
-        if (d >= 32) c = tsum;
-        else { lo = (int)((32 - d - (up & 31)) & 31); hi = lo + (int)d; }
-      } else if (active) {
-        c = tsum;
-      }
-      const unsigned long long plo = __shfl_sync(0xffffffffu, pex, lo);
-      const unsigned long long phi = __shfl_sync(0xffffffffu, pex, hi & 31);
-      if (hi > lo) c = hi <= 32 ? (hi == 32 ? tsum : phi) - plo : (tsum - plo) + phi;
-      part += c;
+      const unsigned long long c = mono_share(org, up);
+      if (active) part += c;
     } else {
 #pragma unroll 1
       for (int r = 0; r < 32; ++r) {
@@ -1297,6 +1363,49 @@ __device__ __forceinline__ unsigned long long tx_shared4(const GsAccess* A, cons
   unsigned long long total = 0;
   const int nwarps = (h.n_threads + 31) / 32;
   WarpWalk<ND> walk(h, ts, bs, cst, lane);
+  // one emulated warp, every constant residue mod 4 that occurs
+  auto warp_total = [&](int64_t org, int64_t up, bool active, bool mono) {
+    unsigned long long t = 0;
+    unsigned m4 = ew;
+    while (m4) {
+      const int e = __ffs(m4) - 1; m4 &= m4 - 1;
+      const unsigned long long we = __shfl_sync(0xffffffffu, tb, e);
+      if (mono) {
+        const int64_t word = (org + e) >> 2, wup = (up + e) >> 2;
+        const bool lead = active && (lane == 0 || word != wup);
+        const unsigned bank = lead ? (unsigned)(word & 31) : 0x80000000u + lane;
+        const unsigned bmask = __match_any_sync(0xffffffffu, bank);
+        const unsigned per_bank = lead ? __popc(bmask) : 0u;
+        t += we * __reduce_max_sync(0xffffffffu, per_bank);
+      } else {
+        t += we * warp_count((unsigned long long)(org + e), active, T_SHARED, mm, 2, 4, 32);
+      }
+    }
+    return t;
+  };
+  if (nwarps >= kRegularMinWarps && regular_tile<ND>(h)) {
+    // every warp has warp 0's lane pattern: the one-transaction test holds
+    // for all warps or for none, and otherwise the count depends on the
+    // shift mod 128 (32 banks x 4 B)
+    bool active;
+    const int64_t org = walk.origin(active);   // warp 0, all lanes active
+    const int64_t up = __shfl_up_sync(0xffffffffu, org, 1);
+    const bool mono = __all_sync(0xffffffffu, lane == 0 || org >= up);
+    const int64_t span = __shfl_sync(0xffffffffu, org, 31) - __shfl_sync(0xffffffffu, org, 0);
+    if (mono && span <= 124) return (unsigned long long)nwarps * tb_all;
+    unsigned cnt[4];
+    shift_hist<ND, 4>(walk, nwarps, lane, cnt);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      unsigned nz = __ballot_sync(0xffffffffu, cnt[j] != 0);
+      while (nz) {
+        const int b = __ffs(nz) - 1; nz &= nz - 1;
+        const unsigned cr = __shfl_sync(0xffffffffu, cnt[j], b);
+        total += (unsigned long long)cr * warp_total(org + 32 * j + b, up + 32 * j + b, true, mono);
+      }
+    }
+    return total;
+  }
   for (int w = 0; w < nwarps; ++w, walk.next()) {
     bool active;
     const int64_t org = walk.origin(active);
@@ -1311,21 +1420,7 @@ __device__ __forceinline__ unsigned long long tx_shared4(const GsAccess* A, cons
     // a distinct bank: one transaction per instruction
     const int64_t span = __shfl_sync(0xffffffffu, org, 31 - __clz(act)) - __shfl_sync(0xffffffffu, org, 0);
     if (mono && span <= 124) { total += tb_all; continue; }
-    unsigned m4 = ew;
-    while (m4) {
-      const int e = __ffs(m4) - 1; m4 &= m4 - 1;
-      const unsigned long long we = __shfl_sync(0xffffffffu, tb, e);
-      if (mono) {
-        const int64_t word = (org + e) >> 2, wup = (up + e) >> 2;
-        const bool lead = active && (lane == 0 || word != wup);
-        const unsigned bank = lead ? (unsigned)(word & 31) : 0x80000000u + lane;
-        const unsigned bmask = __match_any_sync(0xffffffffu, bank);
-        const unsigned per_bank = lead ? __popc(bmask) : 0u;
-        total += we * __reduce_max_sync(0xffffffffu, per_bank);
-      } else {
-        total += we * warp_count((unsigned long long)(org + e), active, T_SHARED, mm, 2, 4, 32);
-      }
-    }
+    total += warp_total(org, up, active, mono);
   }
   return total;
 }
