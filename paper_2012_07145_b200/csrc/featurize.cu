@@ -1107,7 +1107,7 @@ __device__ __forceinline__ void shift_hist(const WarpWalk<ND>& walk, int nwarps,
 }
 
 // the regular-tile path pays off from this many emulated warps on
-constexpr int kRegularMinWarps = 4;
+constexpr int kRegularMinWarps = 4;   // 2 and 8 measure the same
 
 // transactions of one emulated warp for ONE instruction constant r
 // (featurize.py:173-196): global = distinct segments; shared = max over
@@ -1833,8 +1833,10 @@ __device__ __forceinline__ void parallel_feats(double* v, const GsMachine& M, in
   // stream.  Quotients by 1 are the integer values themselves.
   const int lane = lane_id();
   const int kt = kern.k_threads, ws = M.warp_size;
-  const int aw = (n + ws - 1) / ws;
-  int wpb = (kt + ws - 1) / ws;
+  const bool w32 = ws == 32;   // the common warp: shifts instead of divisions
+  const int aw = w32 ? (n + 31) >> 5 : (n + ws - 1) / ws;
+  const int kw = w32 ? (kt + 31) >> 5 : (kt + ws - 1) / ws;
+  int wpb = kw;
   if (wpb < 1) wpb = 1;
   int by_shared;
   if (kern.k_shared > 0) {
@@ -1858,7 +1860,7 @@ __device__ __forceinline__ void parallel_feats(double* v, const GsMachine& M, in
   const double nb = (double)kern.n_blocks, nn = (double)n, mt = (double)M.max_threads_per_block;
   double num = 0.0, den = 1.0;
   num = lane == 0 || lane == 11 || lane == 14 ? nb : num;
-  num = lane == 1 ? (double)((kt + ws - 1) / ws) : num;
+  num = lane == 1 ? (double)kw : num;
   num = lane == 2 ? (double)aw : num;
   num = lane == 3 || lane == 4 || lane == 12 ? nn : num;
   num = lane == 5 ? (double)(ws * aw - n) : num;
