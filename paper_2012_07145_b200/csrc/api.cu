@@ -330,18 +330,18 @@ struct K1Ws {
 
 static int k1_plan(gs_pipeline_t p, int64_t n, int S, bool feats, int reuse, K1Plan& kp) {
   // Launch shapes (CTAs per SM x scorer warps per CTA).  The warps of a CTA
-  // work in lockstep (featurize_kernel).  Sibling slices (mode 2) run best
-  // as two CTAs per SM, one CTA's warps issuing while the other's wait at a
-  // barrier; 240K C5 candidates: 12 warps x 1 CTA 23.1 ms, 5 x 2 22.1 ms,
-  // 4 x 2 22.8 ms, 2 x 6 23.8 ms.  Whole-candidate work (modes 0 / 1:
-  // random schedules, reuse off, run heads) runs best with the most warps
-  // in one CTA (the 1M stress batch: 2.2 s as 12 x 1, 2.7 s as 5 x 2).
-  // Both launches of the two-phase schedule share one slice layout (the
-  // run-head launch saves warp states the sibling launch restores), so they
-  // share the spill choice: the capacity-sized structure arrays go to the
-  // warp's global scratch when that buys more warps.  GS_K1_CTAS (sibling
-  // launch) / GS_K1_SPILL force the choice (diagnostics).  Registers cap a
-  // SM at kK1MaxWarps warps.
+  // work in lockstep (featurize_kernel).  Both launches of the two-phase
+  // schedule share one slice layout (the run-head launch saves warp states
+  // the sibling launch restores), so they share the spill choice: the
+  // capacity-sized structure arrays go to the warp's global scratch when
+  // that buys more warps.  One CTA with the most warps runs best for every
+  // mode now that a run slot saves only the persistent slice prefix:
+  // 1M C5 step, sibling launch as 1 x 12 warps (spill 2) 58.5 ms K1, 2 x 5
+  // (spill 1) 60.5 ms, 2 x 6 (spill 2) 62.7 ms; the 64K C2 steps 7.0 / 6.2
+  // ms against 7.7 / 7.1 ms as 2 x 5 (earlier, with whole-slice slot
+  // copies, 2 x 5 had won: 22.1 vs 23.1 ms on 240K candidates).
+  // GS_K1_CTAS (sibling launch) / GS_K1_SPILL force the choice
+  // (diagnostics).  Registers cap a SM at kK1MaxWarps warps.
   auto fit = [&](int ctas, int spill) {
     const Layout L1 = layout_for(p, S, 1, spill);
     const int per_cta = (p->sm_smem / ctas) - p->cta_reserved;
@@ -360,7 +360,6 @@ static int k1_plan(gs_pipeline_t p, int64_t n, int S, bool feats, int reuse, K1P
   int spill = best(1);
   int ctas2 = 1;
   if (kp.two_phase) {
-    ctas2 = 2;
     if (const char* e = getenv("GS_K1_CTAS")) ctas2 = std::max(1, atoi(e));
     spill = best(ctas2);   // the sibling launch dominates: its best level for both launches
     if (fit(ctas2, spill) < 3) ctas2 = 1;   // too big for several CTAs per SM
