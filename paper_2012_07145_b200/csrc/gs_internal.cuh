@@ -20,7 +20,7 @@ constexpr int kUnit = 64;           // K1 work-unit size (candidates, before run
 #ifndef GS_CHUNK2
 #define GS_CHUNK2 5
 #endif
-constexpr int kChunk2 = GS_CHUNK2;  // K1 two-phase schedule: sibling slice size (C5 K1: 16 -> 80.2 ms, 8 -> 77.2, 5 -> 70.4, 4 -> 74.3)
+constexpr int kChunk2 = GS_CHUNK2;  // K1 two-phase schedule: sibling slice size (1M C5 K1, one 12-warp CTA per SM: 3 -> 63.4 ms, 4 -> 61.9, 5 -> 58.5, 6 -> 64.8, 8 -> 66.4)
 constexpr int64_t kAddrBias = int64_t(1) << 40;  // featurize.py:256
 
 enum Tier : int8_t { T_GLOBAL = 0, T_SHARED = 1, T_REGISTER = 2, T_NONE = 3 };
