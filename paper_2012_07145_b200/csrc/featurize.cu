@@ -2210,6 +2210,9 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   K1<ND> k;
   bind(k, warp);
   WarpScr& W = *reinterpret_cast<WarpScr*>(ws + L.scr);
+  int* s_nd = reinterpret_cast<int*>(sm + L.cta);                  // [nw] dirty rows of each warp's candidate
+  int* s_next = s_nd + kK1MaxWarps;                               // next pooled row
+  int64_t* s_cand = reinterpret_cast<int64_t*>(sm + L.cta + 64);   // [nw] each warp's candidate
   uint8_t* rflag = ws + L.rflag;
   int32_t* rsrc = reinterpret_cast<int32_t*>(ws + L.rsrc);
   // Work units: kUnit-candidate slices of the batch, each extended to start
@@ -2493,20 +2496,50 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
         phaseA(c, pc);
       }
       if (have) { phaseResolve(); phaseA2(c, pc); }
+      // sibling slices pool their rows (1M C5 K1 58.3 -> 54.4 ms, C2 7.0 ->
+      // 5.2 ms); run heads and whole candidates (modes 1 / 0: ~100 rows
+      // each, even work) measured 1-10 % slower pooled
+      const bool pool = lockstep && mode == 2;
+      if (pool) {
+        if (lane == 0) { s_nd[warp] = have ? nd : 0; s_cand[warp] = c; }
+        if (threadIdx.x == 0) *s_next = 0;
+      }
       if (lockstep) __syncthreads();
-      if (have) {
-        phaseB(c, pc);
-        // the rows read the scorer state through a view rebuilt per row:
-        // its pointers are rematerialised from the slice base instead of
-        // staying live across the row code (60.1 vs 61.0 ms per 1M C5 K1)
+      if (have) phaseB(c, pc);
+      if (pool && reuse == 1 && feats) __syncthreads();   // copied blocks land before pooled rows
+      // the rows read the scorer state through a view rebuilt per row: its
+      // pointers are rematerialised from the slice base instead of staying
+      // live across the row code (60.1 vs 61.0 ms per 1M C5 K1).  Pooled:
+      // the CTA's rows in row-major order (row q of every warp's candidate,
+      // then row q + 1: siblings' row q run the same code), each taken by
+      // the next free warp.
+      if (pool) {
+        const int myn = lane < nw ? s_nd[lane] : 0;
+        for (;;) {
+          int p = 0;
+          if (lane == 0) p = atomicAdd(s_next, 1);
+          p = __shfl_sync(0xffffffffu, p, 0);
+          int q = 0, o = -1;
+          for (;; ++q) {
+            const unsigned has = __ballot_sync(0xffffffffu, myn > q);
+            if (!has) break;
+            const int cnt = __popc(has);
+            if (p < cnt) { o = __fns(has, 0, p + 1); break; }
+            p -= cnt;
+          }
+          if (o < 0) break;
+          K1<ND> kr;
+          bind(kr, o);
+          phaseRow(kr, s_cand[o], q);
+        }
+      } else if (have) {
         for (int q = 0; q < nd; ++q) {
           K1<ND> kr;
           bind(kr, warp);
           phaseRow(kr, c, q);
         }
-        phaseB3(c);
-        pc = c; ++c;
       }
+      if (have) { phaseB3(c); pc = c; ++c; }
       if (lockstep) __syncthreads();
     }
   }
@@ -2575,7 +2608,8 @@ Layout make_layout(int nd, int nf, int ns, int blob_bytes, int S, int R, int rca
   auto al = [](int x) { return (x + 15) & ~15; };
   Layout L{};
   L.blob = 0;
-  L.warps = al(blob_bytes);
+  L.cta = al(blob_bytes);            // CTA header: pooled-row bookkeeping
+  L.warps = L.cta + kCtaHeaderBytes;
   int o = 0;
   int g = 0;   // global scratch bytes per warp (spill)
   // capacity-sized arrays: in the smem slice, or in global scratch

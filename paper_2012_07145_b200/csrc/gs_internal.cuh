@@ -16,6 +16,7 @@ constexpr int kRowReads = 64;       // reads attributed to one row
 constexpr int kGroupReads = 16;     // reads in one (tier, producer) group
 constexpr int kLaneIv = 96;         // per-lane interval capacity for unions
 constexpr int kK1MaxWarps = 12;      // K1 warps per CTA (one CTA per SM)
+constexpr int kCtaHeaderBytes = 256;  // K1 CTA header in dynamic shared memory (pooled-row bookkeeping)
 constexpr int kUnit = 64;           // K1 work-unit size (candidates, before run-head snapping)
 #ifndef GS_CHUNK2
 #define GS_CHUNK2 5
@@ -72,7 +73,7 @@ struct RRead {                // one expanded read (resolve.py:56-79 ResolvedRea
 struct Layout {                 // byte offsets inside dynamic shared memory (K1)
   int blob, dec, didx, cf, pcf, reads, paths, rdb, rows, stack, volacc, touched, icall, srcb,
       srcl, rdepb, rdep, dirty, rflag, rowlist, rsrc, kern, dm, cmask, kmb, kml, icb, icl, dlist, gdirty,
-      kdirty, misc, warps, scr;
+      kdirty, misc, warps, scr, cta;
   int mw;                       // dependency-mask words per func (0 = incremental resolve off)
   int gl_bytes;                 // per-warp global scratch bytes (inline-call lists, spilled arrays)
   int spill;                    // capacity-sized structure arrays in global scratch: 0 none, 1 resolve-side, 2 all
