@@ -197,6 +197,14 @@ int64_t gs_struct_hash_workspace_bytes(int64_t n);
 int gs_struct_hash_ws(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
                       int depth, uint64_t* out, void* workspace, int64_t ws_bytes,
                       void* stream);
+/* gs_struct_hash_ws at up to four depths in one pass over the records:
+ * depths[0..ndepths) (host array), out = [ndepths][n] (depth-major).  The
+ * beam step's pass-depth buckets and the bad-hash memo depths
+ * (search.py:196-200: the bottom half's hashes at 1..num_passes) come from
+ * one launch; the memo then gathers instead of re-hashing. */
+int gs_struct_hash_depths_ws(gs_pipeline_t p, const GsDecision* dec, int64_t n, int s,
+                             int ndepths, const int* depths, uint64_t* out,
+                             void* workspace, int64_t ws_bytes, void* stream);
 
 /* K4: bucket by hash + hierarchical-sampling representatives
  * (sampling.py:45-59, search.py:127-165).  `valid[i]` = verdict==0.

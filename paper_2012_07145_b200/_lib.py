@@ -23,7 +23,7 @@ EXPORTS = ("gs_last_error", "gs_version", "gs_launch_count", "gs_pipeline_create
            "gs_featurize_ws", "gs_struct_hash_workspace_bytes", "gs_struct_hash_ws", "gs_beam_topk_reps",
            "gs_model_params", "gs_predict", "gs_train_workspace_bytes", "gs_train",
            "gs_set_placement_info", "gs_phase1_workspace_bytes", "gs_expand_phase1",
-           "gs_random_schedules", "gs_get_reuse")
+           "gs_random_schedules", "gs_get_reuse", "gs_struct_hash_depths_ws")
 
 
 class GsError(RuntimeError):
@@ -78,6 +78,7 @@ def load(path: str = LIB_PATH):
         "gs_train": (i32, [V, i32, i32, V, V, V, V, V, V, V, i32, i32, dbl, dbl, i32, V, i64, V, V, V]),
         "gs_beam_topk_reps": (i32, [V, V, V, i64, V, V, i64, dbl, dbl, u64, i64, dbl, V, i64, V, V, V, V]),
         "gs_struct_hash_ws": (i32, [P, V, i64, i32, i32, V, V, i64, V]),
+        "gs_struct_hash_depths_ws": (i32, [P, V, i64, i32, i32, V, V, V, i64, V]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -29,7 +29,7 @@ int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream
 int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
                 const int32_t* n_rows, const int32_t* row_src, int64_t n, int R, double* total, double* row_cost,
                 double* basis_gh, unsigned* work, int num_sms, cudaStream_t st);
-int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, const int32_t* sorted_funcs,
+int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, HashDepths D, const int32_t* sorted_funcs,
                 const uint8_t* names, const int32_t* name_off, uint64_t* out, uint8_t* head, int repr_bound,
                 int num_sms, cudaStream_t st);
 int64_t select_workspace_bytes(int64_t n);
@@ -556,7 +556,22 @@ int gs_struct_hash_ws(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, 
   if (!p || depth < 0) return fail(GS_ERR_ARG, "depth must be >= 0");
   if (ws_bytes < gs_struct_hash_workspace_bytes(n) || !workspace)
     return fail(GS_ERR_ARG, "hash workspace too small (gs_struct_hash_workspace_bytes)");
-  int rc = launch_hash(dec, n, S, p->host.nf, depth, p->sorted, p->names, p->name_off, out,
+  return gs_struct_hash_depths_ws(p, dec, n, S, 1, &depth, out, workspace, ws_bytes, stream);
+}
+
+int gs_struct_hash_depths_ws(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, int ndepths,
+                             const int* depths, uint64_t* out, void* workspace, int64_t ws_bytes, void* stream) {
+  GS_NVTX("gs_struct_hash_depths_ws");
+  if (!p || ndepths < 1 || ndepths > 4 || !depths) return fail(GS_ERR_ARG, "1..4 depths");
+  HashDepths D{};
+  D.n = ndepths;
+  for (int k = 0; k < ndepths; ++k) {
+    if (depths[k] < 0) return fail(GS_ERR_ARG, "depth must be >= 0");
+    D.d[k] = depths[k];
+  }
+  if (ws_bytes < gs_struct_hash_workspace_bytes(n) || !workspace)
+    return fail(GS_ERR_ARG, "hash workspace too small (gs_struct_hash_workspace_bytes)");
+  int rc = launch_hash(dec, n, S, p->host.nf, D, p->sorted, p->names, p->name_off, out,
                        static_cast<uint8_t*>(workspace), p->repr_bound, p->num_sms, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "too many funcs for the hash kernel");
   CK(cudaGetLastError());
@@ -575,7 +590,10 @@ int gs_struct_hash(gs_pipeline_t p, const GsDecision* dec, int64_t n, int S, int
     CK(cudaMalloc(&p->hscratch, (size_t)n));
     p->hcap = n;
   }
-  int rc = launch_hash(dec, n, S, p->host.nf, depth, p->sorted, p->names, p->name_off, out, p->hscratch,
+  HashDepths D{};
+  D.n = 1;
+  D.d[0] = depth;
+  int rc = launch_hash(dec, n, S, p->host.nf, D, p->sorted, p->names, p->name_off, out, p->hscratch,
                        p->repr_bound, p->num_sms, (cudaStream_t)stream);
   if (rc) return fail(GS_ERR_ARG, "too many funcs for the hash kernel");
   CK(cudaGetLastError());

@@ -93,6 +93,11 @@ struct P1Static {
   const int32_t* sorted;     // funcs in Python str (name) order
 };
 
+struct HashDepths {             // K3: the depths one pass hashes (out: [n][...] per depth, depth-major)
+  int n;
+  int d[4];
+};
+
 struct NetDev {                 // device copies of the coefficient network (K2)
   int E, H;                     // embed / hidden dims
   const double *algo_w, *algo_b, *sched_w, *sched_b, *head_w, *head_b, *out_w, *out_b;

@@ -197,8 +197,8 @@ __global__ void hash_kernel(const GsDecision* __restrict__ dec, int64_t n, int S
 // ---------------------------------------------------------------------------
 // Warp-per-candidate variant: the 32 lanes render the canonical repr in
 // parallel (one decision entry per lane, offsets by a warp scan of entry
-// lengths) into this warp's shared-memory buffer, then one lane runs the
-// blake2b compressions over it.  Used whenever the longest possible repr
+// lengths) into this warp's shared-memory buffer, then the warp runs the
+// blake2b compressions over it (four lanes per state, blake_buf4).  Used whenever the longest possible repr
 // fits the buffer (kHashBuf); the thread-per-candidate kernel above covers
 // the rest.
 constexpr int kHashBuf = 8192;
@@ -207,38 +207,75 @@ constexpr int kHashWarps = 4;   // warps per block
 __device__ __forceinline__ int cstr_len(const char* s) { int n = 0; while (s[n]) ++n; return n; }
 __device__ __forceinline__ int put(uint8_t* buf, int o, const char* s) { while (*s) buf[o++] = (uint8_t)*s++; return o; }
 
-__device__ __forceinline__ uint64_t blake_buf(const uint8_t* buf, int len) {
-  uint64_t h[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) h[i] = kIV[i];
-  h[0] ^= 0x01010000ULL ^ 8ULL;
+// blake2b-64 of buf[0, len) by the whole warp: lane group of four (lane &
+// 3 = q) holds state column q (v[q], v[4+q], v[8+q], v[12+q]); a round is
+// G on the four columns, a rotation of the b / c / d rows across the group
+// (shuffles), G on the four diagonals, and the inverse rotation.  The
+// serial chain is a quarter of the one-lane compressor's; the eight groups
+// compute the same value.  sig: lane q's message indices, 4 bits each:
+// round r's (2q, 2q+1, 8+2q, 9+2q) schedule entries at bits 16r..16r+15
+// (three 64-bit words, four rounds each).
+__device__ __forceinline__ void gmix(uint64_t& a, uint64_t& b, uint64_t& c, uint64_t& d, uint64_t x, uint64_t y) {
+  a = a + b + x; d = rotr(d ^ a, 32); c = c + d; b = rotr(b ^ c, 24);
+  a = a + b + y; d = rotr(d ^ a, 16); c = c + d; b = rotr(b ^ c, 63);
+}
+
+__device__ __forceinline__ uint64_t blake_buf4(const uint8_t* buf, int len, const uint64_t (&sig)[3]) {
+  const int q = threadIdx.x & 3;
+  uint64_t ha = kIV[q], hb = kIV[4 + q];
+  if (q == 0) ha ^= 0x01010000ULL ^ 8ULL;
   const int nblk = len == 0 ? 1 : (len + 127) / 128;
   for (int b = 0; b < nblk; ++b) {
-    uint64_t m[16], v[16];
     const uint64_t* w = reinterpret_cast<const uint64_t*>(buf + 128 * b);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) m[i] = w[i];
     const bool last = b == nblk - 1;
+    uint64_t va = ha, vb = hb, vc = kIV[q], vd = kIV[4 + q];
+    if (q == 0) vd ^= (uint64_t)(last ? len : 128 * (b + 1));
+    if (q == 2 && last) vd = ~vd;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { v[i] = h[i]; v[i + 8] = kIV[i]; }
-    v[12] ^= (uint64_t)(last ? len : 128 * (b + 1));
-    if (last) v[14] = ~v[14];
-    blake_round<0>(v, m); blake_round<1>(v, m); blake_round<2>(v, m); blake_round<3>(v, m);
-    blake_round<4>(v, m); blake_round<5>(v, m); blake_round<6>(v, m); blake_round<7>(v, m);
-    blake_round<8>(v, m); blake_round<9>(v, m); blake_round<10>(v, m); blake_round<11>(v, m);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) h[i] ^= v[i] ^ v[i + 8];
+    for (int r = 0; r < 12; ++r) {
+      const unsigned e = (unsigned)(sig[r >> 2] >> (16 * (r & 3))) & 0xFFFFu;
+      gmix(va, vb, vc, vd, w[e & 15], w[(e >> 4) & 15]);
+      vb = __shfl_sync(0xffffffffu, vb, (q + 1) & 3, 4);
+      vc = __shfl_sync(0xffffffffu, vc, (q + 2) & 3, 4);
+      vd = __shfl_sync(0xffffffffu, vd, (q + 3) & 3, 4);
+      gmix(va, vb, vc, vd, w[(e >> 8) & 15], w[(e >> 12) & 15]);
+      vb = __shfl_sync(0xffffffffu, vb, (q + 3) & 3, 4);
+      vc = __shfl_sync(0xffffffffu, vc, (q + 2) & 3, 4);
+      vd = __shfl_sync(0xffffffffu, vd, (q + 1) & 3, 4);
+    }
+    ha ^= va ^ vc;
+    hb ^= vb ^ vd;
   }
-  return h[0];
+  return __shfl_sync(0xffffffffu, ha, 0);
+}
+
+__constant__ uint8_t kSigma[12][16] = {
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+    {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4}, {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+    {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13}, {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+    {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11}, {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+    {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5}, {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
+
+__device__ __forceinline__ void sigma_of_lane(uint64_t (&sig)[3]) {
+  const int q = threadIdx.x & 3;
+  sig[0] = sig[1] = sig[2] = 0;
+  for (int r = 0; r < 12; ++r) {
+    const uint64_t e = (uint64_t)kSigma[r][2 * q] | (uint64_t)kSigma[r][2 * q + 1] << 4 |
+                       (uint64_t)kSigma[r][8 + 2 * q] << 8 | (uint64_t)kSigma[r][9 + 2 * q] << 12;
+    sig[r >> 2] |= e << (16 * (r & 3));
+  }
 }
 
 __global__ void __launch_bounds__(kHashWarps * 32) hash_warp_kernel(
-    const GsDecision* __restrict__ dec, int64_t n, int S, int nf, int depth, const int32_t* __restrict__ sorted_funcs,
+    const GsDecision* __restrict__ dec, int64_t n, int S, int nf, HashDepths D, const int32_t* __restrict__ sorted_funcs,
     const uint8_t* __restrict__ names, const int32_t* __restrict__ name_off, uint64_t* __restrict__ out,
     const uint8_t* __restrict__ head) {
   extern __shared__ __align__(16) uint8_t smh[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint8_t* buf = smh + wib * (kHashBuf + 2 * kHashMaxFuncs);
+  uint64_t sig[3];
+  sigma_of_lane(sig);
   int16_t* didx = reinterpret_cast<int16_t*>(buf + kHashBuf);
   // contiguous candidate ranges per warp: run heads are periodic in a beam
   // step (one per parent), and a grid stride sharing a factor with that
@@ -265,6 +302,12 @@ __global__ void __launch_bounds__(kHashWarps * 32) hash_warp_kernel(
       if (f != 0xFFFF && f < nf) didx[f] = (int16_t)i;
     }
     __syncwarp();
+    // every requested depth from the same records (out: [D.n][n]); a run
+    // at the deepest key is a run at every shallower one
+#pragma unroll 1
+    for (int dk = 0; dk < D.n; ++dk) {
+    const int depth = D.d[dk];
+    uint64_t* outk = out + (int64_t)dk * n;
     int pos;
     if (depth == 0) {
       if (lane == 0) put(buf, 0, "('kernels', (");
@@ -348,20 +391,19 @@ __global__ void __launch_bounds__(kHashWarps * 32) hash_warp_kernel(
     const int padded = ((len + 127) / 128) * 128;
     for (int k = len + lane; k < padded && k < kHashBuf; k += 32) buf[k] = 0;
     __syncwarp();
-    unsigned long long hv = 0;
-    if (lane == 0) hv = len <= kHashBuf ? blake_buf(buf, len) : 0ull;
-    hv = __shfl_sync(0xffffffffu, hv, 0);
-    if (lane == 0) out[c] = hv;
+    const unsigned long long hv = len <= kHashBuf ? blake_buf4(buf, len, sig) : 0ull;
+    if (lane == 0) outk[c] = hv;
     if (head) {   // the run's followers (up to the next head, past this warp's range) copy it
       for (int64_t b = c + 1; b < n; b += 32) {
         const bool follower = b + lane < n && !head[b + lane];
         const unsigned m = __ballot_sync(0xffffffffu, !follower);   // first head / end of batch
         const int stop = m ? __ffs(m) - 1 : 32;
-        if (lane < stop) out[b + lane] = hv;
+        if (lane < stop) outk[b + lane] = hv;
         if (m) break;
       }
     }
     __syncwarp();
+    }
   }
 }
 
@@ -375,12 +417,13 @@ __global__ void hash_fill_kernel(const uint8_t* __restrict__ head, int64_t n, ui
   out[c] = out[j];
 }
 
-int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, const int32_t* sorted_funcs,
+int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, HashDepths D, const int32_t* sorted_funcs,
                 const uint8_t* names, const int32_t* name_off, uint64_t* out, uint8_t* head, int repr_bound,
                 int num_sms, cudaStream_t st) {
   if (n == 0) return 0;
   if (nf > kHashMaxFuncs) return -1;
-  if (depth > 3) depth = 3;
+  if (D.n < 1 || D.n > 4) return -1;
+  for (int k = 0; k < D.n; ++k) D.d[k] = D.d[k] > 3 ? 3 : D.d[k];
   int64_t blocks = (n + 127) / 128;
   if (head) {
     hash_head_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(dec, n, S, head);
@@ -391,15 +434,19 @@ int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, int depth, cons
     cudaFuncSetAttribute(hash_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int64_t want = (n + kHashWarps - 1) / kHashWarps;
     const int grid = (int)(want < (int64_t)num_sms * 8 ? want : (int64_t)num_sms * 8);
-    hash_warp_kernel<<<grid, kHashWarps * 32, smem, st>>>(dec, n, S, nf, depth, sorted_funcs, names, name_off, out,
+    hash_warp_kernel<<<grid, kHashWarps * 32, smem, st>>>(dec, n, S, nf, D, sorted_funcs, names, name_off, out,
                                                            head);
-  } else {
-    hash_kernel<<<(unsigned)blocks, 128, 0, st>>>(dec, n, S, nf, depth, sorted_funcs, names, name_off, out, head);
-  }
-  g_launch_count++;
-  if (head && repr_bound > kHashBuf) {   // the warp kernel writes followers itself
-    hash_fill_kernel<<<(unsigned)blocks, 128, 0, st>>>(head, n, out);
     g_launch_count++;
+    return 0;
+  }
+  for (int k = 0; k < D.n; ++k) {   // per-thread kernel (representations beyond the warp buffer)
+    uint64_t* outk = out + (int64_t)k * n;
+    hash_kernel<<<(unsigned)blocks, 128, 0, st>>>(dec, n, S, nf, D.d[k], sorted_funcs, names, name_off, outk, head);
+    g_launch_count++;
+    if (head) {
+      hash_fill_kernel<<<(unsigned)blocks, 128, 0, st>>>(head, n, outk);
+      g_launch_count++;
+    }
   }
   return 0;
 }

@@ -184,6 +184,21 @@ class Scorer:
                                            _ptr(out), _stream()))
         return out
 
+    def struct_hash_depths(self, dec: torch.Tensor, depths):
+        """K3 at several depths in one pass (gs_struct_hash_depths_ws):
+        int64 [len(depths), N], row k = depth depths[k]."""
+        depths = [int(d) for d in depths]
+        if not 1 <= len(depths) <= 4 or min(depths) < 0:
+            raise ValueError("1..4 depths, each >= 0")
+        n = dec.shape[0]
+        out = torch.empty((len(depths), n), dtype=torch.int64, device=self.device)
+        wsb = self.lib.gs_struct_hash_workspace_bytes(n)
+        ws = torch.empty((wsb,), dtype=torch.uint8, device=self.device)
+        d = (C.c_int * len(depths))(*depths)
+        _lib.check(self.lib.gs_struct_hash_depths_ws(self.handle, _ptr(dec), n, dec.shape[1] // 16, len(depths),
+                                                     C.cast(d, C.c_void_p), _ptr(out), _ptr(ws), wsb, _stream()))
+        return out
+
     def memo_hashes(self, dec: torch.Tensor, num_passes: int, h3=None):
         """Hashes at depths 1..num_passes (the bad-hash memo, search.py:196-200).
         The canonical key caps the depth at 3 (loopnest.py:137), so deeper

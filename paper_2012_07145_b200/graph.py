@@ -55,7 +55,9 @@ class CapturedStep:
         self.dec = torch.zeros((n, S * 16), dtype=torch.uint8, device=dev)
         # K3: pass depth + memo depths 1..min(num_passes, 3) (deeper keys cap at 3)
         self.depths = sorted({pass_index} | set(range(1, min(num_passes, 3) + 1)))
-        self.hash = {d: e((n,), torch.int64) for d in self.depths}
+        self.H = e((len(self.depths), n), torch.int64)   # one K3 pass, every depth
+        self.hash = {d: self.H[i] for i, d in enumerate(self.depths)}
+        self._depths_c = (C.c_int * len(self.depths))(*self.depths)
         self.hws_b = lib.gs_struct_hash_workspace_bytes(n)
         self.hws = e((self.hws_b,), torch.uint8)
         # K1 (reuse mode 2: computed rows only; K2 gathers through row_src)
@@ -93,9 +95,9 @@ class CapturedStep:
         sc, lib = self.sc, self.lib
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         h = sc.handle
-        for d in self.depths:
-            _lib.check(lib.gs_struct_hash_ws(h, _p(self.dec), self.n, self.S, d, _p(self.hash[d]), _p(self.hws),
-                                             self.hws_b, st))
+        _lib.check(lib.gs_struct_hash_depths_ws(h, _p(self.dec), self.n, self.S, len(self.depths),
+                                                C.cast(self._depths_c, C.c_void_p), _p(self.H), _p(self.hws),
+                                                self.hws_b, st))
         prev = sc.reuse_mode
         sc.set_reuse(2)
         try:

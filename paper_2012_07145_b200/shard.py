@@ -116,7 +116,14 @@ class StepPlan:
                 ev.append(e)
 
         mark()
-        h = sc.struct_hash(dec, self.pass_index)
+        # K3 once over the records at the pass depth and every memo depth
+        # (1..num_passes; keys cap at depth 3, loopnest.py:137): the memo
+        # below gathers the bottom half's hashes instead of re-hashing them
+        cap = lambda x: min(x, 3)  # noqa: E731
+        depths = [self.pass_index] + sorted({cap(x) for x in range(1, self.num_passes + 1)} - {cap(self.pass_index)})
+        H = sc.struct_hash_depths(dec, depths)
+        row_of = {cap(x): i for i, x in enumerate(depths)}
+        h = H[0]
         if self.world > 1:
             mine = torch.nonzero(torch.remainder(h, self.world) == self.rank).flatten()
             d = dec.index_select(0, mine)
@@ -180,8 +187,7 @@ class StepPlan:
         if n_all > 1 and mem_src.numel():
             keep = torch.nonzero(bot[:mem_src.numel()]).flatten()
             bsel = mem_src.index_select(0, keep)
-            h3 = ph.index_select(0, keep) if self.pass_index >= 3 else None
-            memo = sc.memo_hashes(dec.index_select(0, bsel), self.num_passes, h3=h3)
+            memo = [H[row_of[cap(x)]].index_select(0, bsel) for x in range(1, self.num_passes + 1)]
         mark()
         if times is not None:
             torch.cuda.synchronize()

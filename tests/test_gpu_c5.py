@@ -110,6 +110,17 @@ def test_sample_features_costs_verdicts_hashes(golden, step):
         assert [str(int(x)) for x in hs] == [h[depth] for h in meta["hashes"]], depth
 
 
+def test_multi_depth_hash_on_full_step(step):
+    """One K3 pass at the pass depth and the memo depths equals one pass per
+    depth over the whole 1M-candidate step (run heads hashed, followers
+    filled at every depth)."""
+    sc, dec, _ = step
+    depths = [3, 1, 2]
+    H = sc.struct_hash_depths(dec, depths)
+    for row, depth in enumerate(depths):
+        assert torch.equal(H[row], sc.struct_hash(dec, depth)), depth
+
+
 @pytest.mark.parametrize("variant", ["bench", "memo", "memo_T05"])
 def test_full_step_cut_equals_reference(golden, step, variant):
     meta, arr = golden

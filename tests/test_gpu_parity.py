@@ -61,6 +61,12 @@ def test_features_costs_hashes_match_reference(name, dev):
         h = sc.struct_hash(dec, depth).cpu().numpy().view(np.uint64)
         want = np.array([cs.hashes[i][depth] for i in range(len(cs))], dtype=np.uint64)
         assert np.array_equal(h, want), (name, depth)
+    # several depths in one K3 pass (the beam step's pass + memo depths)
+    for depths in ([0, 1, 2, 3], [5, 1, 4]):
+        H = sc.struct_hash_depths(dec, depths).cpu().numpy().view(np.uint64)
+        for row, depth in enumerate(depths):
+            want = np.array([cs.hashes[i][depth] for i in range(len(cs))], dtype=np.uint64)
+            assert np.array_equal(H[row], want), (name, depths, depth)
 
 
 @pytest.mark.parametrize("name", ["chain3", "diamond", "stencil_chain"])
