@@ -1,11 +1,12 @@
 // K1 — per-candidate resolve + 56 schedule features per stage row + prune
 // (reference featurize.py:275-617, resolve.py:207-425, options.py:200-255).
 //
-// One CTA per SM; every warp is an independent scorer with its own slice of
-// shared memory, taking work units from a global counter:
+// One CTA per SM (up to 12 warps); every warp is a scorer with its own slice
+// of shared memory (capacity-sized arrays optionally in an L1-cached global
+// scratch: spill levels), taking work from a global counter:
 //   * the candidate-independent pipeline descriptor is staged ONCE per CTA
 //     into shared memory with a bulk async copy (TMA `cp.async.bulk`, SASS
-//     UBLKCP) completing on an mbarrier — the only CTA-wide barrier;
+//     UBLKCP) completing on an mbarrier;
 //   * per candidate the warp loads its 16-byte decision records with 128-bit
 //     loads, diffs them against the previous candidate it scored (siblings
 //     of a beam step share their decision structure), re-resolves only the
@@ -13,15 +14,23 @@
 //     prune verdict warp-parallel, and recomputes only the feature rows whose
 //     own / host / kernel / producer-layout records changed (the rest are
 //     bit-identical copies, or — reuse mode 2 — not written at all);
+//   * the CTA's warps run in lockstep: phase A (records, diff, resolve,
+//     prune, row flags) for every warp's candidate, a CTA barrier, then the
+//     feature rows, and a barrier again, so the SM streams one phase's code
+//     at a time;
 //   * large batches of long sibling runs use a two-phase schedule: run heads
-//     first (each saves its warp state to its run's slot in HBM), then
-//     16-candidate sibling slices that resume from their head's state, so a
-//     run splits across warps without re-resolving;
+//     first (each saves the persistent prefix of its warp state to its run's
+//     slot in HBM), then 5-candidate sibling slices, claimed 12 at a time per
+//     CTA, that resume from their head's state, so a run splits across warps
+//     without re-resolving; the sibling launch pools the CTA's dirty rows in
+//     row-major order (row q of every warp's candidate, then q + 1), each
+//     taken by the next free warp;
 //   * warp-instruction transaction counts (featurize.py:173-196, 508-571)
 //     use the residue invariance of the counts (global: address constant mod
 //     32 B; shared: mod the 4 B bank width): residue histograms in registers,
-//     interval sums over one prefix scan for monotonic warps, and
-//     __match_any_sync / __ballot_sync for the rest.
+//     interval sums over one prefix scan for monotonic warps, one evaluation
+//     per shift class for regular thread tiles, and __match_any_sync /
+//     __ballot_sync for the rest.
 // See DESIGN.md "K1 featurize" for the roofline reading.
 #include "gs_internal.cuh"
 #include "scan.cuh"

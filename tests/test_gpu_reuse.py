@@ -138,6 +138,20 @@ def test_rows_only_mode(src, parents, dev):
     assert torch.equal(t1, t2)
     with pytest.raises(ValueError):
         sc.cost(f2, reuse=False)
+    # against reuse off (every row of every candidate computed from its own
+    # records, no run slots, no pooled rows): the computed rows are equal,
+    # every shared row's source row is equal to the row it stands for, and
+    # the totals are bit-equal
+    sc.set_reuse(0)
+    f0 = sc.featurize(d)
+    t0, _, _ = sc.cost(f0)
+    sc.check()
+    z = f0["feats"].cpu().numpy()
+    assert np.array_equal(z[own], b["feats"][own])
+    valid = np.arange(sc.R)[None, :] < b["n_rows"][:, None]
+    ci, ri = np.nonzero(valid)
+    assert np.array_equal(z[ci, ri], z[b["row_src"][ci, ri], ri])
+    assert torch.equal(t0, t2)
     sc.set_reuse(True)
 
 
