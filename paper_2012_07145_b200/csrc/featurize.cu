@@ -2430,6 +2430,14 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   // eight rows, some of them 256-channel windows) run free (the same loop
   // without barriers): lockstep took C4's K1 from 88 to 122 ms.
   const bool lockstep = mode != 0 || L.R >= 16;   // 1M C5 K1 without: 101 ms
+  // Reuse mode 2 (rows written only where computed): the run-head launch
+  // resolves and prunes the heads but leaves their feature rows to the
+  // sibling launch, where a head is the first candidate of its run with
+  // every row dirty and its rows join the CTA's pool — the head launch's
+  // tail (~2.4 heads per warp) shrinks to the resolve.  With reuse mode 1
+  // a sibling copies its predecessor's feature block, so heads keep their
+  // rows.
+  const bool heads_later = reuse == 2 && feats != nullptr && mode != 0;
   {
     int64_t c = 0, c1 = 0, pc = 0, cur_run = -1, jcur = -1;
     bool done = false;
@@ -2442,7 +2450,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     for (;;) {
       bool have = false;
       if (cta_blocks) {
-        while (c < c1 && heads[c]) { cur_run = -1; ++c; }
+        while (c < c1 && heads[c] && !heads_later) { cur_run = -1; ++c; }
         if (__syncthreads_and(c >= c1)) {
           if (threadIdx.x == 0) s_base = (int64_t)atomicAdd(work, (unsigned)nw);
           __syncthreads();
@@ -2458,7 +2466,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
             c = c0; pc = c0; cur_run = -1;
             if (lane == 0) { m.prev_valid = 0; m.same_struct = 0; m.ndec = 0; }
             __syncwarp();
-            while (c < c1 && heads[c]) { cur_run = -1; ++c; }
+            while (c < c1 && heads[c] && !heads_later) { cur_run = -1; ++c; }
           }
         }
         have = c < c1;
@@ -2486,7 +2494,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
           if (lane == 0) { m.prev_valid = 0; m.same_struct = 0; m.ndec = 0; }
           __syncwarp();
         }
-        if (mode == 2 && heads[c]) { cur_run = -1; ++c; continue; }
+        if (mode == 2 && heads[c] && !heads_later) { cur_run = -1; ++c; continue; }
         have = true;
         break;
       }
@@ -2497,14 +2505,29 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
       } else if (!have) {
         break;
       }
+      bool head_rows = false;   // mode 2: a run head whose state the slot holds
       if (have) {
         if (mode == 2) {
           const int64_t r = run_id[c];
           if (r != cur_run) { slot_copy(r, false); pc = run_head[r]; cur_run = r; }
+          head_rows = heads_later && c == pc && heads[c];
         }
-        phaseA(c, pc);
+        if (!head_rows) phaseA(c, pc);
       }
-      if (have) { phaseResolve(); phaseA2(c, pc); }
+      if (have && !head_rows) { phaseResolve(); phaseA2(c, pc); }
+      if (head_rows) {
+        // verdict and n_rows came from the head launch; every row is computed
+        nr = m.nrows;
+        nd = nr;
+        diffable = false;
+        for (int r = lane; r < nr; r += 32) { k.rowlist[r] = (int16_t)r; rsrc[r] = (int32_t)c; }
+        __syncwarp();
+        if (lane == 0) st_rows += nd;
+      }
+      if (have && mode == 1 && heads_later) {   // the head's rows: in the sibling launch
+        if (lane == 0) st_rows -= nd;
+        nd = 0;
+      }
       // sibling slices pool their rows (1M C5 K1 58.3 -> 54.4 ms, C2 7.0 ->
       // 5.2 ms); run heads and whole candidates (modes 1 / 0: ~100 rows
       // each, even work) measured 1-10 % slower pooled
@@ -2548,7 +2571,15 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
           phaseRow(kr, c, q);
         }
       }
-      if (have) { phaseB3(c); pc = c; ++c; }
+      if (have) {
+        if (mode == 1 && heads_later) {   // row keys / sources are written with the rows
+          if (lane == 0) m.prev_valid = m.err == 0;
+          __syncwarp();
+        } else {
+          phaseB3(c);
+        }
+        pc = c; ++c;
+      }
       if (lockstep) __syncthreads();
     }
   }
