@@ -270,20 +270,37 @@ __device__ __noinline__ void resolve_structure(K1<ND>& k) {
     if (k.dec[i].kind == GS_INLINE) k.rows[nr++] = (k.dec[i].func << 8);
   m.nrows = nr;
   // per-row dependencies besides its own func / host / kernel: producers of
-  // the reads it owns and its fuse_at_thread children
+  // the reads it owns and its fuse_at_thread children.  The children come
+  // from a consumer CSR (kmb offsets, kml list, icb cursors: scratch here,
+  // rebuilt as the kernel CSRs below), an inline row's reads from the root
+  // stages it was expanded into (its icall entries), so the build is linear
+  // in decisions + reads (it was rows x decisions and inline rows x reads:
+  // half of the run-head launch).
+  for (int f = 0; f <= nf; ++f) k.kmb[f] = 0;
+  for (int i = 0; i < m.ndec; ++i)
+    if (k.dec[i].kind == GS_FUSE_THREAD) k.kmb[k.dec[i].consumer + 1]++;
+  for (int f = 0; f < nf; ++f) k.kmb[f + 1] += k.kmb[f];
+  for (int f = 0; f < nf; ++f) k.icb[f] = k.kmb[f];
+  for (int i = 0; i < m.ndec; ++i)
+    if (k.dec[i].kind == GS_FUSE_THREAD) k.kml[k.icb[k.dec[i].consumer]++] = (int16_t)k.dec[i].func;
   int nd = 0;
+  const int cap = k.rcap + nf;
   for (int r = 0; r < nr; ++r) {
     k.rdepb[r] = nd;
     const int f = k.rows[r] >> 8, si = k.rows[r] & 255;
-    const bool inl = k.dec[k.didx[f]].kind == GS_INLINE;
-    int lo = inl ? 0 : k.rdb[2 * (k.F[f].stage_begin + si)];
-    int hi = inl ? m.nreads : k.rdb[2 * (k.F[f].stage_begin + si) + 1];
-    for (int j = lo; j < hi; ++j)
-      if (k.rd[j].owner == f && nd < k.rcap + nf) k.rdep[nd++] = k.rd[j].producer;
-    if (!inl)
-      for (int i = 0; i < m.ndec; ++i)
-        if (k.dec[i].kind == GS_FUSE_THREAD && k.dec[i].consumer == f && nd < k.rcap + nf)
-          k.rdep[nd++] = (int16_t)k.dec[i].func;
+    if (k.dec[k.didx[f]].kind == GS_INLINE) {
+      for (int e = 0; e < m.nicall; ++e) {
+        if (k.icall[e].iname != f) continue;
+        const int g = k.F[k.icall[e].root].stage_begin + k.icall[e].stage;
+        for (int j = k.rdb[2 * g]; j < k.rdb[2 * g + 1]; ++j)
+          if (k.rd[j].owner == f && nd < cap) k.rdep[nd++] = k.rd[j].producer;
+      }
+    } else {
+      const int g = k.F[f].stage_begin + si;
+      for (int j = k.rdb[2 * g]; j < k.rdb[2 * g + 1]; ++j)
+        if (k.rd[j].owner == f && nd < cap) k.rdep[nd++] = k.rd[j].producer;
+      for (int q = k.kmb[f]; q < k.kmb[f + 1] && nd < cap; ++q) k.rdep[nd++] = k.kml[q];
+    }
   }
   k.rdepb[nr] = nd;
 
