@@ -305,6 +305,250 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) cost_rows_kernel(NetDev ne
   }
 }
 
+// ---------------------------------------------------------------------------
+// K2 on the fp64 tensor cores (DMMA m8n8k4).  Same queue/claim structure as
+// cost_rows_kernel, but a warp evaluates its 32 queued rows TOGETHER: the
+// three layers are 32-row GEMMs (X[32x56]·Ws, relu(E)[32xE]·Whs[E:], relu(Z)
+// [32xH]·Wo) issued as m8n8k4 fp64 MMAs, one per 256 FMAs instead of one
+// DFMA per 32.  The weights live in shared memory pre-arranged in B-fragment
+// order (frag[kb][nb][lane] = B[4kb + lane%4][8nb + lane/4]), so each
+// fragment is one conflict-free 8-byte load per lane.  The log1p of the
+// features is taken directly in A-fragment order (lane 4r+j owns
+// X[r][4kb+j]); C fragments are turned into the next layer's A fragments
+// with quad shuffles.  The pre-softplus outputs go through a per-warp
+// shared-memory tile so that the row's owner lane does softplus + the basis
+// dot exactly as the scalar path does.  Accumulation order inside an MMA
+// differs from the scalar FMA chains: costs agree with the reference to
+// ~1e-15 relative (tolerance 1e-9, tests/test_gpu_parity.py).
+#ifndef GS_K2M_WARPS
+#define GS_K2M_WARPS 16
+#endif
+#ifndef GS_K2M_SP
+#define GS_K2M_SP 2
+#endif
+static_assert(GS_K2M_SP == 2 || GS_K2M_SP == 4, "");
+constexpr int kMmaWarps = GS_K2M_WARPS;
+constexpr int kCS = 33;   // per-warp coefficient tile row stride (doubles)
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// A fragment of k-block (4h + j) within an 8-column C tile: lane 4r+j takes
+// column 4h+j of row r, held by lane 4r + 2h + j/2 as element j%2
+__device__ __forceinline__ double c_to_a(double c0, double c1, int h, int lane) {
+  const int src = (lane & ~3) | (2 * h + ((lane & 3) >> 1));
+  const double v0 = __shfl_sync(0xffffffffu, c0, src), v1 = __shfl_sync(0xffffffffu, c1, src);
+  return (lane & 1) ? v1 : v0;
+}
+
+template <int E, int H>
+__global__ void __launch_bounds__(kMmaWarps * 32, 1) cost_rows_mma_kernel(
+    NetDev net, const int32_t* __restrict__ stage_of_func, const double* __restrict__ feats,
+    const int32_t* __restrict__ row_key, const int32_t* __restrict__ n_rows, const int32_t* __restrict__ row_src,
+    int64_t n, int R, double* __restrict__ row_cost, unsigned* __restrict__ work, int64_t kSpan) {
+  static_assert(E % 8 == 0 && H % 8 == 0 && E <= 64 && H <= 128, "");
+  constexpr int KB1 = GS_NUM_FEATURES / 4, NB1 = E / 8;   // layer 1: 14 k-blocks x E/8 n-tiles
+  constexpr int KB2 = E / 4, NB2 = H / 8;                 // layer 2
+  constexpr int NB3 = 4;                                  // 30 coefficients padded to 32
+  extern __shared__ __align__(16) double smd[];
+  __shared__ int64_t ring[kMmaWarps][kRing];
+  double* w1 = smd;                          // KB1*NB1*32
+  double* w2 = w1 + KB1 * NB1 * 32;          // KB2*NB2*32
+  double* w3 = w2 + KB2 * NB2 * 32;          // (H/4)*NB3*32
+  double* bs = w3 + (H / 4) * NB3 * 32;      // E
+  double* bo = bs + E;                       // 32
+  double* cs = bo + 32;                      // kMmaWarps x 32 x kCS
+  for (int i = threadIdx.x; i < KB1 * NB1 * 32; i += blockDim.x) {
+    const int l = i & 31, t = i >> 5, nb = t % NB1, kb = t / NB1;
+    w1[i] = net.sched_w[(4 * kb + (l & 3)) * E + 8 * nb + (l >> 2)];
+  }
+  for (int i = threadIdx.x; i < KB2 * NB2 * 32; i += blockDim.x) {
+    const int l = i & 31, t = i >> 5, nb = t % NB2, kb = t / NB2;
+    w2[i] = net.head_w[(E + 4 * kb + (l & 3)) * H + 8 * nb + (l >> 2)];
+  }
+  for (int i = threadIdx.x; i < (H / 4) * NB3 * 32; i += blockDim.x) {
+    const int l = i & 31, t = i >> 5, nb = t % NB3, kb = t / NB3;
+    const int o = 8 * nb + (l >> 2);
+    w3[i] = o < GS_NUM_COEFFS ? net.out_w[(4 * kb + (l & 3)) * GS_NUM_COEFFS + o] : 0.0;
+  }
+  for (int i = threadIdx.x; i < E; i += blockDim.x) bs[i] = net.sched_b[i];
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) bo[i] = i < GS_NUM_COEFFS ? net.out_b[i] : 0.0;
+  __syncthreads();
+  const int64_t total_rows = n * (int64_t)R;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int qr = lane >> 2, qc = lane & 3;
+  int64_t* q = ring[warp];
+  double* ct = cs + warp * 32 * kCS;
+
+  // the warp's 32 queued rows (cnt valid; the rest repeat row 0 and are not written)
+  auto run_warp = [&](unsigned h0, int cnt) {
+    int64_t rrow[4];
+    const double* hz[4];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int r = 8 * mt + qr;
+      rrow[mt] = q[(h0 + (r < cnt ? r : 0)) & (kRing - 1)];
+      const int key = __ldg(row_key + rrow[mt]);
+      hz[mt] = net.hoisted + (int64_t)(stage_of_func[key >> 8] + (key & 255)) * H;
+    }
+    // layer 1: E1 = relu(log1p(X) Ws + bs)
+    double e1[4][NB1][2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nb = 0; nb < NB1; ++nb) {
+        e1[mt][nb][0] = bs[8 * nb + 2 * qc];
+        e1[mt][nb][1] = bs[8 * nb + 2 * qc + 1];
+      }
+    // feature loads run two k-blocks ahead of their log1p (the loads are
+    // L2 / HBM latency; without the prefetch they were the top stall)
+    const double* fp[4];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) fp[mt] = feats + rrow[mt] * GS_NUM_FEATURES + qc;
+    double f0[4], f1[4];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) { f0[mt] = __ldg(fp[mt]); f1[mt] = __ldg(fp[mt] + 4); }
+#pragma unroll 1
+    for (int kb = 0; kb < KB1; ++kb) {
+      double a[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const double fk = f0[mt];
+        f0[mt] = f1[mt];
+        if (kb + 2 < KB1) f1[mt] = __ldg(fp[mt] + 4 * (kb + 2));
+        a[mt] = fk == 0.0 ? 0.0 : log1p(fk);
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB1; ++nb) {
+        const double b = w1[(kb * NB1 + nb) * 32 + lane];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) dmma(e1[mt][nb][0], e1[mt][nb][1], a[mt], b);
+      }
+    }
+    // relu(E1) as layer-2 A fragments, parked in the warp's coefficient tile
+    // (fragment order: one conflict-free load per lane; keeps the 32 doubles
+    // out of registers so 16 warps fit without spills)
+    static_assert(4 * KB2 * 32 <= 32 * kCS, "");
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nb = 0; nb < NB1; ++nb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          ct[(mt * KB2 + 2 * nb + h) * 32 + lane] =
+              c_to_a(fmax(e1[mt][nb][0], 0.0), fmax(e1[mt][nb][1], 0.0), h, lane);
+    __syncwarp();
+    // layers 2 + 3, one 8-unit block of the hidden layer at a time
+    double zo[4][NB3][2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int ot = 0; ot < NB3; ++ot) {
+        zo[mt][ot][0] = bo[8 * ot + 2 * qc];
+        zo[mt][ot][1] = bo[8 * ot + 2 * qc + 1];
+      }
+#pragma unroll 1
+    for (int nb = 0; nb < NB2; ++nb) {
+      double z[4][2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        z[mt][0] = __ldg(hz[mt] + 8 * nb + 2 * qc);
+        z[mt][1] = __ldg(hz[mt] + 8 * nb + 2 * qc + 1);
+      }
+#pragma unroll
+      for (int kb = 0; kb < KB2; ++kb) {
+        const double b = w2[(kb * NB2 + nb) * 32 + lane];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) dmma(z[mt][0], z[mt][1], ct[(mt * KB2 + kb) * 32 + lane], b);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double a3[4];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) a3[mt] = c_to_a(fmax(z[mt][0], 0.0), fmax(z[mt][1], 0.0), h, lane);
+#pragma unroll
+        for (int ot = 0; ot < NB3; ++ot) {
+          const double b = w3[((2 * nb + h) * NB3 + ot) * 32 + lane];
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) dmma(zo[mt][ot][0], zo[mt][ot][1], a3[mt], b);
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int ot = 0; ot < NB3; ++ot) {
+        ct[(8 * mt + qr) * kCS + 8 * ot + 2 * qc] = zo[mt][ot][0];
+        ct[(8 * mt + qr) * kCS + 8 * ot + 2 * qc + 1] = zo[mt][ot][1];
+      }
+    __syncwarp();
+    if (lane < cnt) {
+      const int64_t row = q[(h0 + lane) & (kRing - 1)];
+      double* c = ct + lane * kCS;
+      // GS_K2M_SP independent softplus evaluations per step (the padded
+      // columns 30, 31 hold finite values and are never read by the dot)
+#pragma unroll 1
+      for (int o = 0; o < GS_NUM_COEFFS; o += GS_K2M_SP) {
+        double v[GS_K2M_SP];
+#pragma unroll
+        for (int u = 0; u < GS_K2M_SP; ++u) v[u] = softplus_bf(c[o + u]);
+#pragma unroll
+        for (int u = 0; u < GS_K2M_SP; ++u) c[o + u] = v[u] + kEps;
+      }
+      row_cost[row] = basis_dot<1>(feats + row * GS_NUM_FEATURES, c, nullptr);
+    }
+    __syncwarp();
+  };
+
+  constexpr int kBatch = 4;
+  auto claim = [&]() -> int64_t {
+    unsigned v = 0;
+    if (lane == 0) v = atomicAdd(work, 1u);
+    return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+  };
+  int64_t sp = claim(), s0 = sp * kSpan;
+  unsigned head = 0, tail = 0;
+  for (;;) {
+    while (tail - head < 32 && s0 < total_rows) {
+      const int64_t end = sp * kSpan + kSpan < total_rows ? sp * kSpan + kSpan : total_rows;
+      unsigned tm = 0;
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int64_t row = s0 + 32 * u + lane;
+        if (row < end) {
+          const int64_t c = row / R;
+          const int r = (int)(row - c * R);
+          tm |= (unsigned)(r < __ldg(n_rows + c) && __ldg(row_src + row) == (int32_t)c) << u;
+        }
+      }
+#pragma unroll 1
+      for (int u = 0; u < kBatch; ++u) {
+        const bool t = (tm >> u) & 1u;
+        const unsigned b = __ballot_sync(0xffffffffu, t);
+        if (t) q[(tail + __popc(b & ((1u << lane) - 1))) & (kRing - 1)] = s0 + 32 * u + lane;
+        tail += __popc(b);
+      }
+      s0 += 32 * kBatch;
+      if (s0 >= end) { sp = claim(); s0 = sp * kSpan; }
+    }
+    if (tail == head) break;
+    __syncwarp();
+    const int cnt = tail - head < 32 ? (int)(tail - head) : 32;
+    run_warp(head, cnt);
+    head += cnt;
+  }
+}
+
+template <int E, int H>
+int mma_smem_bytes() {
+  return ((GS_NUM_FEATURES / 4) * (E / 8) * 32 + (E / 4) * (H / 8) * 32 + (H / 4) * 4 * 32 + E + 32 +
+          kMmaWarps * 32 * kCS) * 8;
+}
+
 __global__ void __launch_bounds__(128) stage_sum_kernel(const int32_t* __restrict__ n_rows,
                                                         const int32_t* __restrict__ row_src,
                                                         const double* __restrict__ row_cost, int64_t n, int R,
@@ -362,7 +606,16 @@ int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* f
     const int64_t rows_total = n * (int64_t)R, warps = (int64_t)gridA * kRowsWarps;
     int64_t span = 2048;
     while (span > 128 && rows_total / span < 4 * warps) span >>= 1;
-    if (net.E <= 32) {
+    static const bool scalar_only = getenv("GS_K2_SCALAR") != nullptr;   // A/B switch for the DMMA path
+    if (net.E == 32 && net.H == 64 && !scalar_only) {
+      const int smM = mma_smem_bytes<32, 64>();
+      const int64_t wM = (int64_t)gridA * kMmaWarps;
+      int64_t spanM = 2048;
+      while (spanM > 128 && rows_total / spanM < 4 * wM) spanM >>= 1;
+      cudaFuncSetAttribute(cost_rows_mma_kernel<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smM);
+      cost_rows_mma_kernel<32, 64><<<gridA, kMmaWarps * 32, smM, st>>>(net, stage_of_func, feats, row_key, n_rows,
+                                                                      row_src, n, R, row_cost, work, spanM);
+    } else if (net.E <= 32) {
       cudaFuncSetAttribute(cost_rows_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smA);
       cost_rows_kernel<32><<<gridA, kRowsWarps * 32, smA, st>>>(net, stage_of_func, feats, row_key, n_rows, row_src,
                                                                 n, R, row_cost, work, span);

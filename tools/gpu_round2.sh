@@ -10,7 +10,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
    --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-extras > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:featurize_kernel -s 1 -c 1 \
    -o gpurun_out/prof_k1 -f python tools/prof_k1.py 1000 > gpurun_out/ncu_full.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:cost_rows_kernel -s 1 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:cost_rows -s 1 -c 1 \
    -o gpurun_out/prof_k2 -f python tools/prof_k1.py 1000 > gpurun_out/ncu_full_k2.log 2>&1
 timeout 1200 python tools/search_timing.py --beam 8 --passes 2 > gpurun_out/search_b8.json 2> gpurun_out/search_b8.err
 exit 0
