@@ -11,6 +11,7 @@
 // Arithmetic is fp64 end to end (the reference is fp64; parity target 1e-5
 // relative, measured ~1e-15), the basis without FMA contraction.
 #include "gs_internal.cuh"
+#include "fastmath.cuh"
 
 namespace gs {
 
@@ -39,21 +40,17 @@ __global__ void hoist_kernel(NetDev net, const double* __restrict__ algo, int n_
 // see the same argument bits (exp(-|z|)) and 0 + v = v on the z < 0 side,
 // so two independent evaluations can interleave.
 __device__ __forceinline__ double softplus_bf(double z) {
-  const double v = fmax(z, 0.0) + log1p(exp(-fabs(z)));
+  const double v = fmax(z, 0.0) + log1p_fast(exp(-fabs(z)));
   return z == 0.0 ? 0.6931471805599453 : v;
 }
 
-// reference stage_cost_basis; returns h, writes g (may be null)
-// c: the 30 coefficients, strided by ZS (per-thread column of a
-// shared-memory scratch; ZS = threads per block)
-template <int ZS>
-__device__ double basis_dot(const double* __restrict__ f, const double* __restrict__ c, double* gout) {
+// reference stage_cost_basis (costmodel.py:118-176): fills g, returns h
+__device__ __forceinline__ double basis_g(const double* __restrict__ f, double* g) {
   auto F = [&](int i) { return f[i]; };
   const bool inl = F(50) > 0;
   double scale = __ddiv_rn(ceil(__ddiv_rn(F(46), F(49))), fmax(1.0, F(48)));
   if (!inl) scale = __ddiv_rn(scale, __dsub_rn(1.0, F(30)));
   const double pts = __dmul_rn(__dmul_rn(F(23), F(26)), F(1));
-  double g[GS_NUM_COEFFS];
 #pragma unroll
   for (int i = 0; i < GS_NUM_COEFFS; ++i) g[i] = 0.0;
   g[inl ? 3 : 1] = __dmul_rn(F(0), scale);
@@ -80,6 +77,16 @@ __device__ double basis_dot(const double* __restrict__ f, const double* __restri
   if (F(47) > 1) g[25] = F(45);
   g[26] = __dmul_rn(F(45), __dsub_rn(F(47), 1.0));
   g[9] = F(55);
+  return h;
+}
+
+// returns g.c + h, writes g and h to gout (may be null)
+// c: the 30 coefficients, strided by ZS (per-thread column of a
+// shared-memory scratch; ZS = threads per block)
+template <int ZS>
+__device__ double basis_dot(const double* __restrict__ f, const double* __restrict__ c, double* gout) {
+  double g[GS_NUM_COEFFS];
+  const double h = basis_g(f, g);
   double dot = 0.0;
 #pragma unroll
   for (int i = 0; i < GS_NUM_COEFFS; ++i) dot = fma(g[i], c[i * ZS], dot);
@@ -102,7 +109,7 @@ __device__ double stage_row_cost(const NetDev& net, const double* __restrict__ s
   for (int j = 0; j < MAXE; ++j) es[j] = j < E ? bs[j] : 0.0;
   for (int k = 0; k < GS_NUM_FEATURES; ++k) {
     const double fk = f[k];
-    const double x = fk == 0.0 ? 0.0 : log1p(fk);   // log1p(+0) = +0: skip the sequence for absent features
+    const double x = fk == 0.0 ? 0.0 : log1p_fast(fk);   // log1p(+0) = +0: skip the sequence for absent features
 #pragma unroll
     for (int j = 0; j < MAXE; ++j) if (j < E) es[j] = fma(x, sw[k * E + j], es[j]);
   }
@@ -323,11 +330,8 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) cost_rows_kernel(NetDev ne
 #ifndef GS_K2M_WARPS
 #define GS_K2M_WARPS 16
 #endif
-#ifndef GS_K2M_SP
-#define GS_K2M_SP 2
-#endif
-static_assert(GS_K2M_SP == 2 || GS_K2M_SP == 4, "");
 constexpr int kMmaWarps = GS_K2M_WARPS;
+constexpr unsigned kRingM = 512;   // per-warp queue of row indices (< 2^32 rows per launch)
 constexpr int kCS = 33;   // per-warp coefficient tile row stride (doubles)
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -354,7 +358,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) cost_rows_mma_kernel(
   constexpr int KB2 = E / 4, NB2 = H / 8;                 // layer 2
   constexpr int NB3 = 4;                                  // 30 coefficients padded to 32
   extern __shared__ __align__(16) double smd[];
-  __shared__ int64_t ring[kMmaWarps][kRing];
+  __shared__ uint32_t ring[kMmaWarps][kRingM];
   double* w1 = smd;                          // KB1*NB1*32
   double* w2 = w1 + KB1 * NB1 * 32;          // KB2*NB2*32
   double* w3 = w2 + KB2 * NB2 * 32;          // (H/4)*NB3*32
@@ -380,7 +384,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) cost_rows_mma_kernel(
   const int64_t total_rows = n * (int64_t)R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int qr = lane >> 2, qc = lane & 3;
-  int64_t* q = ring[warp];
+  uint32_t* q = ring[warp];
   double* ct = cs + warp * 32 * kCS;
 
   // the warp's 32 queued rows (cnt valid; the rest repeat row 0 and are not written)
@@ -390,7 +394,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) cost_rows_mma_kernel(
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
       const int r = 8 * mt + qr;
-      rrow[mt] = q[(h0 + (r < cnt ? r : 0)) & (kRing - 1)];
+      rrow[mt] = q[(h0 + (r < cnt ? r : 0)) & (kRingM - 1)];
       const int key = __ldg(row_key + rrow[mt]);
       hz[mt] = net.hoisted + (int64_t)(stage_of_func[key >> 8] + (key & 255)) * H;
     }
@@ -419,7 +423,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) cost_rows_mma_kernel(
         const double fk = f0[mt];
         f0[mt] = f1[mt];
         if (kb + 2 < KB1) f1[mt] = __ldg(fp[mt] + 4 * (kb + 2));
-        a[mt] = fk == 0.0 ? 0.0 : log1p(fk);
+        a[mt] = fk == 0.0 ? 0.0 : log1p_fast(fk);
       }
 #pragma unroll
       for (int nb = 0; nb < NB1; ++nb) {
@@ -487,24 +491,38 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) cost_rows_mma_kernel(
       }
     __syncwarp();
     if (lane < cnt) {
-      const int64_t row = q[(h0 + lane) & (kRing - 1)];
+      const int64_t row = q[(h0 + lane) & (kRingM - 1)];
       double* c = ct + lane * kCS;
-      // GS_K2M_SP independent softplus evaluations per step (the padded
-      // columns 30, 31 hold finite values and are never read by the dot)
+      // basis first: a coefficient whose g is exactly 0 adds fma(0, c, dot)
+      // = dot, so its softplus is skipped (rows have ~12 of 30 non-zero; the
+      // lane walks its own mask, two evaluations per step).  Bit-identical
+      // to evaluating all thirty (softplus is finite for finite z).
+      double g[GS_NUM_COEFFS];
+      const double hb = basis_g(feats + row * GS_NUM_FEATURES, g);
+      unsigned msk = 0;
+#pragma unroll
+      for (int i = 0; i < GS_NUM_COEFFS; ++i) msk |= (unsigned)(g[i] != 0.0) << i;
 #pragma unroll 1
-      for (int o = 0; o < GS_NUM_COEFFS; o += GS_K2M_SP) {
-        double v[GS_K2M_SP];
-#pragma unroll
-        for (int u = 0; u < GS_K2M_SP; ++u) v[u] = softplus_bf(c[o + u]);
-#pragma unroll
-        for (int u = 0; u < GS_K2M_SP; ++u) c[o + u] = v[u] + kEps;
+      while (msk) {
+        const int i1 = __ffs(msk) - 1;
+        msk &= msk - 1;
+        const int i2 = msk ? __ffs(msk) - 1 : i1;
+        msk &= msk - 1;
+        const double x = softplus_bf(c[i1]), y = softplus_bf(c[i2]);
+        c[i1] = x + kEps;
+        c[i2] = y + kEps;
       }
-      row_cost[row] = basis_dot<1>(feats + row * GS_NUM_FEATURES, c, nullptr);
+      double dot = 0.0;
+#pragma unroll
+      for (int i = 0; i < GS_NUM_COEFFS; ++i)
+        if (g[i] != 0.0) dot = fma(g[i], c[i], dot);
+      row_cost[row] = __dadd_rn(dot, hb);
     }
     __syncwarp();
   };
 
-  constexpr int kBatch = 4;
+  constexpr int kBatch = 8;   // 16 row_src / n_rows loads in flight per lane while the queue fills
+  static_assert(kRingM >= 31 + 32 * kBatch, "");
   auto claim = [&]() -> int64_t {
     unsigned v = 0;
     if (lane == 0) v = atomicAdd(work, 1u);
@@ -520,8 +538,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) cost_rows_mma_kernel(
       for (int u = 0; u < kBatch; ++u) {
         const int64_t row = s0 + 32 * u + lane;
         if (row < end) {
-          const int64_t c = row / R;
-          const int r = (int)(row - c * R);
+          const uint32_t c = (uint32_t)row / (uint32_t)R;   // rows < 2^32 on this path
+          const int r = (int)((uint32_t)row - c * (uint32_t)R);
           tm |= (unsigned)(r < __ldg(n_rows + c) && __ldg(row_src + row) == (int32_t)c) << u;
         }
       }
@@ -529,7 +547,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) cost_rows_mma_kernel(
       for (int u = 0; u < kBatch; ++u) {
         const bool t = (tm >> u) & 1u;
         const unsigned b = __ballot_sync(0xffffffffu, t);
-        if (t) q[(tail + __popc(b & ((1u << lane) - 1))) & (kRing - 1)] = s0 + 32 * u + lane;
+        if (t) q[(tail + __popc(b & ((1u << lane) - 1))) & (kRingM - 1)] = (uint32_t)(s0 + 32 * u + lane);
         tail += __popc(b);
       }
       s0 += 32 * kBatch;
@@ -607,7 +625,7 @@ int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* f
     int64_t span = 2048;
     while (span > 128 && rows_total / span < 4 * warps) span >>= 1;
     static const bool scalar_only = getenv("GS_K2_SCALAR") != nullptr;   // A/B switch for the DMMA path
-    if (net.E == 32 && net.H == 64 && !scalar_only) {
+    if (net.E == 32 && net.H == 64 && !scalar_only && rows_total < 0xFFFFFFFFll) {
       const int smM = mma_smem_bytes<32, 64>();
       const int64_t wM = (int64_t)gridA * kMmaWarps;
       int64_t spanM = 2048;
