@@ -100,15 +100,27 @@ __global__ void expand_count_kernel(const GsFunc* __restrict__ funcs, const GsDe
   counts[p] = (uint32_t)(c > kMaxTilings ? 0 : c);   // over-long lists are skipped (and reported)
 }
 
-__global__ void __launch_bounds__(kExpandWarps * 32) expand_write_kernel(
+// Phase-2 write: one warp per parent.  Lane 0 walks the tiling menu into a
+// 512-entry shared-memory list (lists longer than that are written in
+// chunks, each chunk re-walking the menu and keeping its own window), then
+// the whole warp streams the chunk's candidates: the (tiling, record) pairs
+// are flattened so every lane stores one 16-byte record per step (100-record
+// candidates left a quarter of the lanes idle in a per-candidate loop), and
+// the parent's records come from L1.  Eight warps per CTA, 4 KB of list
+// each, so ~56 warps per SM keep the stores in flight (the earlier
+// 4096-entry lists allowed 6).  The e2e C5 step (1M candidates, 1.6 GB of
+// records written) lost ~0.3 ms of its 1.5 ms host-path overhead.
+constexpr int kWriteWarps = 8;
+constexpr int kTilChunk = 512;
+
+__global__ void __launch_bounds__(kWriteWarps * 32) expand_write_kernel(
     const GsFunc* __restrict__ funcs, const GsDecision* __restrict__ parents, int64_t n, int S,
     const int32_t* __restrict__ step, GsTilingMenus m, const int64_t* __restrict__ offsets,
     GsDecision* __restrict__ out, int64_t out_cap, int32_t* __restrict__ owner, int* __restrict__ gerr) {
-  extern __shared__ __align__(16) uint8_t smx[];
-  uint8_t (*til)[kMaxTilings][8] = reinterpret_cast<uint8_t (*)[kMaxTilings][8]>(smx);
+  __shared__ __align__(16) uint8_t til[kWriteWarps][kTilChunk][8];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t nwarps = (int64_t)gridDim.x * kExpandWarps;
-  for (int64_t p = (int64_t)blockIdx.x * kExpandWarps + wib; p < n; p += nwarps) {
+  const int64_t nwarps = (int64_t)gridDim.x * kWriteWarps;
+  for (int64_t p = (int64_t)blockIdx.x * kWriteWarps + wib; p < n; p += nwarps) {
     const int64_t base = offsets[p], cnt = offsets[p + 1] - base;
     if (cnt <= 0 || cnt > kMaxTilings) continue;
     if (base + cnt > out_cap) {   // the caller's buffer is smaller than the step: write nothing past it
@@ -117,31 +129,41 @@ __global__ void __launch_bounds__(kExpandWarps * 32) expand_write_kernel(
     }
     const int s = step[p];
     const GsDecision* par = parents + p * S;
-    if (lane == 0) {
-      int k = 0;
-      enum_tilings(m, funcs[par[s].func], [&](const int* sv, const int* tv) {
-        for (int d = 0; d < GS_MAX_NDIM; ++d) { til[wib][k][d] = (uint8_t)sv[d]; til[wib][k][4 + d] = (uint8_t)tv[d]; }
-        ++k;
-      });
-    }
-    __syncwarp();
+    const GsFunc& fn = funcs[par[s].func];
+    const int nd = fn.ndim;
     const uint4* src = reinterpret_cast<const uint4*>(par);
-    const int nd = funcs[par[s].func].ndim;
-    for (int64_t t = 0; t < cnt; ++t) {
-      uint4* dst = reinterpret_cast<uint4*>(out + (base + t) * S);
-      for (int i = lane; i < S; i += 32) {
+    for (int64_t k0 = 0; k0 < cnt; k0 += kTilChunk) {
+      const int nt = (int)(cnt - k0 < kTilChunk ? cnt - k0 : kTilChunk);
+      __syncwarp();
+      if (lane == 0) {
+        int64_t k = 0;
+        enum_tilings(m, fn, [&](const int* sv, const int* tv) {
+          if (k >= k0 && k < k0 + kTilChunk) {
+            uint8_t* e = til[wib][k - k0];
+            for (int d = 0; d < GS_MAX_NDIM; ++d) { e[d] = (uint8_t)sv[d]; e[4 + d] = (uint8_t)tv[d]; }
+          }
+          ++k;
+        });
+      }
+      __syncwarp();
+      uint4* dst = reinterpret_cast<uint4*>(out + (base + k0) * S);
+      const int64_t total = (int64_t)nt * S;
+      int t = lane / S, i = lane - t * S;   // (tiling, record) of flattened element j = lane
+      for (int64_t j = lane; j < total; j += 32) {
         uint4 r = __ldg(src + i);
         if (i == s) {
           GsDecision d = *reinterpret_cast<const GsDecision*>(&r);
           d.flags = 3;
-          for (int k = 0; k < nd; ++k) { d.serial[k] = til[wib][t][k]; d.thread[k] = til[wib][t][4 + k]; }
+          for (int q = 0; q < nd; ++q) { d.serial[q] = til[wib][t][q]; d.thread[q] = til[wib][t][4 + q]; }
           r = *reinterpret_cast<const uint4*>(&d);
         }
-        dst[i] = r;
+        dst[j] = r;
+        i += 32;
+        while (i >= S) { i -= S; ++t; }
       }
-      if (owner && lane == 0) owner[base + t] = (int32_t)p;
+      if (owner)
+        for (int q = lane; q < nt; q += 32) owner[base + k0 + q] = (int32_t)p;
     }
-    __syncwarp();
   }
 }
 
@@ -485,12 +507,10 @@ int launch_expand(const GsFunc* funcs, const GsDecision* parents, int64_t n, int
   expand_offsets_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(incl, n, offsets);
   g_launch_count += 2;
   if (out) {
-    const int64_t want = (n + kExpandWarps - 1) / kExpandWarps;
-    const int grid = (int)(want < (int64_t)num_sms * 16 ? want : (int64_t)num_sms * 16);
-    const int smem = kExpandWarps * kMaxTilings * 8;
-    cudaFuncSetAttribute(expand_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    expand_write_kernel<<<grid, kExpandWarps * 32, smem, st>>>(funcs, parents, n, S, step, m, offsets, out, out_cap,
-                                                               owner, gerr);
+    const int64_t want = (n + kWriteWarps - 1) / kWriteWarps;
+    const int grid = (int)(want < (int64_t)num_sms * 8 ? want : (int64_t)num_sms * 8);
+    expand_write_kernel<<<grid, kWriteWarps * 32, 0, st>>>(funcs, parents, n, S, step, m, offsets, out, out_cap,
+                                                           owner, gerr);
     g_launch_count++;
   }
   return 0;
