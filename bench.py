@@ -222,6 +222,12 @@ class Clocks:
             self.proc = None
         return self
 
+    def wait_first(self, timeout=3.0):
+        """Block until nvidia-smi has produced its first sample."""
+        t0 = time.time()
+        while self.proc and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
@@ -337,6 +343,11 @@ def run_gpu(args):
     def step(d, timed=False):
         return plan.run(d, times=phase_ms if timed else None)
 
+    # the clock sampler starts before the warm-up: nvidia-smi's own start-up
+    # (driver / NVML initialisation) landed inside the timed region and, at
+    # the step's one host read-back, showed up as sporadic 10-400 ms steps
+    clk = Clocks(local).__enter__()
+    clk.wait_first()
     for _ in range(args.warmup):
         step(dec)
     sc.check()
@@ -349,17 +360,19 @@ def run_gpu(args):
     import gc
     gc.collect()
     gc.disable()   # no collector pauses between the step's kernel launches
-    with Clocks(local) as clk:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            res = step(dec, timed=True)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    n_pre = len(clk.rows)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        res = step(dec, timed=True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk.__exit__(None, None, None)
+    clk.rows = clk.rows[max(0, n_pre - 1):]   # the samples taken during the timed region (+ the one before)
     gc.enable()
     launches = lib.gs_launch_count() - l0
     ms = ev0.elapsed_time(ev1) / args.steps

@@ -521,8 +521,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) cost_rows_mma_kernel(
     __syncwarp();
   };
 
-  constexpr int kBatch = 8;   // 16 row_src / n_rows loads in flight per lane while the queue fills
-  static_assert(kRingM >= 31 + 32 * kBatch, "");
+  // queue fill: each lane takes 4 consecutive rows per group (one 16-byte
+  // row_src load when aligned; n_rows once per candidate it touches), three
+  // 128-row groups per step
+  constexpr int kV = 3;
+  static_assert(kRingM >= 31 + 128 * kV, "");
+  const bool vec = ((uintptr_t)row_src & 15) == 0;
   auto claim = [&]() -> int64_t {
     unsigned v = 0;
     if (lane == 0) v = atomicAdd(work, 1u);
@@ -533,24 +537,46 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) cost_rows_mma_kernel(
   for (;;) {
     while (tail - head < 32 && s0 < total_rows) {
       const int64_t end = sp * kSpan + kSpan < total_rows ? sp * kSpan + kSpan : total_rows;
-      unsigned tm = 0;
+      unsigned tm = 0;   // bit 4u + e: row s0 + 128u + 4 lane + e is computed
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        const int64_t row = s0 + 32 * u + lane;
-        if (row < end) {
-          const uint32_t c = (uint32_t)row / (uint32_t)R;   // rows < 2^32 on this path
-          const int r = (int)((uint32_t)row - c * (uint32_t)R);
-          tm |= (unsigned)(r < __ldg(n_rows + c) && __ldg(row_src + row) == (int32_t)c) << u;
+      for (int u = 0; u < kV; ++u) {
+        const int64_t r0 = s0 + 128 * u + 4 * lane;
+        if (r0 < end) {
+          int v[4];
+          if (vec && r0 + 3 < end) {
+            const int4 w = __ldg(reinterpret_cast<const int4*>(row_src + r0));
+            v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = r0 + e < end ? __ldg(row_src + r0 + e) : -1;
+          }
+          const uint32_t c0 = (uint32_t)r0 / (uint32_t)R;   // rows < 2^32 on this path
+          int r = (int)((uint32_t)r0 - c0 * (uint32_t)R);
+          uint32_t c = c0;
+          int nr = __ldg(n_rows + c0);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (e > 0 && ++r >= R) { r = 0; ++c; nr = r0 + e < end ? __ldg(n_rows + c) : 0; }
+            tm |= (unsigned)(r < nr && v[e] == (int32_t)c) << (4 * u + e);
+          }
         }
       }
 #pragma unroll 1
-      for (int u = 0; u < kBatch; ++u) {
-        const bool t = (tm >> u) & 1u;
-        const unsigned b = __ballot_sync(0xffffffffu, t);
-        if (t) q[(tail + __popc(b & ((1u << lane) - 1))) & (kRingM - 1)] = (uint32_t)(s0 + 32 * u + lane);
-        tail += __popc(b);
+      for (int u = 0; u < kV; ++u) {
+        const unsigned mine = (tm >> (4 * u)) & 15u;
+        const int cntl = __popc(mine);
+        int incl = cntl;   // inclusive prefix of the lanes' counts: rows stay in order
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        unsigned pos = tail + (unsigned)(incl - cntl);
+        for (int e = 0; e < 4; ++e)
+          if ((mine >> e) & 1u) q[(pos++) & (kRingM - 1)] = (uint32_t)(s0 + 128 * u + 4 * lane + e);
+        tail += (unsigned)__shfl_sync(0xffffffffu, incl, 31);
       }
-      s0 += 32 * kBatch;
+      s0 += 128 * kV;
       if (s0 >= end) { sp = claim(); s0 = sp * kSpan; }
     }
     if (tail == head) break;
