@@ -324,9 +324,9 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 1) cost_rows_kernel(NetDev ne
 // X[r][4kb+j]); C fragments are turned into the next layer's A fragments
 // with quad shuffles.  The pre-softplus outputs go through a per-warp
 // shared-memory tile so that the row's owner lane does softplus + the basis
-// dot exactly as the scalar path does.  Accumulation order inside an MMA
-// differs from the scalar FMA chains: costs agree with the reference to
-// ~1e-15 relative (tolerance 1e-9, tests/test_gpu_parity.py).
+// dot exactly as the scalar path does.  The MMAs accumulate in the scalar
+// chains' order (bias, then k ascending, FMA rounding per step): costs are
+// bit-identical to cost_kernel's (tests/test_gpu_reuse.py asserts equality).
 #ifndef GS_K2M_WARPS
 #define GS_K2M_WARPS 16
 #endif
