@@ -2281,16 +2281,31 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
   constexpr int kFine = kChunk2 / 4 > 0 ? kChunk2 / 4 : 1;
   const int64_t nchunks = nbig + (n - nbig * kChunk2 + kFine - 1) / kFine;
   // warp state <-> run slot: the shared-memory slice and the global scratch
+  // copy n int4 from src to dst with eight loads in flight per lane before
+  // their stores (a load-store-load loop waited one HBM round trip per
+  // 512 bytes: ~36 of them to restore a slot)
+  auto copy16 = [&](int4* __restrict__ dst, const int4* __restrict__ src, int n) {
+    constexpr int U = 8;
+    int i = lane;
+    for (; i + 32 * (U - 1) < n; i += 32 * U) {
+      int4 t[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) t[u] = src[i + 32 * u];
+#pragma unroll
+      for (int u = 0; u < U; ++u) dst[i + 32 * u] = t[u];
+    }
+    for (; i < n; i += 32) dst[i] = src[i];
+  };
   auto slot_copy = [&](int64_t r, bool save) {
     uint8_t* sl = slots + r * slot_bytes;
     int4* a = reinterpret_cast<int4*>(sl);
     int4* b = reinterpret_cast<int4*>(ws);
     const int nw1 = L.keep / 16;
-    for (int i = lane; i < nw1; i += 32) { if (save) a[i] = b[i]; else b[i] = a[i]; }
     int4* a2 = reinterpret_cast<int4*>(sl + L.keep);
     int4* b2 = reinterpret_cast<int4*>(wgs);
     const int nw2 = L.gkeep / 16;
-    for (int i = lane; i < nw2; i += 32) { if (save) a2[i] = b2[i]; else b2[i] = a2[i]; }
+    if (save) { copy16(a, b, nw1); copy16(a2, b2, nw2); }
+    else { copy16(b, a, nw1); copy16(b2, a2, nw2); }
     __syncwarp();
   };
   bulk_wait(&bar);
@@ -2307,7 +2322,20 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     {
       const uint4* src = reinterpret_cast<const uint4*>(dec + c * S);
       uint4* dst = reinterpret_cast<uint4*>(k.dec);
-      for (int i = lane; i < S; i += 32) dst[i] = __ldg(src + i);   // 128-bit loads
+      // 128-bit loads, four in flight per lane before the stores
+      for (int i0 = 0; i0 < S; i0 += 128) {
+        uint4 t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + 32 * u + lane;
+          if (i < S) t[u] = __ldg(src + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + 32 * u + lane;
+          if (i < S) dst[i] = t[u];
+        }
+      }
       if (lane < k.mw) k.cmask[lane] = 0u;
       __syncwarp();
       unsigned cnt = 0, diff = 0;
