@@ -329,6 +329,27 @@ class Scorer:
         return pos, cnt, bot
 
 
+    def beam_topk_reps(self, total, pass_hash, rep, n_max, cnt, flagged, penalty, temperature, phase_seed, k,
+                       tie_band=TIE_BAND):
+        """K5 over K4's representatives without a host round trip
+        (gs_beam_topk_reps): costs and pass hashes are the per-candidate
+        arrays, `rep` the representative list and cnt[0] its device-side
+        length.  Returns (positions into `rep` in cut order, count (device),
+        bottom-half flags over the representative positions)."""
+        wsb = self.lib.gs_topk_workspace_bytes(n_max)
+        ws = torch.empty((wsb,), dtype=torch.uint8, device=self.device)
+        pos = torch.empty((max(1, k),), dtype=torch.int64, device=self.device)
+        kcnt = torch.zeros((1,), dtype=torch.int64, device=self.device)
+        bot = torch.zeros((max(1, n_max),), dtype=torch.uint8, device=self.device)
+        fl = flagged if flagged is not None and flagged.numel() else None
+        _lib.check(self.lib.gs_beam_topk_reps(_ptr(total), _ptr(pass_hash), _ptr(rep), n_max,
+                                              C.c_void_p(cnt.data_ptr()), _ptr(fl),
+                                              0 if fl is None else fl.numel(), float(penalty), float(temperature),
+                                              C.c_uint64(phase_seed & 0xFFFFFFFFFFFFFFFF), k, float(tie_band),
+                                              _ptr(ws), wsb, _ptr(pos), _ptr(kcnt), _ptr(bot), _stream()))
+        return pos, kcnt, bot
+
+
 def u64_sorted_tensor(values, device) -> torch.Tensor:
     """Sorted uint64 values as an int64 tensor holding the same bits."""
     arr = np.array(sorted(int(v) & 0xFFFFFFFFFFFFFFFF for v in values), dtype=np.uint64)

@@ -147,36 +147,60 @@ class StepPlan:
             rej = torch.nonzero(~valid).flatten() if rejects else None
             nrep_t = torch.tensor(rep.numel(), device=sc.device)
             nrej_t = torch.tensor(0 if rej is None else rej.numel(), device=sc.device)
-        nrep = int(nrep_t.item())
-        rep = rep[:nrep]
-        costs = total.index_select(0, rep)
-        ph = hl.index_select(0, rep)
-        cand = rep if mine is None else mine.index_select(0, rep)
-        mark()
         fl = flagged_tensor(flagged, sc.device)
-        if self.world > 1:
-            from . import exchange
-            beam, beam_costs, bot_local, n_global = exchange.sharded_cut(
-                sc, costs, ph, cand, fl, self.penalty, temperature, self.phase_seed, self.beam,
-                self.tie_band, self.world, self.group)
-            self.last_exchange_bytes = exchange.LAST_BYTES
-            n_all = n_global
-            bot = bot_local
-            mem_src = cand
-        else:
-            n_all = int(costs.shape[0])
+        if self.world == 1 and self.sampling and hl.shape[0] > 0:
+            # one rank: K5 reads the representative count K4 left on the
+            # device (gs_beam_topk_reps), so the GPU goes from K4 to K5
+            # without waiting for the host; the count is read once K5 is queued
+            mark()
+            n_loc = int(hl.shape[0])
+            pos, kcnt, bot = sc.beam_topk_reps(total, hl, rep, n_loc, cnt, fl, self.penalty, temperature,
+                                               self.phase_seed, max(1, min(self.beam, n_loc)),
+                                               tie_band=self.tie_band)
+            nrep = int(nrep_t.item())
+            rep = rep[:nrep]
+            cand = rep
+            n_all = nrep
             if n_all:
-                pos, kcnt, bot = sc.beam_topk(costs, ph, fl, self.penalty, temperature, self.phase_seed,
-                                              min(self.beam, n_all), tie_band=self.tie_band)
                 kk = int(kcnt.item())
                 if kk < 0:
                     raise GsError("beam_topk: a tie group is wider than the cut window")
-                beam = cand.index_select(0, pos[:kk])
-                beam_costs = costs.index_select(0, pos[:kk])
+                beam = rep.index_select(0, pos[:kk])
+                beam_costs = total.index_select(0, beam)
             else:
-                beam = cand[:0]
-                beam_costs = costs[:0]
+                beam = rep[:0]
+                beam_costs = total[:0]
                 bot = None
+            mem_src = cand
+        else:
+            nrep = int(nrep_t.item())
+            rep = rep[:nrep]
+            costs = total.index_select(0, rep)
+            ph = hl.index_select(0, rep)
+            cand = rep if mine is None else mine.index_select(0, rep)
+            mark()
+            if self.world > 1:
+                from . import exchange
+                beam, beam_costs, bot_local, n_global = exchange.sharded_cut(
+                    sc, costs, ph, cand, fl, self.penalty, temperature, self.phase_seed, self.beam,
+                    self.tie_band, self.world, self.group)
+                self.last_exchange_bytes = exchange.LAST_BYTES
+                n_all = n_global
+                bot = bot_local
+            else:
+                n_all = int(costs.shape[0])
+                if n_all:
+                    pos, kcnt, bot = sc.beam_topk(costs, ph, fl, self.penalty, temperature, self.phase_seed,
+                                                  min(self.beam, n_all), tie_band=self.tie_band)
+                    kk = int(kcnt.item())
+                    if kk < 0:
+                        raise GsError("beam_topk: a tie group is wider than the cut window")
+                    beam = cand.index_select(0, pos[:kk])
+                    beam_costs = costs.index_select(0, pos[:kk])
+                else:
+                    beam = cand[:0]
+                    beam_costs = costs[:0]
+                    bot = None
             mem_src = cand
         mark()
         # bad-hash memo (search.py:196-200): hashes of the bottom half at
