@@ -2322,20 +2322,7 @@ featurize_kernel(const PipeDev* __restrict__ P, const uint8_t* __restrict__ blob
     {
       const uint4* src = reinterpret_cast<const uint4*>(dec + c * S);
       uint4* dst = reinterpret_cast<uint4*>(k.dec);
-      // 128-bit loads, four in flight per lane before the stores
-      for (int i0 = 0; i0 < S; i0 += 128) {
-        uint4 t[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = i0 + 32 * u + lane;
-          if (i < S) t[u] = __ldg(src + i);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = i0 + 32 * u + lane;
-          if (i < S) dst[i] = t[u];
-        }
-      }
+      for (int i = lane; i < S; i += 32) dst[i] = __ldg(src + i);   // 128-bit loads
       if (lane < k.mw) k.cmask[lane] = 0u;
       __syncwarp();
       unsigned cnt = 0, diff = 0;
