@@ -184,6 +184,15 @@ int gs_cost(gs_pipeline_t p, const double* feats, const int32_t* row_key,
             const int32_t* n_rows, const int32_t* row_src, int64_t n,
             double* total, double* row_cost, double* basis_gh, void* stream);
 
+/* K2 totals only, with row reuse (the beam step's cut needs no per-row
+ * costs): as gs_cost with row_src, but row_scratch ([N][R]) ends up
+ * holding only the computed rows' costs — the other rows' costs are not
+ * written back (770 MB per 1M-candidate C5 step).  Same totals, bit for
+ * bit.  Replaces CostEvaluator.cost (search.py:115-124) for a batch. */
+int gs_cost_totals(gs_pipeline_t p, const double* feats, const int32_t* row_key,
+                   const int32_t* n_rows, const int32_t* row_src, int64_t n,
+                   double* total, double* row_scratch, void* stream);
+
 /* K3: blake2b-64 structural hash at `depth` (loopnest.py:131-165).  A
  * candidate whose (func, kind, consumer, serial/thread presence) fields
  * equal its predecessor's takes the predecessor's hash (equal canonical

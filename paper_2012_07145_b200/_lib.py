@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GS_LIB_PATH") or os.path.join(HERE, "libgs_sched.so")   # override: diagnostics builds
 
 EXPORTS = ("gs_last_error", "gs_version", "gs_launch_count", "gs_pipeline_create", "gs_pipeline_destroy",
-           "gs_pipeline_max_rows", "gs_set_weights", "gs_set_reuse", "gs_featurize", "gs_cost",
+           "gs_pipeline_max_rows", "gs_set_weights", "gs_set_reuse", "gs_featurize", "gs_cost", "gs_cost_totals",
            "gs_struct_hash", "gs_select_workspace_bytes", "gs_select_reps",
            "gs_topk_workspace_bytes", "gs_beam_topk", "gs_check", "gs_stats", "gs_debug_phases",
            "gs_expand_workspace_bytes", "gs_expand_step", "gs_simulate", "gs_featurize_workspace_bytes",
@@ -54,6 +54,7 @@ def load(path: str = LIB_PATH):
         "gs_get_reuse": (i32, [P]),
         "gs_featurize": (i32, [P, V, i64, i32, V, V, V, V, V, V]),
         "gs_cost": (i32, [P, V, V, V, V, i64, V, V, V, V]),
+        "gs_cost_totals": (i32, [P, V, V, V, V, i64, V, V, V]),
         "gs_struct_hash": (i32, [P, V, i64, i32, i32, V, V]),
         "gs_select_workspace_bytes": (i64, [i64]),
         "gs_select_reps": (i32, [V, V, i64, u64, V, i64, V, V, V, V, V]),

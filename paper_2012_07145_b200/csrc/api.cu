@@ -28,7 +28,7 @@ int read_phases(long long* out);
 int launch_hoist(const NetDev& net, const double* algo, int n_stages, cudaStream_t st);
 int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
                 const int32_t* n_rows, const int32_t* row_src, int64_t n, int R, double* total, double* row_cost,
-                double* basis_gh, unsigned* work, int num_sms, cudaStream_t st);
+                double* basis_gh, unsigned* work, int num_sms, cudaStream_t st, bool rows_out = true);
 int launch_hash(const GsDecision* dec, int64_t n, int S, int nf, HashDepths D, const int32_t* sorted_funcs,
                 const uint8_t* names, const int32_t* name_off, uint64_t* out, uint8_t* head, int repr_bound,
                 int num_sms, cudaStream_t st);
@@ -543,6 +543,19 @@ int gs_cost(gs_pipeline_t p, const double* feats, const int32_t* row_key, const 
   int rc = launch_cost(p->net, p->stage_of_func, feats, row_key, n_rows, row_src, n, std::max(1, p->host.max_rows),
                        total, row_cost, basis_gh, reinterpret_cast<unsigned*>(p->err + 15), p->num_sms,
                        (cudaStream_t)stream);
+  if (rc) return fail(GS_ERR_ARG, "unsupported network dims");
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
+int gs_cost_totals(gs_pipeline_t p, const double* feats, const int32_t* row_key, const int32_t* n_rows,
+                   const int32_t* row_src, int64_t n, double* total, double* row_scratch, void* stream) {
+  GS_NVTX("gs_cost_totals");
+  if (!p || !p->net.sched_w) return fail(GS_ERR_ARG, "weights not set (gs_set_weights)");
+  if (n > 0 && (!row_src || !row_scratch)) return fail(GS_ERR_ARG, "gs_cost_totals needs row_src and the row scratch");
+  int rc = launch_cost(p->net, p->stage_of_func, feats, row_key, n_rows, row_src, n, std::max(1, p->host.max_rows),
+                       total, row_scratch, nullptr, reinterpret_cast<unsigned*>(p->err + 15), p->num_sms,
+                       (cudaStream_t)stream, false);
   if (rc) return fail(GS_ERR_ARG, "unsupported network dims");
   CK(cudaGetLastError());
   return GS_OK;

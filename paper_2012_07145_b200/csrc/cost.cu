@@ -635,7 +635,7 @@ int cost_smem_bytes(int E, int H, int CB, int R) {
 
 int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* feats, const int32_t* row_key,
                 const int32_t* n_rows, const int32_t* row_src, int64_t n, int R, double* total, double* row_cost,
-                double* basis_gh, unsigned* work, int num_sms, cudaStream_t st) {
+                double* basis_gh, unsigned* work, int num_sms, cudaStream_t st, bool rows_out) {
   if (n == 0) return 0;
   if (row_src && row_cost && !basis_gh) {
     if (n * (int64_t)R / 128 >= 0xFFFFFFFFll) return -1;
@@ -676,7 +676,8 @@ int launch_cost(const NetDev& net, const int32_t* stage_of_func, const double* f
     const int64_t blocks = (n + CB - 1) / CB;
     const int gridB = (int)(blocks < (int64_t)num_sms * 16 ? blocks : (int64_t)num_sms * 16);
     cudaFuncSetAttribute(stage_sum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smB);
-    stage_sum_kernel<<<gridB, 128, smB, st>>>(n_rows, row_src, row_cost, n, R, CB, total, row_cost);
+    stage_sum_kernel<<<gridB, 128, smB, st>>>(n_rows, row_src, row_cost, n, R, CB, total,
+                                              rows_out ? row_cost : nullptr);
     g_launch_count++;
     return 0;
   }

@@ -169,6 +169,12 @@ class Scorer:
             rc = scratch if scratch is not None else torch.empty((n, self.R), dtype=torch.float64,
                                                                  device=self.device)
         gh = torch.empty((n, self.R, 31), dtype=torch.float64, device=self.device) if basis else None
+        if src is not None and not rows and not basis:
+            # totals only: the non-computed rows' costs are not written back
+            _lib.check(self.lib.gs_cost_totals(self.handle, _ptr(f["feats"]), _ptr(f["row_key"]),
+                                               _ptr(f["n_rows"]), _ptr(src), n, _ptr(total), _ptr(rc),
+                                               _stream()))
+            return total, None, None
         _lib.check(self.lib.gs_cost(self.handle, _ptr(f["feats"]), _ptr(f["row_key"]), _ptr(f["n_rows"]),
                                     _ptr(src), n, _ptr(total), _ptr(rc), _ptr(gh), _stream()))
         return total, (rc if rows else None), gh
